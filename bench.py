@@ -1,0 +1,404 @@
+"""Benchmark: ensemble sample-solves/s of one adaptive level (BASELINE.json metric).
+
+One *step* = the hot path over one level's batch of samples: device stable
+sort of the surrogate keys + chunking into width-S groups, KL coefficient at
+every node, sample-interleaved assembly of every group's operator, batched
+Jacobi-PCG of all groups to their own termination, per-lane QoI.  The
+workload (default C2: n=256, M=4, S=16, rtol 1e-8, adaptive grid to total
+level 5) is the last adaptive level of the study: levels 1..L-1 are solved in
+the untimed setup to fit the iteration surrogate that keys the final level.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+N>1 (torchrun): weak scaling - rank r solves the final level's sample set
+reflected through the sign pattern of r's bits (same grid, same shape of
+work, distinct samples), no collective on the solve path; the step time is
+the max over ranks.  Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+WORKLOADS = ROOT / "bench_workloads"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# workload
+
+def bytes_model(cfg):
+    """Algorithmic bytes per group per launch (DESIGN.md / SURVEY.md 8d)."""
+    S, N, nnz = cfg.ensemble_size, cfg.n_dofs, cfg.nnz
+    spmv = 8 * S * nnz + 4 * nnz + 4 * (N + 1) + 16 * S * N
+    update = 7 * 8 * S * N
+    direction = 4 * 8 * S * N
+    return {"spmv": spmv, "update": update, "dir": direction,
+            "pcg_iter": 8 * S * (nnz + 13 * N) + 4 * (nnz + N + 1)}
+
+
+def make_workload(cfg, solver=None):
+    """(ids, coords (n,M), keys (n,) or None) of the final adaptive level."""
+    path = WORKLOADS / f"{cfg.name}.npz"
+    if path.exists():
+        z = np.load(path)
+        keys = z["keys"] if z["keys"].size else None
+        return z["ids"].tolist(), z["coords"], keys, json.loads(str(z["meta"]))
+    from paper_1705_02003_b200.driver import ITER, QOI, adaptive_run, sample_set
+    if cfg.synthetic_samples:
+        coords = sample_set(cfg)
+        ids, keys, meta = list(range(len(coords))), None, {"source": "seeded U[-1,1]^M, rng 0"}
+    else:
+        t0 = time.time()
+        records, stop, grid = adaptive_run(cfg, solver, max_levels=cfg.max_levels - 1)
+        new, _ = grid.refine(cfg.tau, QOI, cfg.n_max)
+        start = len(grid) - len(new)
+        ids = list(range(start, len(grid)))
+        coords = grid.node_coords()[start:]
+        keys = grid.evaluate(ITER, coords, n_nodes=start)
+        meta = {"source": f"adaptive levels 1..{len(records)} solved on device "
+                          f"({[len(r.ids) for r in records]} samples, {time.time() - t0:.1f}s); "
+                          f"final level {len(records) + 1}",
+                "prior_levels": [len(r.ids) for r in records]}
+    WORKLOADS.mkdir(exist_ok=True)
+    np.savez(path, ids=np.array(ids), coords=coords,
+             keys=np.array([]) if keys is None else keys, meta=json.dumps(meta))
+    return ids, coords, keys, meta
+
+
+def reflect(coords, rank):
+    """Rank-specific reflection y_d -> -y_d for the set bits of rank (weak scaling)."""
+    if rank == 0:
+        return coords
+    signs = np.array([-1.0 if (rank >> d) & 1 else 1.0 for d in range(coords.shape[1])])
+    return coords * signs
+
+
+# ---------------------------------------------------------------------------
+# clocks
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.proc, self.lines = index, None, []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.index)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle = the reference algorithm restated; test infra, used here
+# only as the timed CPU baseline)
+
+def _cpu_group_worker(args):
+    cfg_name, samples = args
+    from threadpoolctl import threadpool_limits
+
+    from oracle import fv2d as ofv, field2d, pcg as opcg
+    from paper_1705_02003_b200.configs import get
+
+    cfg = get(cfg_name)
+    with threadpool_limits(limits=1):
+        fld = field2d.KL2D.select(**cfg.field_kwargs())
+        mesh = ofv.Mesh2D(cfg.cells)
+        table = fld.mode_table(mesh.node_points)
+        t0 = time.perf_counter()
+        sysm = ofv.assemble(mesh, fld, samples, table, cfg.a2)
+        res = opcg.pcg(sysm.row_offsets, sysm.col_indices, sysm.values, sysm.rhs, tol=cfg.tol,
+                       maxit=cfg.maxit)
+        q = [ofv.qoi(u) for u in res.solution]
+        return time.perf_counter() - t0, res.ensemble_iterations, q
+
+
+def cpu_plan(cfg, coords, keys):
+    from oracle import grouping as ogrp
+    ids = list(range(len(coords)))
+    if keys is None:
+        return ogrp.natural(ids, cfg.ensemble_size)[0]
+    return ogrp.by_key(ids, dict(zip(ids, keys)), cfg.ensemble_size)[0]
+
+
+def cpu_baseline(cfg, coords, keys):
+    """Oracle port, 1 thread, one median-cost group of the same level."""
+    ens = cpu_plan(cfg, coords, keys)
+    g = ens[len(ens) // 2]
+    dt, its, _ = _cpu_group_worker((cfg.name, coords[list(g)]))
+    S = cfg.ensemble_size
+    return {"value": S / dt, "unit": "sample-solves/s", "cores": 1, "kind": "port",
+            "sample": f"1 group (S={S}) of the {cfg.name} final level (group {len(ens) // 2} of "
+                      f"{len(ens)} in surrogate order): 2D KL + assembly + Jacobi-PCG "
+                      f"({its} iterations) + QoI, oracle/ numpy+scipy, 1 thread, {dt:.1f}s"}
+
+
+def run_reference(args, cfg):
+    """--impl reference: the CPU path on all host cores (multiprocessing, 1 thread each)."""
+    import multiprocessing as mproc
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    ids, coords, keys, meta = make_workload(cfg)
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    ens = cpu_plan(cfg, coords, keys)
+    t_group = time.perf_counter() - t0
+    P = max(1, min(cores, len(ens)))
+    steps = max(1, min(args.steps, 3))
+    times, done = [], 0
+    ctx = mproc.get_context("spawn")
+    with ctx.Pool(P) as pool:
+        for st in range(steps):
+            chosen = [ens[(st * P + j) % len(ens)] for j in range(P)]
+            t0 = time.perf_counter()
+            out = pool.map(_cpu_group_worker, [(cfg.name, coords[list(g)]) for g in chosen])
+            times.append(time.perf_counter() - t0 + t_group)
+            done += P * cfg.ensemble_size
+    total = sum(times)
+    value = done / total
+    S = cfg.ensemble_size
+    line = {
+        "impl": "reference", "metric": "ensemble sample-solves/s", "value": value,
+        "unit": "sample-solves/s", "n_gpus": args.gpus, "steps": steps, "warmup": 0,
+        "ms_per_step": 1e3 * total / steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name} final adaptive level, {P} groups per step",
+                   "n": cfg.cells, "M": cfg.n_modes, "S": S, "rtol": cfg.tol},
+        "cpu_baseline": {"value": value, "unit": "sample-solves/s", "cores": P, "kind": "port",
+                         "sample": f"{P} groups x S={S} per step (one group per process, "
+                                   "1 BLAS thread each) of the final level; oracle/ restatement "
+                                   "of uqgroup's path (reference is pure Python; its 2D operator "
+                                   "does not exist, see DESIGN.md)"},
+        "e2e": {"value": value, "unit": "sample-solves/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+def main():
+    args = parse()
+    from paper_1705_02003_b200.configs import get
+    cfg = get(args.config)
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_1705_02003_b200 as uq
+    from paper_1705_02003_b200 import _lib
+    from paper_1705_02003_b200.build import needs_build, build
+
+    if needs_build():
+        build()
+    field = uq.build_field(**cfg.field_kwargs())
+    solver = uq.EnsembleSolver2D(field, cfg.cells, cfg.tol, cfg.maxit, cfg.a2)
+    ids, coords, keys, meta = make_workload(cfg, solver)
+    # weak scaling: rank r solves the mirror images of the level's samples and
+    # groups them by the keys of their originals (same sort work, same costs shape)
+    coords = reflect(coords, rank)
+    n, S = len(ids), cfg.ensemble_size
+    dev = _lib.device()
+    d_coords = torch.from_numpy(np.ascontiguousarray(coords)).to(dev)
+    d_keys = None if keys is None else torch.from_numpy(np.ascontiguousarray(keys)).to(dev)
+    lib, ctx = _lib.load(), _lib.ctx()
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step():
+        return solver.run_level_device(d_coords, n, S, d_keys)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    import ctypes
+    NK = 10
+    ms = (ctypes.c_double * NK)()
+    cnt = (ctypes.c_longlong * NK)()
+    lib.uqg_ctx_profile_read(ctx, ms, cnt, 1)
+    lib.uqg_ctx_profile(ctx, 1)
+    launches0 = lib.uqg_ctx_launch_count(ctx)
+    times, group_iters, n_groups = [], 0, 0
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        for _ in range(args.steps):
+            barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            groups, pad, it, cv, en, q = step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1)
+            if world > 1:
+                tt = torch.tensor([t], device=dev)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                t = float(tt.item())
+            times.append(t)
+            group_iters += int(en.sum().item())
+            n_groups = pad.numel()
+            barrier()
+    launches = lib.uqg_ctx_launch_count(ctx) - launches0
+    lib.uqg_ctx_profile_read(ctx, ms, cnt, 1)
+    lib.uqg_ctx_profile(ctx, 0)
+    conv_all = bool(cv.all().item())
+
+    # ---- end to end through the public API: host inputs, host results -------
+    e2e_steps = args.e2e_steps or args.steps
+    e2e_t = []
+    for _ in range(e2e_steps):
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        plan, iters, qois, notes = solver.solve_level(ids, coords, S, keys=keys, level=99)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([dt], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt = float(tt.item())
+        e2e_t.append(dt)
+    K = len(plan.ensembles)
+    h2d = coords.nbytes + (0 if keys is None else 8 * n)
+    d2h = 8 * (K * S * 4 + K)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    total_ms = sum(times)
+    value = world * n * len(times) / (total_ms / 1e3)
+    bm = bytes_model(cfg)
+    peaks = {}
+    pk = ROOT / "MEASURED_PEAKS.json"
+    if pk.exists():
+        peaks = json.loads(pk.read_text())
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    spmv_ms = ms[3]
+    spmv_gbs = group_iters * bm["spmv"] / (spmv_ms / 1e3) / 1e9 if spmv_ms else None
+    loop_ms = ms[3] + ms[4] + ms[5]
+    loop_gbs = group_iters * bm["pcg_iter"] / (loop_ms / 1e3) / 1e9 if loop_ms else None
+    step_gbs = group_iters * bm["pcg_iter"] / (total_ms / 1e3) / 1e9
+    kern = {name: {"ms": ms[k], "launches": int(cnt[k])} for k, name in enumerate(
+        ["kl", "assemble", "pcg_init", "pcg_spmv", "pcg_update", "pcg_dir", "dot_qoi", "group",
+         "spmv", "other"]) if cnt[k]}
+    line = {
+        "metric": "ensemble sample-solves/s",
+        "value": value,
+        "unit": "sample-solves/s",
+        "n_gpus": world,
+        "steps": len(times),
+        "warmup": max(3, args.warmup),
+        "ms_per_step": total_ms / len(times),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: final adaptive level ({n} samples/rank, {K} groups "
+                               f"of S={S}) - group sort + KL + assembly + batched Jacobi-PCG + QoI",
+                   "n": cfg.cells, "unknowns": cfg.n_dofs, "M": cfg.n_modes, "S": S,
+                   "rtol": cfg.tol, "delta": cfg.delta, "sigma": cfg.sigma0,
+                   "parallelism": f"groups sharded weak x{world}",
+                   "l2": "inputs larger than L2 (operator+vectors of all groups ~"
+                         f"{solver.bytes_per_group(S) * K / 1e9:.1f} GB per step)",
+                   "workload_source": meta.get("source")},
+        "gpu_launches": int(launches),
+        "e2e": {"value": world * n * len(e2e_t) / sum(e2e_t), "unit": "sample-solves/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "roofline": {"bound": "hbm", "kernel": "pcg_spmv_kernel",
+                     "achieved": spmv_gbs, "peak": peak, "unit": "GB/s",
+                     "frac": (spmv_gbs / peak) if spmv_gbs else None, "traffic": None,
+                     "peak_source": peak_src,
+                     "bytes_per_group_launch": bm["spmv"],
+                     "group_launches": group_iters},
+        "pcg_loop": {"achieved_gbs": loop_gbs, "frac": loop_gbs / peak if loop_gbs else None,
+                     "bytes_per_group_iter": bm["pcg_iter"], "step_gbs": step_gbs,
+                     "group_iterations": group_iters},
+        "kernels": kern,
+        "all_converged": conv_all,
+        "clocks": clocks.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, coords, keys)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

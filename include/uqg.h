@@ -1,0 +1,157 @@
+/*
+ * uqg.h - C ABI of the B200-native ensemble solve (libuqg.so).
+ *
+ * The reference (uqgroup, pure Python) has no FFI: its boundary is Python duck
+ * typing.  These entry points are what a ctypes binding of the
+ * reference's hot path binds; each names the reference interface it replaces.
+ * Conventions:
+ *   - every array argument is a DEVICE pointer unless its name ends in _host;
+ *   - ensemble data is sample-interleaved: values [G][nnz][S], vectors [G][N][S],
+ *     G independent groups ("ensembles") of S lanes ("samples") sharing one
+ *     CSR graph (row_offsets [N+1], col_indices [nnz], int32, sorted per row);
+ *   - `stream` is a cudaStream_t (may be NULL = legacy default stream); every
+ *     call is stream-ordered; only uqg_pcg, uqg_status_sync and calls that
+ *     return a validation verdict synchronise the stream;
+ *   - return value: UQG_OK or an error code; uqg_last_error() gives a
+ *     thread-local message for the last failing call.
+ */
+#ifndef UQG_H
+#define UQG_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define UQG_OK 0
+#define UQG_EINVAL 1      /* -> EnsembleError / GroupingError / FemError       */
+#define UQG_EBREAKDOWN 2  /* -> NumericalBreakdownError (ensemble.py:48-49)   */
+#define UQG_ECUDA 3       /* CUDA runtime error                                */
+#define UQG_ENOMEM 4      /* device allocation failed                          */
+#define UQG_ECAPACITY 5   /* residual-history buffer too small; re-run larger  */
+
+typedef struct uqg_ctx uqg_ctx;
+
+int uqg_version(void);
+const char* uqg_last_error(void);
+
+/* One context per device per process; owns scratch workspace and events. */
+int uqg_ctx_create(int device, uqg_ctx** out);
+int uqg_ctx_destroy(uqg_ctx* ctx);
+
+/* Hand the context a caller-owned device buffer to carve scratch from (e.g. a
+ * torch allocation); calls needing more fall back to a library allocation.
+ * ptr NULL detaches.  The buffer must outlive every call that uses it. */
+int uqg_ctx_set_workspace(uqg_ctx* ctx, void* ptr, long long bytes);
+
+/* Kernel classes for launch accounting / timing. */
+#define UQG_K_KL 0
+#define UQG_K_ASSEMBLE 1
+#define UQG_K_PCG_INIT 2
+#define UQG_K_PCG_SPMV 3   /* Ap = A p + p.Ap          (dominant kernel) */
+#define UQG_K_PCG_UPDATE 4 /* x, r update + r.r, r.z                    */
+#define UQG_K_PCG_DIR 5    /* p = z + beta p                             */
+#define UQG_K_DOT 6        /* lane_dot / qoi                             */
+#define UQG_K_GROUP 7      /* rank sort + chunk                          */
+#define UQG_K_SPMV 8       /* standalone spmv                            */
+#define UQG_K_OTHER 9      /* diagonal, jacobi, finalize                 */
+#define UQG_NKERN 10
+
+/* Per-launch CUDA-event timing on the launching stream (off by default).
+ * uqg_ctx_profile_read returns accumulated milliseconds and launch counts per
+ * kernel class (arrays of UQG_NKERN; either may be NULL) and optionally
+ * resets them; it synchronises on the last recorded event.  Launch counts are
+ * kept whether or not timing is on. */
+int uqg_ctx_profile(uqg_ctx* ctx, int enable);
+int uqg_ctx_profile_read(uqg_ctx* ctx, double* ms_host, long long* launches_host, int reset);
+/* Total kernels this context has launched. */
+long long uqg_ctx_launch_count(uqg_ctx* ctx);
+
+/* Device-side sticky status word (bit 0: non-positive coefficient or diagonal,
+ * bit 1: non-finite grouping key).  Synchronises `stream`, returns the word in
+ * *status_host and clears it. */
+int uqg_status_sync(uqg_ctx* ctx, void* stream, int* status_host);
+
+/* KL coefficient at the (n+1)^2 nodes of the unit-square grid, separable modes.
+ * Replaces KLDiffusionField.eval_a_batch (random_field.py:145-166) evaluated at
+ * the mesh nodes with mode_values (random_field.py:135-143) = factor products.
+ *   table1d [n_factors][n+1]: 1D factor f at x_i = i*h (np.interp, host setup)
+ *   mode_p/mode_q [M]: factor ids of mode m; sqrt_lam [M] = sqrt(eigenvalues)
+ *   samples [*][M] sample rows; lane_ids [G*S] (may be NULL = identity): lane
+ *   g*S+s evaluates sample row lane_ids[g*S+s] - the grouping plan from
+ *   uqg_group_sort feeds the solve without a host round trip;
+ *   a_hat_mode 0=constant 1=test2; expansion 0=log 1=linear
+ *   a_out [G][(n+1)^2][S].  a <= 0 anywhere sets status bit 0 (fem3d.py:153). */
+int uqg_kl_eval_sep2d(uqg_ctx* ctx, int n_cells, const double* table1d, int n_factors,
+                      const int* mode_p, const int* mode_q, const double* sqrt_lam, int M,
+                      const double* samples, const int* lane_ids, int G, int S, double a_min,
+                      int a_hat_mode, double a_hat_value, int expansion, double* a_out,
+                      void* stream);
+
+/* Dense form: a[l][p] = a_min + a_hat(y_l) * f(sum_m sqrt_lam[m] y_l[m] modes[m][p]),
+ * output lane-major [L][P] exactly like eval_a_batch's (S, P) result. */
+int uqg_kl_eval_table(uqg_ctx* ctx, const double* modes, int P, int M, const double* sqrt_lam,
+                      const double* samples, int L, double a_min, int a_hat_mode,
+                      double a_hat_value, int expansion, double* a_out, void* stream);
+
+/* 2D 5-point FV ensemble assembly into the shared graph (
+ * contract of assemble, fem3d.py:138-175).  a_nodes [G][(n+1)^2][S];
+ * vals [G][nnz][S]; dinv [G][N][S] = 1/diag (may be NULL; jacobi_precond,
+ * ensemble.py:179-183).  a2_same=0: y-faces use a_y (reference convention). */
+int uqg_assemble_fv2d(uqg_ctx* ctx, int n_cells, int G, int S, const double* a_nodes,
+                      double a_y, int a2_same, const int* row_offsets, double* vals,
+                      double* dinv, void* stream);
+
+/* Jacobi inverse diagonal from any shared-graph ensemble matrix
+ * (EnsembleCsrMatrix.diagonal + jacobi_precond, ensemble.py:130-137,179-183).
+ * Synchronises; returns UQG_EINVAL if any lane diagonal <= 0. */
+int uqg_jacobi_dinv(uqg_ctx* ctx, int N, int nnz, int S, int G, const int* row_offsets,
+                    const int* col_indices, const double* vals, double* dinv, void* stream);
+
+/* Raw lane diagonals diag [G][N][S] (EnsembleCsrMatrix.diagonal,
+ * ensemble.py:130-137): last diagonal entry of a row wins, absent reads 0. */
+int uqg_diagonal(uqg_ctx* ctx, int N, int nnz, int S, int G, const int* row_offsets,
+                 const int* col_indices, const double* vals, double* diag, void* stream);
+
+/* y = A x per lane, sequential CSR order without FMA: bitwise equal to scipy
+ * csr_matvec per lane (EnsembleCsrMatrix.spmv, ensemble.py:116-128). */
+int uqg_spmv(uqg_ctx* ctx, int N, int nnz, int S, int G, const int* row_offsets,
+             const int* col_indices, const double* vals, const double* x, double* y,
+             void* stream);
+
+/* out[g][s] = sum_j a[g][j][s] * b[g][j][s] (lane_dot, ensemble.py:155-161);
+ * deterministic fixed-shape reduction tree.  Also serves qoi (fem3d.py:178-183). */
+int uqg_lane_dot(uqg_ctx* ctx, int N, int S, int G, const double* a, const double* b,
+                 double* out, void* stream);
+
+/* Ensemble Jacobi-PCG on G independent groups at once (ensemble_pcg,
+ * ensemble.py:205-281; exact semantics in SURVEY.md Appendix A).
+ *   rhs [G][N][S] or NULL (then every entry is rhs_const);
+ *   dinv [G][N][S] or NULL (IdentityPreconditioner, ensemble.py:164-166);
+ *   x [G][N][S] out; iters [G][S] int32 out; converged/frozen [G][S] uint8 out;
+ *   ens_iters [G] int32 out;
+ *   hist_host: NULL, or host buffer [(hist_cap+1)][G][S] receiving the lane
+ *   residual norms per iteration (row 0 = ||b||); *hist_rows_host = rows used.
+ * Runs the whole loop on the device; the host only polls a done-counter.
+ * Returns UQG_EBREAKDOWN on a non-finite residual in an active lane. */
+int uqg_pcg(uqg_ctx* ctx, int N, int nnz, int S, int G, const int* row_offsets,
+            const int* col_indices, const double* vals, const double* rhs, double rhs_const,
+            const double* dinv, double tol, int maxit, double* x, int* iters,
+            unsigned char* converged, unsigned char* frozen, int* ens_iters,
+            double* hist_host, int hist_cap, int* hist_rows_host, void* stream);
+
+/* Device bytes of scratch uqg_pcg needs for (N, S, G) (r, p, Ap, partials). */
+long long uqg_pcg_workspace_bytes(int N, int nnz, int S, int G);
+
+/* Stable ascending sort of keys[n] (ties keep generation order) and chunking
+ * into width-S groups, the short last group padded with its last sample
+ * (group_by_key/_chunk, grouping.py:83-95,105-122).  keys NULL = natural
+ * order (group_natural, grouping.py:98-102).  order [n] out (may be NULL),
+ * groups [ceil(n/S)][S] out (indices into the input), pad [ceil(n/S)] out.
+ * Synchronises; returns UQG_EINVAL on a non-finite key. */
+int uqg_group_sort(uqg_ctx* ctx, const double* keys, int n, int S, int* order, int* groups,
+                   int* pad, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UQG_H */

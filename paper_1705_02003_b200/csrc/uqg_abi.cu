@@ -1,0 +1,518 @@
+// uqg_abi.cu - the C ABI of libuqg.so (include/uqg.h): argument validation,
+// context / workspace management, launch accounting and the host side of the
+// device-resident PCG loop.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/uqg.h"
+#include "uqg_common.cuh"
+#include "uqg_kernels.cuh"
+
+namespace uqg {
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace uqg
+
+using namespace uqg;
+
+struct uqg_ctx {
+  int device = 0;
+  int* status_dev = nullptr;       // sticky device status word
+  int* pinned = nullptr;           // [4] pinned host scratch
+  cudaEvent_t ev = nullptr;
+  void* ws = nullptr;              // workspace (library-owned, grow-only)
+  size_t ws_bytes = 0;
+  void* ext = nullptr;             // caller-provided workspace (uqg_ctx_set_workspace)
+  size_t ext_bytes = 0;
+  // launch accounting / optional per-launch event timing (uqg_ctx_profile*)
+  long long launches = 0;
+  long long kind_launches[UQG_NKERN] = {};
+  double kind_ms[UQG_NKERN] = {};
+  bool prof = false;
+  std::vector<cudaEvent_t> evpool;  // start/stop pairs
+  std::vector<int> pend_kind;
+  int pend = 0;
+};
+
+namespace {
+
+constexpr int kEventPairs = 512;
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int grid_for(long long total, int threads) {
+  long long b = (total + threads - 1) / threads;
+  long long cap = 148LL * 16;
+  if (b > cap) b = cap;
+  return b < 1 ? 1 : (int)b;
+}
+
+// Accumulate the elapsed times of all recorded (start, stop) pairs.
+int harvest(uqg_ctx* ctx) {
+  if (!ctx->pend) return UQG_OK;
+  UQG_TRY_CUDA(cudaEventSynchronize(ctx->evpool[2 * (ctx->pend - 1) + 1]));
+  for (int i = 0; i < ctx->pend; ++i) {
+    float ms = 0.f;
+    UQG_TRY_CUDA(cudaEventElapsedTime(&ms, ctx->evpool[2 * i], ctx->evpool[2 * i + 1]));
+    ctx->kind_ms[ctx->pend_kind[i]] += ms;
+  }
+  ctx->pend = 0;
+  return UQG_OK;
+}
+
+// Every kernel launch of the library goes through here: it counts launches
+// per kernel class and, when profiling is on, brackets the launch with CUDA
+// events on the launching stream.
+template <class F>
+int launch(uqg_ctx* ctx, int kind, cudaStream_t s, F&& fn) {
+  ctx->launches++;
+  ctx->kind_launches[kind]++;
+  if (ctx->prof) {
+    if (ctx->pend == kEventPairs) {
+      int rc = harvest(ctx);
+      if (rc) return rc;
+    }
+    UQG_TRY_CUDA(cudaEventRecord(ctx->evpool[2 * ctx->pend], s));
+    fn();
+    UQG_TRY_CUDA(cudaEventRecord(ctx->evpool[2 * ctx->pend + 1], s));
+    ctx->pend_kind[ctx->pend++] = kind;
+  } else {
+    fn();
+  }
+  UQG_CHECK_LAUNCH();
+  return UQG_OK;
+}
+
+#define UQG_LAUNCH(kind, stream, ...)                                    \
+  do {                                                                   \
+    int _rc = launch(ctx, (kind), (stream), [&] { __VA_ARGS__; });       \
+    if (_rc) return _rc;                                                 \
+  } while (0)
+
+// Workspace: the caller's buffer when it is large enough, else a grow-only
+// library allocation.  ws_base() returns whichever ensure_ws selected.
+void* ws_base(uqg_ctx* ctx, size_t bytes) {
+  return (ctx->ext && bytes <= ctx->ext_bytes) ? ctx->ext : ctx->ws;
+}
+
+int ensure_ws(uqg_ctx* ctx, size_t bytes) {
+  if (ctx->ext && bytes <= ctx->ext_bytes) return UQG_OK;
+  if (bytes <= ctx->ws_bytes) return UQG_OK;
+  if (ctx->ws) {
+    cudaDeviceSynchronize();
+    cudaFree(ctx->ws);
+    ctx->ws = nullptr;
+    ctx->ws_bytes = 0;
+  }
+  cudaError_t e = cudaMalloc(&ctx->ws, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error("workspace allocation of " + std::to_string(bytes) + " bytes failed: " +
+              cudaGetErrorString(e));
+    return UQG_ENOMEM;
+  }
+  ctx->ws_bytes = bytes;
+  return UQG_OK;
+}
+
+struct Carver {
+  char* base;
+  size_t off = 0;
+  template <class T>
+  T* take(size_t n) {
+    off = (off + 255) & ~size_t(255);
+    T* p = reinterpret_cast<T*>(base + off);
+    off += n * sizeof(T);
+    return p;
+  }
+};
+
+size_t pcg_layout(Carver& c, long long N, const Geo& geo, int G, PcgState* st, double** r,
+                  double** p, double** ap) {
+  const size_t vec = (size_t)G * N * geo.S;
+  const size_t lanes = (size_t)G * geo.S;
+  double* rr = c.take<double>(vec);
+  double* pp = c.take<double>(vec);
+  double* aa = c.take<double>(vec);
+  PcgState s{};
+  s.G = G;
+  s.part = c.take<double>((size_t)G * geo.B * 2 * geo.S);
+  s.ticket = c.take<unsigned int>(G);
+  s.rz = c.take<double>(lanes);
+  s.thr = c.take<double>(lanes);
+  s.alpha = c.take<double>(lanes);
+  s.beta = c.take<double>(lanes);
+  s.it = c.take<int>(G);
+  s.done = c.take<int>(G);
+  s.status = c.take<int>(G);
+  s.ndone = c.take<int>(1);
+  s.overflow = c.take<int>(1);
+  if (st) *st = s;
+  if (r) *r = rr;
+  if (p) *p = pp;
+  if (ap) *ap = aa;
+  return c.off + 256;
+}
+
+}  // namespace
+
+extern "C" {
+
+int uqg_version(void) { return 1; }
+
+const char* uqg_last_error(void) { return g_last_error.c_str(); }
+
+int uqg_ctx_create(int device, uqg_ctx** out) {
+  UQG_REQUIRE(out != nullptr, "uqg_ctx_create: out is NULL");
+  UQG_TRY_CUDA(cudaSetDevice(device));
+  uqg_ctx* c = new uqg_ctx();
+  c->device = device;
+  cudaError_t e = cudaMalloc(&c->status_dev, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(c->status_dev, 0, sizeof(int));
+  if (e == cudaSuccess) e = cudaHostAlloc(&c->pinned, 4 * sizeof(int), cudaHostAllocDefault);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    set_error(std::string("uqg_ctx_create: ") + cudaGetErrorString(e));
+    delete c;
+    return UQG_ECUDA;
+  }
+  *out = c;
+  return UQG_OK;
+}
+
+int uqg_ctx_destroy(uqg_ctx* ctx) {
+  if (!ctx) return UQG_OK;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  if (ctx->ws) cudaFree(ctx->ws);
+  if (ctx->status_dev) cudaFree(ctx->status_dev);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->ev) cudaEventDestroy(ctx->ev);
+  for (cudaEvent_t e : ctx->evpool) cudaEventDestroy(e);
+  delete ctx;
+  return UQG_OK;
+}
+
+int uqg_ctx_set_workspace(uqg_ctx* ctx, void* ptr, long long bytes) {
+  UQG_REQUIRE(ctx && bytes >= 0, "uqg_ctx_set_workspace: bad argument");
+  ctx->ext = ptr;
+  ctx->ext_bytes = ptr ? (size_t)bytes : 0;
+  return UQG_OK;
+}
+
+int uqg_ctx_profile(uqg_ctx* ctx, int enable) {
+  UQG_REQUIRE(ctx, "uqg_ctx_profile: NULL ctx");
+  if (enable && ctx->evpool.empty()) {
+    ctx->evpool.resize(2 * kEventPairs);
+    ctx->pend_kind.resize(kEventPairs);
+    for (auto& e : ctx->evpool) UQG_TRY_CUDA(cudaEventCreate(&e));
+  }
+  if (!enable) {
+    int rc = harvest(ctx);
+    if (rc) return rc;
+  }
+  ctx->prof = enable != 0;
+  return UQG_OK;
+}
+
+int uqg_ctx_profile_read(uqg_ctx* ctx, double* ms_host, long long* launches_host, int reset) {
+  UQG_REQUIRE(ctx, "uqg_ctx_profile_read: NULL ctx");
+  int rc = harvest(ctx);
+  if (rc) return rc;
+  for (int k = 0; k < UQG_NKERN; ++k) {
+    if (ms_host) ms_host[k] = ctx->kind_ms[k];
+    if (launches_host) launches_host[k] = ctx->kind_launches[k];
+    if (reset) {
+      ctx->kind_ms[k] = 0.0;
+      ctx->kind_launches[k] = 0;
+    }
+  }
+  return UQG_OK;
+}
+
+long long uqg_ctx_launch_count(uqg_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int uqg_status_sync(uqg_ctx* ctx, void* stream, int* status_host) {
+  UQG_REQUIRE(ctx && status_host, "uqg_status_sync: NULL argument");
+  cudaStream_t s = as_stream(stream);
+  UQG_TRY_CUDA(cudaMemcpyAsync(ctx->pinned, ctx->status_dev, sizeof(int), cudaMemcpyDeviceToHost, s));
+  UQG_TRY_CUDA(cudaMemsetAsync(ctx->status_dev, 0, sizeof(int), s));
+  UQG_TRY_CUDA(cudaStreamSynchronize(s));
+  *status_host = ctx->pinned[0];
+  return UQG_OK;
+}
+
+int uqg_kl_eval_sep2d(uqg_ctx* ctx, int n_cells, const double* table1d, int n_factors,
+                      const int* mode_p, const int* mode_q, const double* sqrt_lam, int M,
+                      const double* samples, const int* lane_ids, int G, int S, double a_min,
+                      int a_hat_mode, double a_hat_value, int expansion, double* a_out,
+                      void* stream) {
+  UQG_REQUIRE(ctx && table1d && mode_p && mode_q && sqrt_lam && samples && a_out,
+              "uqg_kl_eval_sep2d: NULL argument");
+  UQG_REQUIRE(n_cells >= 2 && n_factors >= 1 && M >= 1 && G >= 1 && S >= 1,
+              "uqg_kl_eval_sep2d: bad sizes");
+  UQG_REQUIRE(a_hat_mode == 0 || a_hat_mode == 1, "unknown a_hat mode");
+  UQG_REQUIRE(expansion == 0 || expansion == 1, "unknown expansion");
+  const int n1 = n_cells + 1;
+  const long long total = (long long)G * n1 * n1 * S;
+  cudaStream_t s = as_stream(stream);
+  UQG_LAUNCH(UQG_K_KL, s,
+             kl_sep2d_kernel<<<grid_for(total, 256), 256, 0, s>>>(
+                 n1, table1d, mode_p, mode_q, sqrt_lam, M, samples, lane_ids, G, S, a_min,
+                 a_hat_mode, a_hat_value, expansion, a_out, ctx->status_dev));
+  return UQG_OK;
+}
+
+int uqg_kl_eval_table(uqg_ctx* ctx, const double* modes, int P, int M, const double* sqrt_lam,
+                      const double* samples, int L, double a_min, int a_hat_mode,
+                      double a_hat_value, int expansion, double* a_out, void* stream) {
+  UQG_REQUIRE(ctx && modes && sqrt_lam && samples && a_out, "uqg_kl_eval_table: NULL argument");
+  UQG_REQUIRE(P >= 1 && M >= 1 && L >= 1, "uqg_kl_eval_table: bad sizes");
+  UQG_REQUIRE(a_hat_mode == 0 || a_hat_mode == 1, "unknown a_hat mode");
+  UQG_REQUIRE(expansion == 0 || expansion == 1, "unknown expansion");
+  const long long total = (long long)L * P;
+  cudaStream_t s = as_stream(stream);
+  UQG_LAUNCH(UQG_K_KL, s,
+             kl_table_kernel<<<grid_for(total, 256), 256, 0, s>>>(
+                 modes, P, M, sqrt_lam, samples, L, a_min, a_hat_mode, a_hat_value, expansion,
+                 a_out, ctx->status_dev));
+  return UQG_OK;
+}
+
+int uqg_assemble_fv2d(uqg_ctx* ctx, int n_cells, int G, int S, const double* a_nodes,
+                      double a_y, int a2_same, const int* row_offsets, double* vals,
+                      double* dinv, void* stream) {
+  UQG_REQUIRE(ctx && a_nodes && row_offsets && vals, "uqg_assemble_fv2d: NULL argument");
+  UQG_REQUIRE(n_cells >= 2 && G >= 1 && S >= 1, "uqg_assemble_fv2d: bad sizes");
+  const long long N = (long long)(n_cells - 1) * (n_cells - 1);
+  const long long total = (long long)G * N * S;
+  cudaStream_t s = as_stream(stream);
+  UQG_LAUNCH(UQG_K_ASSEMBLE, s,
+             assemble_fv2d_kernel<<<grid_for(total, 256), 256, 0, s>>>(
+                 n_cells, G, S, a_nodes, a_y, a2_same, row_offsets, vals, dinv));
+  return UQG_OK;
+}
+
+int uqg_jacobi_dinv(uqg_ctx* ctx, int N, int nnz, int S, int G, const int* row_offsets,
+                    const int* col_indices, const double* vals, double* dinv, void* stream) {
+  UQG_REQUIRE(ctx && row_offsets && dinv, "uqg_jacobi_dinv: NULL argument");
+  UQG_REQUIRE(N >= 0 && nnz >= 0 && S >= 1 && G >= 1, "uqg_jacobi_dinv: bad sizes");
+  int st = 0;
+  int rc = uqg_status_sync(ctx, stream, &st);  // clear stale bits
+  if (rc) return rc;
+  const long long total = (long long)G * N * S;
+  cudaStream_t s = as_stream(stream);
+  if (total > 0) {
+    UQG_LAUNCH(UQG_K_OTHER, s,
+               jacobi_dinv_kernel<<<grid_for(total, 256), 256, 0, s>>>(
+                   N, S, G, nnz, row_offsets, col_indices, vals, dinv, ctx->status_dev, 0));
+  }
+  rc = uqg_status_sync(ctx, stream, &st);
+  if (rc) return rc;
+  UQG_REQUIRE(!(st & 1), "Jacobi preconditioner needs strictly positive lane diagonals");
+  return UQG_OK;
+}
+
+int uqg_diagonal(uqg_ctx* ctx, int N, int nnz, int S, int G, const int* row_offsets,
+                 const int* col_indices, const double* vals, double* diag, void* stream) {
+  UQG_REQUIRE(ctx && row_offsets && diag, "uqg_diagonal: NULL argument");
+  UQG_REQUIRE(N >= 0 && nnz >= 0 && S >= 1 && G >= 1, "uqg_diagonal: bad sizes");
+  const long long total = (long long)G * N * S;
+  cudaStream_t s = as_stream(stream);
+  if (total > 0) {
+    UQG_LAUNCH(UQG_K_OTHER, s,
+               jacobi_dinv_kernel<<<grid_for(total, 256), 256, 0, s>>>(
+                   N, S, G, nnz, row_offsets, col_indices, vals, diag, ctx->status_dev, 1));
+  }
+  return UQG_OK;
+}
+
+int uqg_spmv(uqg_ctx* ctx, int N, int nnz, int S, int G, const int* row_offsets,
+             const int* col_indices, const double* vals, const double* x, double* y,
+             void* stream) {
+  UQG_REQUIRE(ctx && row_offsets && x && y, "uqg_spmv: NULL argument");
+  UQG_REQUIRE(N >= 0 && nnz >= 0 && S >= 1 && S <= 1024 && G >= 1, "uqg_spmv: bad sizes");
+  if (N == 0) return UQG_OK;
+  Geo geo = make_geo(N, S);
+  cudaStream_t s = as_stream(stream);
+  UQG_LAUNCH(UQG_K_SPMV, s,
+             spmv_kernel<<<dim3(geo.B, G), geo.T, 0, s>>>(N, nnz, geo, row_offsets, col_indices,
+                                                          vals, x, y));
+  return UQG_OK;
+}
+
+int uqg_lane_dot(uqg_ctx* ctx, int N, int S, int G, const double* a, const double* b,
+                 double* out, void* stream) {
+  UQG_REQUIRE(ctx && a && b && out, "uqg_lane_dot: NULL argument");
+  UQG_REQUIRE(N >= 0 && S >= 1 && S <= 1024 && G >= 1, "uqg_lane_dot: bad sizes");
+  cudaStream_t s = as_stream(stream);
+  Geo geo = make_geo(N, S);
+  size_t need = (size_t)G * geo.B * geo.S * sizeof(double) + (size_t)G * sizeof(unsigned) + 1024;
+  int rc = ensure_ws(ctx, need);
+  if (rc) return rc;
+  Carver c{(char*)ws_base(ctx, need)};
+  double* part = c.take<double>((size_t)G * geo.B * geo.S);
+  unsigned* ticket = c.take<unsigned>(G);
+  UQG_TRY_CUDA(cudaMemsetAsync(ticket, 0, G * sizeof(unsigned), s));
+  UQG_LAUNCH(UQG_K_DOT, s,
+             lane_dot_kernel<<<dim3(geo.B, G), geo.T, geo.T * sizeof(double), s>>>(
+                 N, geo, a, b, out, part, ticket));
+  return UQG_OK;
+}
+
+long long uqg_pcg_workspace_bytes(int N, int nnz, int S, int G) {
+  (void)nnz;
+  if (N < 0 || S < 1 || G < 1) return -1;
+  Geo geo = make_geo(N, S);
+  Carver c{nullptr};
+  return (long long)pcg_layout(c, N, geo, G, nullptr, nullptr, nullptr, nullptr);
+}
+
+int uqg_pcg(uqg_ctx* ctx, int N, int nnz, int S, int G, const int* row_offsets,
+            const int* col_indices, const double* vals, const double* rhs, double rhs_const,
+            const double* dinv, double tol, int maxit, double* x, int* iters,
+            unsigned char* converged, unsigned char* frozen, int* ens_iters,
+            double* hist_host, int hist_cap, int* hist_rows_host, void* stream) {
+  UQG_REQUIRE(ctx && row_offsets && x && iters && converged && frozen && ens_iters,
+              "uqg_pcg: NULL argument");
+  UQG_REQUIRE(N >= 0 && nnz >= 0 && S >= 1 && S <= 1024 && G >= 1, "uqg_pcg: bad sizes");
+  UQG_REQUIRE(tol > 0.0 && tol <= 1.7976931348623157e308, "tol must be positive and finite");
+  UQG_REQUIRE(maxit >= 0, "maxit must be >= 0");
+  UQG_REQUIRE(!hist_host || (hist_cap >= 0 && hist_rows_host), "uqg_pcg: bad history buffer");
+  cudaStream_t s = as_stream(stream);
+  Geo geo = make_geo(N, S);
+  Carver probe{nullptr};
+  size_t need = pcg_layout(probe, N, geo, G, nullptr, nullptr, nullptr, nullptr);
+  size_t hist_elems = hist_host ? (size_t)(hist_cap + 1) * G * S : 0;
+  need += hist_elems * sizeof(double) + 256;
+  int rc = ensure_ws(ctx, need);
+  if (rc) return rc;
+  Carver c{(char*)ws_base(ctx, need)};
+  PcgState st;
+  double *r, *p, *ap;
+  pcg_layout(c, N, geo, G, &st, &r, &p, &ap);
+  st.iters = iters;
+  st.conv = converged;
+  st.frozen = frozen;
+  st.hist = hist_host ? c.take<double>(hist_elems) : nullptr;
+  st.hist_cap = hist_cap;
+  UQG_TRY_CUDA(cudaMemsetAsync(st.ticket, 0, G * sizeof(unsigned), s));
+  UQG_TRY_CUDA(cudaMemsetAsync(st.ndone, 0, sizeof(int), s));
+  UQG_TRY_CUDA(cudaMemsetAsync(st.overflow, 0, sizeof(int), s));
+
+  const dim3 grid(geo.B, G);
+  const size_t smem2 = 2 * geo.T * sizeof(double), smem1 = geo.T * sizeof(double);
+  UQG_LAUNCH(UQG_K_PCG_INIT, s,
+             pcg_init_kernel<<<grid, geo.T, smem2, s>>>(N, geo, st, rhs, rhs_const, dinv, tol,
+                                                        maxit, x, r, p));
+  // Host polls the device done-counter between chunks of iterations.  Groups
+  // that have terminated turn every later launch into a no-op, so the extra
+  // launches of the last chunk cannot change any result.
+  long long launched = 0;
+  int chunk = 2;
+  for (;;) {
+    UQG_TRY_CUDA(cudaMemcpyAsync(ctx->pinned, st.ndone, sizeof(int), cudaMemcpyDeviceToHost, s));
+    UQG_TRY_CUDA(cudaEventRecord(ctx->ev, s));
+    UQG_TRY_CUDA(cudaEventSynchronize(ctx->ev));
+    if (ctx->prof) {
+      rc = harvest(ctx);
+      if (rc) return rc;
+    }
+    if (ctx->pinned[0] >= G) break;
+    if (launched > (long long)maxit + 1) {
+      set_error("uqg_pcg: device loop failed to terminate");
+      return UQG_ECUDA;
+    }
+    for (int k = 0; k < chunk; ++k) {
+      UQG_LAUNCH(UQG_K_PCG_SPMV, s,
+                 pcg_spmv_kernel<<<grid, geo.T, smem1, s>>>(N, nnz, geo, st, row_offsets,
+                                                            col_indices, vals, p, ap));
+      UQG_LAUNCH(UQG_K_PCG_UPDATE, s,
+                 pcg_update_kernel<<<grid, geo.T, smem2, s>>>(N, geo, st, dinv, maxit, x, r, p,
+                                                              ap));
+      UQG_LAUNCH(UQG_K_PCG_DIR, s,
+                 pcg_dir_kernel<<<grid, geo.T, 0, s>>>(N, geo, st, dinv, r, p));
+    }
+    launched += chunk;
+    chunk = std::min(chunk * 2, 64);
+  }
+  UQG_LAUNCH(UQG_K_OTHER, s,
+             pcg_finalize_kernel<<<(G + 127) / 128, 128, 0, s>>>(st, G, S, ens_iters));
+  // breakdown / history bookkeeping
+  std::vector<int> h_status(G);
+  cudaError_t e =
+      cudaMemcpyAsync(h_status.data(), st.status, G * sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(ctx->pinned + 1, st.overflow, sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    set_error(std::string("uqg_pcg: ") + cudaGetErrorString(e));
+    return UQG_ECUDA;
+  }
+  for (int g = 0; g < G; ++g) {
+    if (h_status[g] == 2) {
+      set_error("non-finite residual in active lane (group " + std::to_string(g) + ")");
+      return UQG_EBREAKDOWN;
+    }
+  }
+  if (hist_host) {
+    if (ctx->pinned[1]) {
+      set_error("residual history capacity exceeded");
+      return UQG_ECAPACITY;
+    }
+    std::vector<int> h_it(G);
+    e = cudaMemcpy(h_it.data(), st.it, G * sizeof(int), cudaMemcpyDeviceToHost);
+    int rows = 1 + *std::max_element(h_it.begin(), h_it.end());
+    if (e == cudaSuccess)
+      e = cudaMemcpy(hist_host, st.hist, (size_t)rows * G * S * sizeof(double),
+                     cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+      set_error(std::string("uqg_pcg history: ") + cudaGetErrorString(e));
+      return UQG_ECUDA;
+    }
+    *hist_rows_host = rows;
+  }
+  return UQG_OK;
+}
+
+int uqg_group_sort(uqg_ctx* ctx, const double* keys, int n, int S, int* order, int* groups,
+                   int* pad, void* stream) {
+  UQG_REQUIRE(ctx && groups && pad, "uqg_group_sort: NULL argument");
+  UQG_REQUIRE(n >= 1, "cannot group an empty sample set");
+  UQG_REQUIRE(S >= 1, "ensemble size must be >= 1");
+  cudaStream_t s = as_stream(stream);
+  int st = 0;
+  int rc = uqg_status_sync(ctx, stream, &st);
+  if (rc) return rc;
+  const int K = (n + S - 1) / S;
+  int* ord = order;
+  if (keys) {
+    if (!ord) {
+      const size_t need = (size_t)n * sizeof(int) + 256;
+      rc = ensure_ws(ctx, need);
+      if (rc) return rc;
+      ord = (int*)ws_base(ctx, need);
+    }
+    UQG_LAUNCH(UQG_K_GROUP, s,
+               rank_sort_kernel<<<(n + 255) / 256, 256, 0, s>>>(keys, n, ord, ctx->status_dev));
+  } else {
+    ord = nullptr;  // natural order
+  }
+  const long long slots = (long long)K * S;
+  UQG_LAUNCH(UQG_K_GROUP, s,
+             chunk_kernel<<<(int)((slots + 255) / 256), 256, 0, s>>>(ord, n, S, K, groups, pad));
+  if (!keys && order) {
+    UQG_TRY_CUDA(cudaMemcpyAsync(order, groups, (size_t)n * sizeof(int), cudaMemcpyDeviceToDevice, s));
+  }
+  rc = uqg_status_sync(ctx, stream, &st);
+  if (rc) return rc;
+  UQG_REQUIRE(!(st & 2), "grouping keys must be finite");
+  return UQG_OK;
+}
+
+}  // extern "C"

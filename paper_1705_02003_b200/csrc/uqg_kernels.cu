@@ -1,0 +1,433 @@
+// uqg_kernels.cu - sm_100a kernels of the ensemble solve hot path.
+//
+// Layout: G groups x S lanes; matrix values
+// [G][nnz][S], vectors [G][N][S]; one shared CSR graph.  All elementwise
+// arithmetic that the reference performs with numpy is written with explicit
+// round-to-nearest intrinsics (no FMA contraction; the library is also built
+// with --fmad=false) so each lane reproduces numpy's rounding sequence.
+// Only the order of the reductions (dots/norms) differs from numpy's BLAS.
+
+#include <cuda_runtime.h>
+#include <float.h>
+#include <math.h>
+
+#include "uqg_common.cuh"
+#include "uqg_kernels.cuh"
+
+namespace uqg {
+
+// ===========================================================================
+// KL coefficient (random_field.py:145-166)
+
+__device__ __forceinline__ double a_hat_of(const double* y, int M, int mode, double value) {
+  if (mode == 0) return value;
+  // "test2" (random_field.py:126-132): piecewise amplitude over the sample radius
+  double ss = 0.0;
+  for (int m = 0; m < M; ++m) ss = __dadd_rn(ss, __dmul_rn(y[m], y[m]));
+  const double r = sqrt(ss), d = 1.7320508075688772;  // sqrt(3.0)
+  const double f = r < d / 4.0 ? 1.0 : (r < d / 2.0 ? 100.0 : 10.0);
+  return __dmul_rn(value, f);
+}
+
+__device__ __forceinline__ double kl_finish(double e, int expansion, double a_min, double ahat) {
+  e = expansion == 0 ? exp(e) : __dadd_rn(1.0, e);
+  return __dadd_rn(a_min, __dmul_rn(ahat, e));
+}
+
+// One thread per (group, node, lane); lanes fastest so the a_out store is
+// coalesced.  Mode values are rebuilt on the fly from the separable 1D tables
+// (one rounded product each, bit-identical to the host mode table), so the
+// (M x P) table never has to be streamed from HBM.
+__global__ void kl_sep2d_kernel(int n1, const double* __restrict__ table1d,
+                                const int* __restrict__ mode_p, const int* __restrict__ mode_q,
+                                const double* __restrict__ sqrt_lam, int M,
+                                const double* __restrict__ samples,
+                                const int* __restrict__ lane_ids, int G, int S, double a_min,
+                                int a_hat_mode, double a_hat_value, int expansion,
+                                double* __restrict__ a_out, int* status) {
+  const long long P = (long long)n1 * n1;
+  const long long total = (long long)G * P * S;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(idx % S);
+    const long long gp = idx / S;
+    const long long p = gp % P;
+    const int g = (int)(gp / P);
+    const int i = (int)(p / n1), j = (int)(p % n1);
+    const size_t lane = (size_t)g * S + s;
+    const double* y = samples + (lane_ids ? (size_t)__ldg(&lane_ids[lane]) : lane) * M;
+    double e = 0.0;
+    for (int m = 0; m < M; ++m) {
+      const double mv = __dmul_rn(__ldg(&table1d[(size_t)__ldg(&mode_p[m]) * n1 + i]),
+                                  __ldg(&table1d[(size_t)__ldg(&mode_q[m]) * n1 + j]));
+      e = __fma_rn(__dmul_rn(y[m], __ldg(&sqrt_lam[m])), mv, e);
+    }
+    const double a = kl_finish(e, expansion, a_min, a_hat_of(y, M, a_hat_mode, a_hat_value));
+    if (a <= 0.0) atomicOr(status, 1);
+    a_out[idx] = a;
+  }
+}
+
+// Dense-table form, output lane-major [L][P] (eval_a_batch's (S, P)).
+__global__ void kl_table_kernel(const double* __restrict__ modes, int P, int M,
+                                const double* __restrict__ sqrt_lam,
+                                const double* __restrict__ samples, int L, double a_min,
+                                int a_hat_mode, double a_hat_value, int expansion,
+                                double* __restrict__ a_out, int* status) {
+  const long long total = (long long)L * P;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int l = (int)(idx / P);
+    const long long p = idx % P;
+    const double* y = samples + (size_t)l * M;
+    double e = 0.0;
+    for (int m = 0; m < M; ++m)
+      e = __fma_rn(__dmul_rn(y[m], __ldg(&sqrt_lam[m])), __ldg(&modes[(size_t)m * P + p]), e);
+    const double a = kl_finish(e, expansion, a_min, a_hat_of(y, M, a_hat_mode, a_hat_value));
+    if (a <= 0.0) atomicOr(status, 1);
+    a_out[idx] = a;
+  }
+}
+
+// ===========================================================================
+// 2D 5-point FV assembly (oracle/fv2d.py; contract of fem3d.py:138-175)
+
+__device__ __forceinline__ double harm(double a, double b) {
+  return __ddiv_rn(__dmul_rn(__dmul_rn(2.0, a), b), __dadd_rn(a, b));
+}
+
+__global__ void assemble_fv2d_kernel(int n, int G, int S, const double* __restrict__ a_nodes,
+                                     double a_y, int a2_same, const int* __restrict__ row_offsets,
+                                     double* __restrict__ vals, double* __restrict__ dinv) {
+  const int m = n - 1, n1 = n + 1;
+  const long long N = (long long)m * m, P = (long long)n1 * n1;
+  const long long nnz = 5 * N - 4 * (long long)m;
+  const long long total = (long long)G * N * S;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(idx % S);
+    const long long gr = idx / S;
+    const long long row = gr % N;
+    const int g = (int)(gr / N);
+    const int i = (int)(row / m) + 1, j = (int)(row % m) + 1;
+    const double* a = a_nodes + (size_t)g * P * S + s;
+    const long long c = (long long)i * n1 + j;
+    const double ac = a[c * S];
+    const double tw = harm(a[(c - n1) * S], ac);
+    const double te = harm(ac, a[(c + n1) * S]);
+    double ts = a_y, tn = a_y;
+    if (a2_same) {
+      ts = harm(a[(c - 1) * S], ac);
+      tn = harm(ac, a[(c + 1) * S]);
+    }
+    const double diag = __dadd_rn(__dadd_rn(__dadd_rn(tw, te), ts), tn);
+    double* v = vals + ((size_t)g * nnz + row_offsets[row]) * S + s;
+    int k = 0;
+    if (i > 1) v[(k++) * S] = -tw;
+    if (j > 1) v[(k++) * S] = -ts;
+    v[(k++) * S] = diag;
+    if (j < m) v[(k++) * S] = -tn;
+    if (i < m) v[(k++) * S] = -te;
+    if (dinv) dinv[idx] = __ddiv_rn(1.0, diag);
+  }
+}
+
+// ===========================================================================
+// Jacobi inverse diagonal (ensemble.py:130-137,179-183).  The last diagonal
+// entry of a row wins (numpy fancy assignment), an absent one reads 0.
+
+__global__ void jacobi_dinv_kernel(long long N, int S, int G, long long nnz,
+                                   const int* __restrict__ ro, const int* __restrict__ ci,
+                                   const double* __restrict__ vals, double* __restrict__ dinv,
+                                   int* status, int raw) {
+  const long long total = (long long)G * N * S;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(idx % S);
+    const long long gr = idx / S;
+    const long long row = gr % N;
+    const int g = (int)(gr / N);
+    double d = 0.0;
+    for (int k = ro[row]; k < ro[row + 1]; ++k)
+      if (ci[k] == row) d = vals[((size_t)g * nnz + k) * S + s];
+    if (raw) {
+      dinv[idx] = d;
+    } else {
+      if (d <= 0.0) atomicOr(status, 1);
+      dinv[idx] = __ddiv_rn(1.0, d);
+    }
+  }
+}
+
+// ===========================================================================
+// SpMV.  Per (row, lane): acc = 0; acc = acc + v_k * x_{c_k} in CSR order with
+// separate roundings - scipy's csr_matvec order, so lanes match it bitwise.
+
+__device__ __forceinline__ double row_dot(const int* __restrict__ ci, const double* __restrict__ v,
+                                          const double* __restrict__ x, int k0, int k1, int S) {
+  double acc = 0.0;
+  for (int k = k0; k < k1; ++k) {
+    const int c = __ldg(&ci[k]);
+    acc = __dadd_rn(acc, __dmul_rn(__ldg(&v[(size_t)k * S]), x[(size_t)c * S]));
+  }
+  return acc;
+}
+
+__global__ void spmv_kernel(long long N, long long nnz, Geo geo, const int* __restrict__ ro,
+                            const int* __restrict__ ci, const double* __restrict__ vals,
+                            const double* __restrict__ x, double* __restrict__ y) {
+  const int g = blockIdx.y, t = threadIdx.x;
+  const int s = t % geo.Sp, rr = t / geo.Sp, S = geo.S;
+  if (s >= S) return;
+  const double* vg = vals + (size_t)g * nnz * S + s;
+  const double* xg = x + (size_t)g * N * S + s;
+  double* yg = y + (size_t)g * N * S + s;
+  for (long long tile = blockIdx.x; tile < geo.tiles; tile += geo.B) {
+    const long long row = tile * geo.R + rr;
+    if (row < N) yg[row * S] = row_dot(ci, vg, xg, __ldg(&ro[row]), __ldg(&ro[row + 1]), S);
+  }
+}
+
+// out[g][s] = sum_j a*b (lane_dot / qoi); fused multiply-add in the reduction
+// (reduction order is implementation-defined in the reference too).
+__global__ void lane_dot_kernel(long long N, Geo geo, const double* __restrict__ a,
+                                const double* __restrict__ b, double* __restrict__ out,
+                                double* part, unsigned int* ticket) {
+  extern __shared__ double red[];
+  const int g = blockIdx.y, t = threadIdx.x;
+  const int s = t % geo.Sp, rr = t / geo.Sp, S = geo.S;
+  double acc[1] = {0.0};
+  if (s < S) {
+    const double* ag = a + (size_t)g * N * S + s;
+    const double* bg = b + (size_t)g * N * S + s;
+    for (long long tile = blockIdx.x; tile < geo.tiles; tile += geo.B) {
+      const long long row = tile * geo.R + rr;
+      if (row < N) acc[0] = __fma_rn(ag[row * S], bg[row * S], acc[0]);
+    }
+  }
+  if (reduce_lanes<1>(acc, red, part, ticket, g, geo) && t < S) out[(size_t)g * S + t] = red[t];
+}
+
+// ===========================================================================
+// Ensemble PCG (ensemble.py:205-281).  Per-group device state:
+
+__global__ void pcg_init_kernel(long long N, Geo geo, PcgState st, const double* __restrict__ rhs,
+                                double rhs_const, const double* __restrict__ dinv, double tol,
+                                int maxit, double* __restrict__ x, double* __restrict__ r,
+                                double* __restrict__ p) {
+  extern __shared__ double red[];
+  const int g = blockIdx.y, t = threadIdx.x;
+  const int s = t % geo.Sp, rr = t / geo.Sp, S = geo.S;
+  double acc[2] = {0.0, 0.0};  // b.b, r.z
+  if (s < S) {
+    const size_t base = (size_t)g * N * S + s;
+    for (long long tile = blockIdx.x; tile < geo.tiles; tile += geo.B) {
+      const long long row = tile * geo.R + rr;
+      if (row < N) {
+        const size_t o = base + row * S;
+        const double bv = rhs ? rhs[o] : rhs_const;
+        const double zv = dinv ? __dmul_rn(bv, dinv[o]) : bv;
+        x[o] = 0.0;
+        r[o] = bv;
+        p[o] = zv;
+        acc[0] = __fma_rn(bv, bv, acc[0]);
+        acc[1] = __fma_rn(bv, zv, acc[1]);
+      }
+    }
+  }
+  if (!reduce_lanes<2>(acc, red, st.part, st.ticket, g, geo)) return;
+  __shared__ int s_all;
+  if (t == 0) s_all = 1;
+  __syncthreads();
+  if (t < S) {
+    const size_t l = (size_t)g * S + t;
+    const double bn = sqrt(red[t]);
+    const double thr = tol * bn;
+    const bool conv = bn <= thr;  // zero right-hand sides converge at iteration 0
+    st.thr[l] = thr;
+    st.rz[l] = red[geo.T + t];
+    st.conv[l] = conv;
+    st.frozen[l] = 0;
+    st.iters[l] = 0;
+    if (st.hist) st.hist[l] = bn;
+    if (!conv) s_all = 0;
+  }
+  __syncthreads();
+  if (t == 0) {
+    st.it[g] = 0;
+    st.status[g] = 0;
+    const int done = s_all || maxit == 0;
+    st.done[g] = done;
+    if (done) atomicAdd(st.ndone, 1);
+  }
+  if (t < S) {
+    // iterations[~converged] = it (=0) already; converged lanes have 0 too.
+  }
+}
+
+// Ap = A p, partial p.Ap; the last block freezes lanes and forms alpha.
+__global__ void pcg_spmv_kernel(long long N, long long nnz, Geo geo, PcgState st,
+                                const int* __restrict__ ro, const int* __restrict__ ci,
+                                const double* __restrict__ vals, const double* __restrict__ p,
+                                double* __restrict__ ap) {
+  extern __shared__ double red[];
+  const int g = blockIdx.y, t = threadIdx.x;
+  if (st.done[g]) return;
+  const int s = t % geo.Sp, rr = t / geo.Sp, S = geo.S;
+  double acc[1] = {0.0};
+  if (s < S) {
+    const double* vg = vals + (size_t)g * nnz * S + s;
+    const size_t base = (size_t)g * N * S + s;
+    const double* pg = p + base;
+    for (long long tile = blockIdx.x; tile < geo.tiles; tile += geo.B) {
+      const long long row = tile * geo.R + rr;
+      if (row < N) {
+        const double y = row_dot(ci, vg, pg, __ldg(&ro[row]), __ldg(&ro[row + 1]), S);
+        ap[base + row * S] = y;
+        acc[0] = __fma_rn(pg[row * S], y, acc[0]);
+      }
+    }
+  }
+  if (!reduce_lanes<1>(acc, red, st.part, st.ticket, g, geo)) return;
+  if (t < S) {
+    const size_t l = (size_t)g * S + t;
+    const double pap = red[t];
+    const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
+    st.frozen[l] = fr;
+    st.alpha[l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
+  }
+  if (t == 0) st.it[g] += 1;
+}
+
+// x += alpha p; r -= alpha Ap; partial r.r and r.z with z = dinv*r.
+// The last block tests convergence / breakdown / termination and forms beta.
+__global__ void pcg_update_kernel(long long N, Geo geo, PcgState st, const double* __restrict__ dinv,
+                                  int maxit, double* __restrict__ x, double* __restrict__ r,
+                                  const double* __restrict__ p, const double* __restrict__ ap) {
+  extern __shared__ double red[];
+  const int g = blockIdx.y, t = threadIdx.x;
+  if (st.done[g]) return;
+  const int s = t % geo.Sp, rr = t / geo.Sp, S = geo.S;
+  double acc[2] = {0.0, 0.0};
+  if (s < S) {
+    const double alpha = st.alpha[(size_t)g * S + s];
+    const size_t base = (size_t)g * N * S + s;
+    for (long long tile = blockIdx.x; tile < geo.tiles; tile += geo.B) {
+      const long long row = tile * geo.R + rr;
+      if (row < N) {
+        const size_t o = base + row * S;
+        x[o] = __dadd_rn(x[o], __dmul_rn(alpha, p[o]));
+        const double rv = __dsub_rn(r[o], __dmul_rn(alpha, ap[o]));
+        r[o] = rv;
+        const double zv = dinv ? __dmul_rn(rv, dinv[o]) : rv;
+        acc[0] = __fma_rn(rv, rv, acc[0]);
+        acc[1] = __fma_rn(rv, zv, acc[1]);
+      }
+    }
+  }
+  if (!reduce_lanes<2>(acc, red, st.part, st.ticket, g, geo)) return;
+  __shared__ int s_all, s_bad;
+  if (t == 0) { s_all = 1; s_bad = 0; }
+  __syncthreads();
+  const int it = st.it[g];
+  if (t < S) {
+    const size_t l = (size_t)g * S + t;
+    const double rn = sqrt(red[t]);
+    const double rz_new = red[geo.T + t];
+    if (st.hist) {
+      if (it <= st.hist_cap) st.hist[(size_t)it * st.G * S + l] = rn;
+      else atomicOr(st.overflow, 1);
+    }
+    const bool live = !st.frozen[l];
+    if (live && !isfinite(rn)) atomicOr(&s_bad, 1);
+    bool conv = st.conv[l];
+    if (live && !conv && rn <= st.thr[l]) {
+      st.iters[l] = it;
+      st.conv[l] = 1;
+      conv = true;
+    }
+    if (!(conv || !live)) atomicAnd(&s_all, 0);
+    const double rz_old = st.rz[l];
+    st.beta[l] = (live && rz_old > 0.0) ? __ddiv_rn(rz_new, rz_old) : 0.0;
+    st.rz[l] = rz_new;
+  }
+  __syncthreads();
+  const bool finish = s_bad || s_all || it >= maxit;
+  if (finish && t < S) {
+    const size_t l = (size_t)g * S + t;
+    if (!st.conv[l]) st.iters[l] = it;  // unconverged / frozen lanes report iterations run
+  }
+  if (finish && t == 0) {
+    if (s_bad) st.status[g] = 2;
+    st.done[g] = 1;
+    atomicAdd(st.ndone, 1);
+  }
+}
+
+// p = z + beta p with z = dinv * r.
+__global__ void pcg_dir_kernel(long long N, Geo geo, PcgState st, const double* __restrict__ dinv,
+                               const double* __restrict__ r, double* __restrict__ p) {
+  const int g = blockIdx.y, t = threadIdx.x;
+  if (st.done[g]) return;
+  const int s = t % geo.Sp, rr = t / geo.Sp, S = geo.S;
+  if (s >= S) return;
+  const double beta = st.beta[(size_t)g * S + s];
+  const size_t base = (size_t)g * N * S + s;
+  for (long long tile = blockIdx.x; tile < geo.tiles; tile += geo.B) {
+    const long long row = tile * geo.R + rr;
+    if (row < N) {
+      const size_t o = base + row * S;
+      const double zv = dinv ? __dmul_rn(r[o], dinv[o]) : r[o];
+      p[o] = __dadd_rn(zv, __dmul_rn(beta, p[o]));
+    }
+  }
+}
+
+// ensemble_iterations = max over lanes (ensemble.py:277)
+__global__ void pcg_finalize_kernel(PcgState st, int G, int S, int* ens_iters) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= G) return;
+  int mx = 0;
+  for (int s = 0; s < S; ++s) mx = max(mx, st.iters[(size_t)g * S + s]);
+  ens_iters[g] = mx;
+}
+
+// ===========================================================================
+// Grouping: stable rank sort + chunk/pad (grouping.py:83-122)
+
+// rank_i = #{j : k_j < k_i or (k_j == k_i and j < i)}; order[rank_i] = i.
+// IEEE comparisons already treat -0.0 == +0.0, as numpy's stable argsort does.
+__global__ void rank_sort_kernel(const double* __restrict__ keys, int n, int* __restrict__ order,
+                                 int* status) {
+  __shared__ double tile[1024];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const double ki = i < n ? keys[i] : 0.0;
+  if (i < n && !isfinite(ki)) atomicOr(status, 2);
+  int rank = 0;
+  for (int base = 0; base < n; base += 1024) {
+    __syncthreads();
+    for (int q = threadIdx.x; q < 1024; q += blockDim.x)
+      tile[q] = base + q < n ? keys[base + q] : 0.0;
+    __syncthreads();
+    const int lim = min(1024, n - base);
+    if (i < n) {
+      for (int q = 0; q < lim; ++q) {
+        const double kj = tile[q];
+        rank += (kj < ki) || (kj == ki && base + q < i);
+      }
+    }
+  }
+  if (i < n) order[rank] = i;
+}
+
+__global__ void chunk_kernel(const int* __restrict__ order, int n, int S, int K,
+                             int* __restrict__ groups, int* __restrict__ pad) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx < (long long)K * S) {
+    const long long src = idx < n ? idx : n - 1;  // replicate the last real sample
+    groups[idx] = order ? order[src] : (int)src;
+  }
+  if (idx < K) pad[idx] = idx == K - 1 ? (int)((long long)K * S - n) : 0;
+}
+
+}  // namespace uqg

@@ -1,0 +1,63 @@
+// uqg_kernels.cuh - kernel declarations and the PCG per-group device state.
+#pragma once
+
+#include "uqg_common.cuh"
+
+namespace uqg {
+
+// Per-lane / per-group solver state living in device memory (ctx scratch), so
+// the whole PCG loop - alpha, beta, freezing, convergence, termination - is
+// decided on the device.  Lane index l = g*S + s.
+struct PcgState {
+  int G;
+  double* part;            // [G][B][NV][S] block partials
+  unsigned int* ticket;    // [G] last-block tickets
+  double* rz;              // [G*S] r.z of the current iterate
+  double* thr;             // [G*S] tol * ||b||
+  double* alpha;           // [G*S]
+  double* beta;            // [G*S]
+  int* iters;              // [G*S] -> caller's iterations_per_lane
+  unsigned char* conv;     // [G*S] -> caller's converged_per_lane
+  unsigned char* frozen;   // [G*S] -> caller's frozen_lanes
+  int* it;                 // [G] iterations run
+  int* done;               // [G] group terminated
+  int* status;             // [G] 0 ok, 2 breakdown
+  int* ndone;              // [1] number of terminated groups (host polls it)
+  double* hist;            // [(hist_cap+1)][G][S] or nullptr
+  int hist_cap;
+  int* overflow;           // [1] history capacity exceeded
+};
+
+__global__ void kl_sep2d_kernel(int n1, const double* table1d, const int* mode_p,
+                                const int* mode_q, const double* sqrt_lam, int M,
+                                const double* samples, const int* lane_ids, int G, int S,
+                                double a_min, int a_hat_mode, double a_hat_value, int expansion,
+                                double* a_out, int* status);
+__global__ void kl_table_kernel(const double* modes, int P, int M, const double* sqrt_lam,
+                                const double* samples, int L, double a_min, int a_hat_mode,
+                                double a_hat_value, int expansion, double* a_out, int* status);
+__global__ void assemble_fv2d_kernel(int n, int G, int S, const double* a_nodes, double a_y,
+                                     int a2_same, const int* row_offsets, double* vals,
+                                     double* dinv);
+__global__ void jacobi_dinv_kernel(long long N, int S, int G, long long nnz, const int* ro,
+                                   const int* ci, const double* vals, double* dinv, int* status,
+                                   int raw);
+__global__ void spmv_kernel(long long N, long long nnz, Geo geo, const int* ro, const int* ci,
+                            const double* vals, const double* x, double* y);
+__global__ void lane_dot_kernel(long long N, Geo geo, const double* a, const double* b,
+                                double* out, double* part, unsigned int* ticket);
+__global__ void pcg_init_kernel(long long N, Geo geo, PcgState st, const double* rhs,
+                                double rhs_const, const double* dinv, double tol, int maxit,
+                                double* x, double* r, double* p);
+__global__ void pcg_spmv_kernel(long long N, long long nnz, Geo geo, PcgState st, const int* ro,
+                                const int* ci, const double* vals, const double* p, double* ap);
+__global__ void pcg_update_kernel(long long N, Geo geo, PcgState st, const double* dinv,
+                                  int maxit, double* x, double* r, const double* p,
+                                  const double* ap);
+__global__ void pcg_dir_kernel(long long N, Geo geo, PcgState st, const double* dinv,
+                               const double* r, double* p);
+__global__ void pcg_finalize_kernel(PcgState st, int G, int S, int* ens_iters);
+__global__ void rank_sort_kernel(const double* keys, int n, int* order, int* status);
+__global__ void chunk_kernel(const int* order, int n, int S, int K, int* groups, int* pad);
+
+}  // namespace uqg

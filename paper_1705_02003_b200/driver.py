@@ -1,0 +1,89 @@
+"""Adaptive study loop around the device solve (host; reference ``harness.py:575-701``).
+
+Level 1 is the initial grid grouped in generation order; every later level is
+grouped by the iteration surrogate fitted through the previous level ("sur",
+``harness.py:613-629``) on the device, solved level-batched on the device, and
+its per-sample iterations and QoIs refit both surrogates before refinement.
+With ``world > 1`` the groups of each level are dealt round-robin to ranks
+(``dist.py``) and the per-sample results are allgathered before the refit -
+the only collective of the run.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field as dc_field
+
+import numpy as np
+
+from .configs import StudyConfig
+from .field import build_field
+from .grouping import group_by_key, group_natural
+from .solve import EnsembleSolver2D
+from .sparse_grid import SparseGrid
+
+QOI, ITER = "qoi", "iterations"
+
+
+@dataclass
+class LevelRecord:
+    level: int
+    ids: list
+    coords: np.ndarray
+    predicted: np.ndarray | None
+    ensembles: tuple
+    padding: tuple
+    iterations: dict
+    qois: dict
+    notes: list = dc_field(default_factory=list)
+
+
+def sample_set(cfg: StudyConfig) -> np.ndarray:
+    """Seeded synthetic U[-1,1]^M samples for configs the grid cannot reach (C5)."""
+    return np.random.default_rng(0).uniform(-1.0, 1.0, (cfg.synthetic_samples, cfg.n_modes))
+
+
+def adaptive_run(cfg: StudyConfig, solver: EnsembleSolver2D | None = None, shard=None,
+                 max_levels: int | None = None):
+    """Run the grouped adaptive loop; returns (records, stop_reason, grid).
+
+    ``shard``: optional callable(plan, coords_by_id) -> (iters, qois, notes)
+    replacing ``solver.solve_plan`` (multi-GPU sharded solve + allgather).
+    """
+    if solver is None:
+        solver = EnsembleSolver2D(build_field(**cfg.field_kwargs()), cfg.cells, cfg.tol, cfg.maxit,
+                                  cfg.a2)
+    solve = shard or solver.solve_plan
+    S = cfg.ensemble_size
+    grid = SparseGrid(cfg.n_dims if hasattr(cfg, "n_dims") else cfg.n_modes)
+    batch = grid.add_initial_levels(cfg.initial_level)
+    if len(batch) > cfg.n_max:
+        raise ValueError(f"n_max={cfg.n_max} is smaller than the {len(batch)}-point initial grid")
+    cap = cfg.max_levels if max_levels is None else max_levels
+    records, level, stop = [], 0, None
+    while True:
+        level += 1
+        start = len(grid) - len(batch)
+        ids = list(range(start, len(grid)))
+        coords = grid.node_coords()[start:]
+        coords_by_id = {sid: coords[i] for i, sid in enumerate(ids)}
+        predicted = None
+        if level == 1:
+            plan = group_natural(ids, S, level, "sur")
+        else:
+            predicted = grid.evaluate(ITER, coords, n_nodes=start)
+            plan = group_by_key(ids, {sid: float(predicted[i]) for i, sid in enumerate(ids)}, S,
+                                level, "sur")
+        iters, qois, notes = solve(plan, coords_by_id)
+        grid.fit(QOI, {sid: qois[sid] for sid in ids})
+        grid.fit(ITER, {sid: iters[sid] for sid in ids})
+        records.append(LevelRecord(level, ids, coords, predicted, plan.ensembles, plan.padding,
+                                   iters, qois, notes))
+        if level >= cap:
+            stop = "level_cap"
+            break
+        new, exhausted = grid.refine(cfg.tau, QOI, cfg.n_max)
+        if not new:
+            stop = "budget_exhausted" if exhausted else "tolerance_met"
+            break
+        batch = new
+    return records, stop, grid

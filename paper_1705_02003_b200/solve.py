@@ -1,0 +1,243 @@
+"""Level-batched device solve: the B200 replacement of ``_PdeProblem.solve_plan``.
+
+Reference (``harness.py:399-431``): for each group of a plan, assemble ->
+``ensemble_pcg`` -> QoI, one group after another, on one CPU core.
+
+Here all groups of a level (or as many as fit in HBM, "waves") are solved by
+ONE set of launches: samples [G][S][M] are uploaded once, the KL coefficient
+and the sample-interleaved operator of every group are built on the device,
+and one batched PCG runs every group to its own termination (a finished group
+turns later launches into no-ops), followed by the per-lane QoI.  Per-lane
+arithmetic and the reduction trees do not depend on G, so results are
+bit-identical to solving the groups one at a time.
+
+Only iterations, convergence flags and QoIs come back to the host; the
+first-occurrence rule for replica slots (``harness.py:427-430``) and the
+"hit maxit" notes (``harness.py:421-426``) are applied on the host.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field as dc_field
+
+import numpy as np
+
+from . import _lib
+from .ensemble import run_pcg
+from .errors import FemError
+from .fv2d import FieldTables, StructuredMesh2D, assemble_values, kl_nodes
+
+__all__ = ["LevelSolveResult", "EnsembleSolver2D"]
+
+
+@dataclass
+class LevelSolveResult:
+    iterations: np.ndarray      # (K, S) per-slot iterations
+    converged: np.ndarray       # (K, S) bool
+    frozen: np.ndarray          # (K, S) bool
+    ensemble_iterations: np.ndarray  # (K,)
+    qoi: np.ndarray             # (K, S)
+    histories: list | None = None    # per group: list of (S,) residual norms
+    waves: int = 1
+    stats: dict = dc_field(default_factory=dict)
+
+
+class EnsembleSolver2D:
+    """Device solver for one (field, mesh, solver-config) triple."""
+
+    def __init__(self, field, cells: int, tol: float = 1e-8, maxit: int = 30000,
+                 a2: str = "const", mem_fraction: float = 0.8, max_groups_per_wave: int | None = None):
+        self.field = field
+        self.mesh = StructuredMesh2D(cells)
+        self.tables = FieldTables(field, self.mesh)
+        self.tol, self.maxit, self.a2 = float(tol), int(maxit), a2
+        self.mem_fraction = mem_fraction
+        self.max_groups_per_wave = max_groups_per_wave
+        self._bufs = {}
+        self._ws = None
+
+    # -- memory planning ----------------------------------------------------
+    def bytes_per_group(self, S: int) -> int:
+        m = self.mesh
+        per = 8 * S * (m.nnz + 2 * m.n_dofs + m.n_nodes)      # vals, dinv, x, a_nodes
+        per += _lib.load().uqg_pcg_workspace_bytes(m.n_dofs, m.nnz, S, 1)  # r, p, Ap, ...
+        return int(per)
+
+    def wave_size(self, S: int, K: int) -> int:
+        torch = _lib._torch()
+        free, _ = torch.cuda.mem_get_info()
+        held = sum(t.numel() * t.element_size() for t in self._bufs.values())
+        held += 0 if self._ws is None else self._ws.numel()
+        budget = (free + held) * self.mem_fraction
+        g = max(1, int(budget // self.bytes_per_group(S)))
+        if self.max_groups_per_wave:
+            g = min(g, self.max_groups_per_wave)
+        return min(g, K)
+
+    def _buf(self, name, n, dtype):
+        torch = _lib._torch()
+        t = self._bufs.get(name)
+        if t is None or t.numel() < n or t.dtype != dtype:
+            self._bufs.pop(name, None)
+            t = torch.empty((n,), dtype=dtype, device=_lib.device())
+            self._bufs[name] = t
+        return t[:n]
+
+    def _workspace(self, G, S):
+        torch = _lib._torch()
+        m = self.mesh
+        need = int(_lib.load().uqg_pcg_workspace_bytes(m.n_dofs, m.nnz, S, G)) + (1 << 20)
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = None
+            self._ws = torch.empty((need,), dtype=torch.uint8, device=_lib.device())
+        _lib.call("uqg_ctx_set_workspace", _lib.ctx(), _lib.ptr(self._ws), self._ws.numel())
+
+    def release(self):
+        self._bufs.clear()
+        if self._ws is not None:
+            _lib.call("uqg_ctx_set_workspace", _lib.ctx(), None, 0)
+            self._ws = None
+
+    # -- solve --------------------------------------------------------------
+    def solve_wave(self, d_samples, G: int, S: int, record_history: bool = False, lane_ids=None):
+        """One batched launch set over G groups; samples already on the device.
+
+        ``lane_ids`` (device int32 [G*S]) maps lanes to rows of ``d_samples``
+        (the device grouping plan); None = rows in lane order.
+        Returns device tensors (iters, conv, frozen, ens, qoi, hist, x).
+        """
+        torch = _lib._torch()
+        m, f = self.mesh, self.field
+        a = self._buf("a", G * m.n_nodes * S, torch.float64)
+        vals = self._buf("vals", G * m.nnz * S, torch.float64)
+        dinv = self._buf("dinv", G * m.n_dofs * S, torch.float64)
+        kl_nodes(self.tables, d_samples, G, S, out=a, lane_ids=lane_ids)
+        assemble_values(m, a, G, S, f.a_y, self.a2, vals=vals, dinv=dinv)
+        rowptr, col = m.device()
+        self._workspace(G, S)
+        x, iters, conv, frz, ens, hist = run_pcg(
+            m.n_dofs, m.nnz, S, G, rowptr, col, vals, None, m.h * m.h, dinv, self.tol,
+            self.maxit, record_history)
+        q = torch.empty((G * S,), dtype=torch.float64, device=_lib.device())
+        _lib.call("uqg_lane_dot", _lib.ctx(), m.n_dofs, S, G, _lib.ptr(x), _lib.ptr(x), _lib.ptr(q),
+                  _lib.stream())
+        if _lib.status_sync() & 1:
+            raise FemError("non-positive diffusion coefficient at a mesh node")
+        return iters, conv, frz, ens, q, hist, x
+
+    def solve_groups(self, samples, record_history: bool = False) -> LevelSolveResult:
+        """samples: host (K, S, M) array or device float64 tensor of that shape."""
+        torch = _lib._torch()
+        if isinstance(samples, np.ndarray):
+            samples = np.asarray(samples, dtype=np.float64)
+            K, S, M = samples.shape
+        else:
+            K, S, M = samples.shape
+        if M != self.field.n_modes:
+            raise FemError(f"samples must have {self.field.n_modes} columns, got {M}")
+        if self.field.a_y <= 0:
+            raise FemError("non-positive diffusion coefficient a_y")
+        gw = self.wave_size(S, K)
+        out = {k: [] for k in ("it", "cv", "fz", "en", "q")}
+        hists = [] if record_history else None
+        waves = 0
+        for k0 in range(0, K, gw):
+            g = min(gw, K - k0)
+            chunk = samples[k0:k0 + g]
+            d_y = _lib.to_dev(chunk.reshape(g * S, M)) if isinstance(chunk, np.ndarray) \
+                else chunk.reshape(g * S, M).contiguous()
+            iters, conv, frz, ens, q, hist, _ = self.solve_wave(d_y, g, S, record_history)
+            out["it"].append(iters.reshape(g, S))
+            out["cv"].append(conv.reshape(g, S))
+            out["fz"].append(frz.reshape(g, S))
+            out["en"].append(ens)
+            out["q"].append(q.reshape(g, S))
+            if record_history:
+                hists.extend([[hist[r, gi].copy() for r in range(int(ens[gi].item()) + 1)]
+                              for gi in range(g)])
+            waves += 1
+        cat = {k: torch.cat(v).cpu().numpy() for k, v in out.items()}
+        return LevelSolveResult(cat["it"].astype(int), cat["cv"].astype(bool),
+                                cat["fz"].astype(bool), cat["en"].astype(int), cat["q"], hists,
+                                waves)
+
+    def run_level_device(self, d_coords, n: int, S: int, d_keys=None):
+        """The whole level on the device: group (sort + chunk) -> KL -> assemble
+        -> PCG -> QoI.  ``d_coords`` [n][M] and ``d_keys`` [n] (None = natural
+        order) are device tensors; returns device tensors
+        (groups [K*S], padding [K], iters [K*S], conv [K*S], ens [K], qoi [K*S]).
+        """
+        torch = _lib._torch()
+        from .grouping import device_group
+
+        groups, pad = device_group(n, S, d_keys)
+        K = pad.numel()
+        gw = self.wave_size(S, K)
+        parts = {k: [] for k in ("it", "cv", "en", "q")}
+        for k0 in range(0, K, gw):
+            g = min(gw, K - k0)
+            it, cv, _, en, q, _, _ = self.solve_wave(d_coords, g, S,
+                                                     lane_ids=groups[k0 * S:(k0 + g) * S])
+            parts["it"].append(it)
+            parts["cv"].append(cv)
+            parts["en"].append(en)
+            parts["q"].append(q)
+        cat = {k: (v[0] if len(v) == 1 else torch.cat(v)) for k, v in parts.items()}
+        return groups, pad, cat["it"], cat["cv"], cat["en"], cat["q"]
+
+    def solve_level(self, ids, coords, size: int, keys=None, level: int = 1, tag: str = "sur"):
+        """Public end-to-end entry: host ids / coords (n, M) / keys (n,) in,
+        grouping plan and per-sample results out - ``group_by_key`` (or
+        ``group_natural`` when ``keys`` is None) fused with ``solve_plan`` on
+        the device.  Returns (plan, iters dict, qois dict, notes).
+        """
+        from .grouping import GroupingPlan
+
+        torch = _lib._torch()
+        ids = list(ids)
+        coords = np.ascontiguousarray(coords, dtype=np.float64)
+        n = len(ids)
+        if coords.shape != (n, self.field.n_modes):
+            raise FemError(f"coords must have shape ({n}, {self.field.n_modes})")
+        dev = _lib.device()
+        h_c = torch.from_numpy(coords).pin_memory()
+        d_c = h_c.to(dev, non_blocking=True)
+        d_k = None
+        if keys is not None:
+            h_k = torch.from_numpy(np.ascontiguousarray(keys, dtype=np.float64)).pin_memory()
+            d_k = h_k.to(dev, non_blocking=True)
+        groups, pad, it, cv, en, q = self.run_level_device(d_c, n, size, d_k)
+        host = torch.cat([groups.double(), pad.double(), it.double(), cv.double(), q]).cpu().numpy()
+        K = pad.numel()
+        KS = K * size
+        g_idx = host[:KS].astype(np.int64).reshape(K, size)
+        plan = GroupingPlan(level, size, tuple(tuple(ids[j] for j in row) for row in g_idx),
+                            tuple(int(p) for p in host[KS:KS + K]), tag)
+        o = KS + K
+        res = LevelSolveResult(host[o:o + KS].astype(int).reshape(K, size),
+                               host[o + KS:o + 2 * KS].reshape(K, size) != 0, None, None,
+                               host[o + 2 * KS:o + 3 * KS].reshape(K, size))
+        iters, qois, notes = self.collect(plan, res)
+        return plan, iters, qois, notes
+
+    def solve_plan(self, plan, coords_by_id, residual_sink=None):
+        """Drop-in for ``_PdeProblem.solve_plan`` (``harness.py:399-431``)."""
+        groups = plan.ensembles
+        samples = np.array([[coords_by_id[sid] for sid in grp] for grp in groups], dtype=np.float64)
+        res = self.solve_groups(samples, record_history=residual_sink is not None)
+        return self.collect(plan, res, residual_sink)
+
+    def collect(self, plan, res: LevelSolveResult, residual_sink=None):
+        iters, qois, notes = {}, {}, []
+        for k, grp in enumerate(plan.ensembles):
+            if residual_sink is not None:
+                residual_sink(plan.level, k, res.histories[k])
+            if not res.converged[k].all():
+                bad = int((~res.converged[k]).sum())
+                notes.append(f"level {plan.level} ensemble {k}: {bad} lane(s) hit maxit "
+                             f"({self.maxit}) unconverged")
+            for s, sid in enumerate(grp):
+                if sid not in iters:
+                    iters[sid] = int(res.iterations[k, s])
+                    qois[sid] = float(res.qoi[k, s])
+        return iters, qois, notes

@@ -1,0 +1,229 @@
+"""Generate the committed golden fixtures from the REFERENCE itself.
+
+Run in the build container (where /root/reference exists):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+It imports the unmodified reference package (``/root/reference/pkg/src``) and
+its test helpers (``/root/reference/pkg/tests/_oracles.py``) and writes small
+fixtures next to this file.  Nothing at test/bench time reads /root/reference.
+
+Fixtures:
+* pcg_cases.npz     - random shared-graph SPD ensembles (reference
+                      ``random_spd_system``) with the reference's
+                      ``EnsembleCsrMatrix.spmv`` products and ``ensemble_pcg``
+                      results (solution, counts, flags, residual history);
+* special_cases.npz - the hand cases of test_ensemble.py (zero rhs, identity,
+                      diagonal, subnormal freeze) solved by the reference;
+* grouping.json     - reference ``group_by_key``/``group_natural`` plans on
+                      keys with ties, signed zeros and strings as ids;
+* eigen.npz         - reference ``eigenpairs_1d`` for the config deltas;
+* c1_adaptive.json  - the C1 study (n=64, M=3, S=8) driven by the reference's
+                      own HierGrid, group_by_key/group_natural and
+                      ensemble_pcg, with the 2D operator from oracle/fv2d.py;
+* c2_group.json     - one S=16 group at C2 (n=256) through the same path;
+* fv2d_small.npz    - oracle 2D assembly (n=8, S=3) for bitwise kernel checks.
+"""
+
+from __future__ import annotations
+
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+REPO = HERE.parents[1]
+sys.path[:0] = ["/root/reference/pkg/src", "/root/reference/pkg/tests", str(REPO)]
+
+from uqgroup import ensemble as ref_ens  # noqa: E402
+from uqgroup import grouping as ref_grp  # noqa: E402
+from uqgroup import random_field as ref_rf  # noqa: E402
+from uqgroup.hier_grid import HierGrid, RefinementPolicy  # noqa: E402
+from _oracles import random_spd_system  # noqa: E402
+
+from oracle import field2d, fv2d  # noqa: E402
+from paper_1705_02003_b200.configs import CONFIGS  # noqa: E402
+
+
+def pcg_cases():
+    rng = np.random.default_rng(20260816)
+    out = {}
+    specs = [(12, 1), (30, 4), (45, 3), (60, 8), (120, 2), (200, 8), (7, 16), (90, 5)]
+    for c, (n, width) in enumerate(specs):
+        lanes, rhs = random_spd_system(rng, n, width)
+        ens = ref_ens.EnsembleCsrMatrix.from_scipy_lanes(lanes)
+        x = rng.standard_normal((width, n))
+        tol = [1e-12, 1e-10, 1e-9, 1e-11][c % 4]
+        res = ref_ens.ensemble_pcg(ens, rhs, tol=tol, maxit=5000, record_history=True)
+        pre = f"c{c}_"
+        out.update({
+            pre + "row_offsets": ens.row_offsets, pre + "col_indices": ens.col_indices,
+            pre + "values": ens.values, pre + "rhs": rhs, pre + "x": x, pre + "Ax": ens.spmv(x),
+            pre + "tol": np.array(tol), pre + "solution": res.solution,
+            pre + "iterations": res.iterations_per_lane, pre + "converged": res.converged_per_lane,
+            pre + "frozen": res.frozen_lanes, pre + "history": np.array(res.residual_history),
+            pre + "diag": ens.diagonal(),
+        })
+    out["n_cases"] = np.array(len(specs))
+    np.savez_compressed(HERE / "pcg_cases.npz", **out)
+
+
+def special_cases():
+    out = {}
+    tiny = np.finfo(np.float64).tiny
+
+    def diag_ens(d):
+        d = np.atleast_2d(np.asarray(d, dtype=float))
+        n = d.shape[1]
+        return ref_ens.EnsembleCsrMatrix(np.arange(n + 1), np.arange(n), d.copy())
+
+    r = ref_ens.ensemble_pcg(diag_ens([[2.0, 3.0], [4.0, 5.0]]), np.zeros((2, 2)))
+    out["zero_iters"] = r.iterations_per_lane
+    rhs = np.arange(15.0).reshape(3, 5)
+    r = ref_ens.ensemble_pcg(diag_ens(np.ones((3, 5))), rhs)
+    out["ident_iters"], out["ident_x"] = r.iterations_per_lane, r.solution
+    r = ref_ens.ensemble_pcg(diag_ens([[2.0, 2.0], [0.5 * tiny, 0.5 * tiny]]), np.ones((2, 2)),
+                             precond=ref_ens.IdentityPreconditioner(), tol=1e-8, maxit=50)
+    out.update(frz_x=r.solution, frz_iters=r.iterations_per_lane, frz_conv=r.converged_per_lane,
+               frz_frozen=r.frozen_lanes)
+    r = ref_ens.ensemble_pcg(diag_ens([[2.0, 3.0]]), np.ones((1, 2)), maxit=0)
+    out["maxit0_iters"], out["maxit0_conv"] = r.iterations_per_lane, r.converged_per_lane
+    np.savez_compressed(HERE / "special_cases.npz", **out)
+
+
+def grouping_cases():
+    rng = np.random.default_rng(7)
+    cases = []
+    for n, size in [(1, 1), (5, 4), (13, 4), (64, 8), (97, 16), (300, 8), (2441, 16)]:
+        keys = np.round(rng.normal(50, 20, n))  # plenty of exact ties
+        keys[rng.random(n) < 0.05] = 0.0
+        keys[rng.random(n) < 0.05] = -0.0
+        ids = list(rng.permutation(10 * n)[:n].tolist())
+        kmap = {i: float(k) for i, k in zip(ids, keys)}
+        p1 = ref_grp.group_by_key(ids, kmap, size, level=2, tag="sur")
+        p2 = ref_grp.group_natural(ids, size, level=2)
+        cases.append({"ids": ids, "keys": [float(k) for k in keys], "size": size,
+                      "by_key": [list(g) for g in p1.ensembles], "by_key_pad": list(p1.padding),
+                      "natural": [list(g) for g in p2.ensembles],
+                      "natural_pad": list(p2.padding)})
+    sids = ["a", "b", "c", "d"]
+    p = ref_grp.group_by_key(sids, {"a": 5.0, "b": 1.0, "c": 3.0, "d": 2.0}, 2)
+    cases.append({"ids": sids, "keys": [5.0, 1.0, 3.0, 2.0], "size": 2,
+                  "by_key": [list(g) for g in p.ensembles], "by_key_pad": list(p.padding),
+                  "natural": [["a", "b"], ["c", "d"]], "natural_pad": [0, 0]})
+    (HERE / "grouping.json").write_text(json.dumps(cases))
+
+
+def eigen_cases():
+    out = {}
+    for delta in (0.2, 0.1, 0.05, 0.25):
+        pairs = ref_rf.eigenpairs_1d(delta, 12, 513)
+        out[f"lam_{delta}"] = np.array([p.eigenvalue for p in pairs])
+        out[f"vec_{delta}"] = np.stack([p.values for p in pairs])
+    np.savez_compressed(HERE / "eigen.npz", **out)
+
+
+def reference_study(cfg, max_levels=None):
+    """The reference's adaptive loop (harness.py:604-701, exec plan 'sur') on the 2D operator."""
+    fld = field2d.KL2D.select(**{k: v for k, v in cfg.field_kwargs().items()})
+    mesh = fv2d.Mesh2D(cfg.cells)
+    table = fld.mode_table(mesh.node_points)
+    S = cfg.ensemble_size
+    grid = HierGrid(cfg.n_modes)
+    batch = grid.add_initial_levels(cfg.initial_level)
+    policy = RefinementPolicy(tau=cfg.tau, channel="qoi", max_points=cfg.n_max)
+    cap = cfg.max_levels if max_levels is None else max_levels
+    levels, level = [], 0
+    while True:
+        level += 1
+        start = len(grid) - len(batch)
+        ids = list(range(start, len(grid)))
+        coords = grid.node_coords()[start:]
+        coords_by_id = {sid: coords[i] for i, sid in enumerate(ids)}
+        predicted = None
+        if level == 1:
+            plan = ref_grp.group_natural(ids, S, level, "sur")
+        else:
+            predicted = grid.eval_many("iterations", coords, n_nodes=start)
+            plan = ref_grp.group_by_key(ids, {sid: float(predicted[i]) for i, sid in enumerate(ids)},
+                                        S, level, "sur")
+        iters, qois, ens_iters = {}, {}, []
+        for group in plan.ensembles:
+            ys = np.array([coords_by_id[sid] for sid in group])
+            sysm = fv2d.assemble(mesh, fld, ys, table, cfg.a2)
+            mat = ref_ens.EnsembleCsrMatrix(sysm.row_offsets, sysm.col_indices, sysm.values)
+            res = ref_ens.ensemble_pcg(mat, sysm.rhs, tol=cfg.tol, maxit=cfg.maxit)
+            ens_iters.append(int(res.ensemble_iterations))
+            for s, sid in enumerate(group):
+                if sid not in iters:
+                    iters[sid] = int(res.iterations_per_lane[s])
+                    qois[sid] = float(np.dot(res.solution[s], res.solution[s]))
+        nodes = grid.nodes[start:]
+        grid.compute_surpluses("qoi", {nd: qois[sid] for nd, sid in zip(nodes, ids)})
+        grid.compute_surpluses("iterations", {nd: iters[sid] for nd, sid in zip(nodes, ids)})
+        levels.append({
+            "level": level, "ids": ids, "coords": coords.tolist(),
+            "predicted": None if predicted is None else predicted.tolist(),
+            "ensembles": [list(g) for g in plan.ensembles], "padding": list(plan.padding),
+            "iterations": [iters[sid] for sid in ids], "qoi": [qois[sid] for sid in ids],
+            "ensemble_iterations": ens_iters,
+        })
+        print(f"  level {level}: {len(ids)} samples, {len(plan.ensembles)} groups", flush=True)
+        if level >= cap:
+            break
+        out = grid.refine(policy)
+        if not out.new_nodes:
+            break
+        batch = out.new_nodes
+    return {"config": cfg.to_dict(), "levels": levels}
+
+
+def c2_group():
+    cfg = CONFIGS["C2"]
+    fld = field2d.KL2D.select(**cfg.field_kwargs())
+    mesh = fv2d.Mesh2D(cfg.cells)
+    grid = HierGrid(cfg.n_modes)
+    grid.add_initial_levels(1)
+    ys = grid.node_coords()[:cfg.ensemble_size]
+    sysm = fv2d.assemble(mesh, fld, ys, None, cfg.a2)
+    mat = ref_ens.EnsembleCsrMatrix(sysm.row_offsets, sysm.col_indices, sysm.values)
+    res = ref_ens.ensemble_pcg(mat, sysm.rhs, tol=cfg.tol, maxit=cfg.maxit)
+    doc = {"config": cfg.to_dict(), "samples": ys.tolist(),
+           "iterations": res.iterations_per_lane.tolist(),
+           "ensemble_iterations": int(res.ensemble_iterations),
+           "qoi": [float(np.dot(u, u)) for u in res.solution],
+           "center_value": [float(u[mesh.n_dofs // 2]) for u in res.solution]}
+    (HERE / "c2_group.json").write_text(json.dumps(doc))
+
+
+def fv2d_small():
+    fld = field2d.KL2D.select(0.2, 1.0, 3, 0.0)
+    mesh = fv2d.Mesh2D(8)
+    ys = np.array([[0.5, -0.25, 1.0], [-1.0, 1.0, 0.0], [0.5, -0.25, 1.0]])
+    a = fld.coeff(mesh.node_points, ys)
+    np.savez_compressed(HERE / "fv2d_small.npz", samples=ys, a_nodes=a,
+                        values=fv2d.assemble_values(mesh, a, 1.0),
+                        values_same=fv2d.assemble_values(mesh, a, 1.0, "same"),
+                        row_offsets=mesh.row_offsets, col_indices=mesh.col_indices)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["pcg", "special", "grouping", "eigen", "fv2d", "c1", "c2"]
+    if "pcg" in which:
+        pcg_cases()
+    if "special" in which:
+        special_cases()
+    if "grouping" in which:
+        grouping_cases()
+    if "eigen" in which:
+        eigen_cases()
+    if "fv2d" in which:
+        fv2d_small()
+    if "c1" in which:
+        doc = reference_study(CONFIGS["C1"])
+        (HERE / "c1_adaptive.json").write_text(json.dumps(doc))
+    if "c2" in which:
+        c2_group()
+    print("golden fixtures written to", HERE)
