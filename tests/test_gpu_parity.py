@@ -86,7 +86,10 @@ def test_pcg_matches_reference_golden(pcg_golden):
         hist = np.array(r.residual_history)
         assert hist.shape == c["history"].shape
         np.testing.assert_allclose(hist[0], c["history"][0], rtol=1e-14)
-        np.testing.assert_allclose(hist, c["history"], rtol=1e-6, atol=1e-300)
+        # residual norms agree to rounding relative to ||b|| (the last entries of a
+        # lane that converged far past tol are pure rounding noise in both codes)
+        scale = c["history"][0][None, :]
+        assert np.all(np.abs(hist - c["history"]) <= 1e-9 * scale + 1e-6 * np.abs(c["history"]))
 
 
 def test_trivial_systems(special_golden):
