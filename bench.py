@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--wave", type=int, default=None,
+                    help="max groups per device wave (default: as many as fit in HBM)")
     return ap.parse_args()
 
 
@@ -262,7 +264,8 @@ def main():
     if needs_build():
         build()
     field = uq.build_field(**cfg.field_kwargs())
-    solver = uq.EnsembleSolver2D(field, cfg.cells, cfg.tol, cfg.maxit, cfg.a2)
+    solver = uq.EnsembleSolver2D(field, cfg.cells, cfg.tol, cfg.maxit, cfg.a2,
+                                 max_groups_per_wave=args.wave)
     ids, coords, keys, meta = make_workload(cfg, solver)
     # weak scaling: rank r solves the mirror images of the level's samples and
     # groups them by the keys of their originals (same sort work, same costs shape)

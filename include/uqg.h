@@ -113,8 +113,11 @@ int uqg_diagonal(uqg_ctx* ctx, int N, int nnz, int S, int G, const int* row_offs
                  const int* col_indices, const double* vals, double* diag, void* stream);
 
 /* y = A x per lane, sequential CSR order without FMA: bitwise equal to scipy
- * csr_matvec per lane (EnsembleCsrMatrix.spmv, ensemble.py:116-128). */
-int uqg_spmv(uqg_ctx* ctx, int N, int nnz, int S, int G, const int* row_offsets,
+ * csr_matvec per lane (EnsembleCsrMatrix.spmv, ensemble.py:116-128).
+ * max_row_len: longest row of the graph if known (selects the unrolled row
+ * kernel: <=5 e.g. the 2D 5-point stencil, <=8), 0 = unknown; any value gives
+ * identical results. */
+int uqg_spmv(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const int* row_offsets,
              const int* col_indices, const double* vals, const double* x, double* y,
              void* stream);
 
@@ -132,8 +135,9 @@ int uqg_lane_dot(uqg_ctx* ctx, int N, int S, int G, const double* a, const doubl
  *   hist_host: NULL, or host buffer [(hist_cap+1)][G][S] receiving the lane
  *   residual norms per iteration (row 0 = ||b||); *hist_rows_host = rows used.
  * Runs the whole loop on the device; the host only polls a done-counter.
+ * max_row_len as for uqg_spmv.
  * Returns UQG_EBREAKDOWN on a non-finite residual in an active lane. */
-int uqg_pcg(uqg_ctx* ctx, int N, int nnz, int S, int G, const int* row_offsets,
+int uqg_pcg(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const int* row_offsets,
             const int* col_indices, const double* vals, const double* rhs, double rhs_const,
             const double* dinv, double tol, int maxit, double* x, int* iters,
             unsigned char* converged, unsigned char* frozen, int* ens_iters,

@@ -40,9 +40,9 @@ SIGNATURES = {
                                    _p]),
     "uqg_jacobi_dinv": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _p, _p, _p, _p, _p]),
     "uqg_diagonal": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _p, _p, _p, _p, _p]),
-    "uqg_spmv": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _p, _p, _p, _p, _p, _p]),
+    "uqg_spmv": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _c_int, _p, _p, _p, _p, _p, _p]),
     "uqg_lane_dot": (_c_int, [_p, _c_int, _c_int, _c_int, _p, _p, _p, _p]),
-    "uqg_pcg": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _p, _p, _p, _p, _c_double, _p,
+    "uqg_pcg": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _c_int, _p, _p, _p, _p, _c_double, _p,
                          _c_double, _c_int, _p, _p, _p, _p, _p, _p, _c_int,
                          ctypes.POINTER(_c_int), _p]),
     "uqg_pcg_workspace_bytes": (_c_ll, [_c_int, _c_int, _c_int, _c_int]),

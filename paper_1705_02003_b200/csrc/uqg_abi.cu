@@ -332,24 +332,23 @@ int uqg_diagonal(uqg_ctx* ctx, int N, int nnz, int S, int G, const int* row_offs
   return UQG_OK;
 }
 
-int uqg_spmv(uqg_ctx* ctx, int N, int nnz, int S, int G, const int* row_offsets,
-             const int* col_indices, const double* vals, const double* x, double* y,
-             void* stream) {
+int uqg_spmv(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G,
+             const int* row_offsets, const int* col_indices, const double* vals, const double* x,
+             double* y, void* stream) {
   UQG_REQUIRE(ctx && row_offsets && x && y, "uqg_spmv: NULL argument");
-  UQG_REQUIRE(N >= 0 && nnz >= 0 && S >= 1 && S <= 1024 && G >= 1, "uqg_spmv: bad sizes");
+  UQG_REQUIRE(N >= 0 && nnz >= 0 && S >= 1 && S <= kMaxLanes && G >= 1, "uqg_spmv: bad sizes");
   if (N == 0) return UQG_OK;
-  Geo geo = make_geo(N, S);
+  Geo geo = make_geo(N, S, max_row_len);
   cudaStream_t s = as_stream(stream);
   UQG_LAUNCH(UQG_K_SPMV, s,
-             spmv_kernel<<<dim3(geo.B, G), geo.T, 0, s>>>(N, nnz, geo, row_offsets, col_indices,
-                                                          vals, x, y));
+             launch_spmv(geo, G, s, N, nnz, row_offsets, col_indices, vals, x, y));
   return UQG_OK;
 }
 
 int uqg_lane_dot(uqg_ctx* ctx, int N, int S, int G, const double* a, const double* b,
                  double* out, void* stream) {
   UQG_REQUIRE(ctx && a && b && out, "uqg_lane_dot: NULL argument");
-  UQG_REQUIRE(N >= 0 && S >= 1 && S <= 1024 && G >= 1, "uqg_lane_dot: bad sizes");
+  UQG_REQUIRE(N >= 0 && S >= 1 && S <= kMaxLanes && G >= 1, "uqg_lane_dot: bad sizes");
   cudaStream_t s = as_stream(stream);
   Geo geo = make_geo(N, S);
   size_t need = (size_t)G * geo.B * geo.S * sizeof(double) + (size_t)G * sizeof(unsigned) + 1024;
@@ -359,9 +358,7 @@ int uqg_lane_dot(uqg_ctx* ctx, int N, int S, int G, const double* a, const doubl
   double* part = c.take<double>((size_t)G * geo.B * geo.S);
   unsigned* ticket = c.take<unsigned>(G);
   UQG_TRY_CUDA(cudaMemsetAsync(ticket, 0, G * sizeof(unsigned), s));
-  UQG_LAUNCH(UQG_K_DOT, s,
-             lane_dot_kernel<<<dim3(geo.B, G), geo.T, geo.T * sizeof(double), s>>>(
-                 N, geo, a, b, out, part, ticket));
+  UQG_LAUNCH(UQG_K_DOT, s, launch_lane_dot(geo, G, s, N, a, b, out, part, ticket));
   return UQG_OK;
 }
 
@@ -373,19 +370,19 @@ long long uqg_pcg_workspace_bytes(int N, int nnz, int S, int G) {
   return (long long)pcg_layout(c, N, geo, G, nullptr, nullptr, nullptr, nullptr);
 }
 
-int uqg_pcg(uqg_ctx* ctx, int N, int nnz, int S, int G, const int* row_offsets,
+int uqg_pcg(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const int* row_offsets,
             const int* col_indices, const double* vals, const double* rhs, double rhs_const,
             const double* dinv, double tol, int maxit, double* x, int* iters,
             unsigned char* converged, unsigned char* frozen, int* ens_iters,
             double* hist_host, int hist_cap, int* hist_rows_host, void* stream) {
   UQG_REQUIRE(ctx && row_offsets && x && iters && converged && frozen && ens_iters,
               "uqg_pcg: NULL argument");
-  UQG_REQUIRE(N >= 0 && nnz >= 0 && S >= 1 && S <= 1024 && G >= 1, "uqg_pcg: bad sizes");
+  UQG_REQUIRE(N >= 0 && nnz >= 0 && S >= 1 && S <= kMaxLanes && G >= 1, "uqg_pcg: bad sizes");
   UQG_REQUIRE(tol > 0.0 && tol <= 1.7976931348623157e308, "tol must be positive and finite");
   UQG_REQUIRE(maxit >= 0, "maxit must be >= 0");
   UQG_REQUIRE(!hist_host || (hist_cap >= 0 && hist_rows_host), "uqg_pcg: bad history buffer");
   cudaStream_t s = as_stream(stream);
-  Geo geo = make_geo(N, S);
+  Geo geo = make_geo(N, S, max_row_len);
   Carver probe{nullptr};
   size_t need = pcg_layout(probe, N, geo, G, nullptr, nullptr, nullptr, nullptr);
   size_t hist_elems = hist_host ? (size_t)(hist_cap + 1) * G * S : 0;
@@ -405,11 +402,8 @@ int uqg_pcg(uqg_ctx* ctx, int N, int nnz, int S, int G, const int* row_offsets,
   UQG_TRY_CUDA(cudaMemsetAsync(st.ndone, 0, sizeof(int), s));
   UQG_TRY_CUDA(cudaMemsetAsync(st.overflow, 0, sizeof(int), s));
 
-  const dim3 grid(geo.B, G);
-  const size_t smem2 = 2 * geo.T * sizeof(double), smem1 = geo.T * sizeof(double);
   UQG_LAUNCH(UQG_K_PCG_INIT, s,
-             pcg_init_kernel<<<grid, geo.T, smem2, s>>>(N, geo, st, rhs, rhs_const, dinv, tol,
-                                                        maxit, x, r, p));
+             launch_pcg_init(geo, G, s, N, st, rhs, rhs_const, dinv, tol, maxit, x, r, p));
   // Host polls the device done-counter between chunks of iterations.  Groups
   // that have terminated turn every later launch into a no-op, so the extra
   // launches of the last chunk cannot change any result.
@@ -430,19 +424,14 @@ int uqg_pcg(uqg_ctx* ctx, int N, int nnz, int S, int G, const int* row_offsets,
     }
     for (int k = 0; k < chunk; ++k) {
       UQG_LAUNCH(UQG_K_PCG_SPMV, s,
-                 pcg_spmv_kernel<<<grid, geo.T, smem1, s>>>(N, nnz, geo, st, row_offsets,
-                                                            col_indices, vals, p, ap));
-      UQG_LAUNCH(UQG_K_PCG_UPDATE, s,
-                 pcg_update_kernel<<<grid, geo.T, smem2, s>>>(N, geo, st, dinv, maxit, x, r, p,
-                                                              ap));
-      UQG_LAUNCH(UQG_K_PCG_DIR, s,
-                 pcg_dir_kernel<<<grid, geo.T, 0, s>>>(N, geo, st, dinv, r, p));
+                 launch_pcg_spmv(geo, G, s, N, nnz, st, row_offsets, col_indices, vals, p, ap));
+      UQG_LAUNCH(UQG_K_PCG_UPDATE, s, launch_pcg_update(geo, G, s, N, st, dinv, maxit, r, ap));
+      UQG_LAUNCH(UQG_K_PCG_DIR, s, launch_pcg_dir(geo, G, s, N, st, dinv, r, x, p));
     }
     launched += chunk;
     chunk = std::min(chunk * 2, 64);
   }
-  UQG_LAUNCH(UQG_K_OTHER, s,
-             pcg_finalize_kernel<<<(G + 127) / 128, 128, 0, s>>>(st, G, S, ens_iters));
+  UQG_LAUNCH(UQG_K_OTHER, s, launch_pcg_finalize(G, S, s, st, ens_iters));
   // breakdown / history bookkeeping
   std::vector<int> h_status(G);
   cudaError_t e =

@@ -1,9 +1,10 @@
-// uqg_common.cuh - shared geometry, error state and the deterministic
-// per-lane reduction used by every kernel of libuqg.so.
+// uqg_common.cuh - shared geometry, error state, vector access and the
+// deterministic per-lane reduction used by every kernel of libuqg.so.
 #pragma once
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <string>
 
@@ -43,31 +44,49 @@ void set_error(const std::string& msg);
 // ---------------------------------------------------------------------------
 // Launch geometry for lane-interleaved ensemble data.
 //
-// A block of T threads covers a "tile" of R = T / Sp consecutive rows; thread t
-// owns lane s = t % Sp of row tile*R + t / Sp (lanes >= S idle).  Sp is S
-// rounded up to a power of two so the per-lane reduction tree is a clean
-// binary tree.  Each group gets B blocks that grid-stride over its tiles.
-// B depends only on (N, S) - never on the number of groups or GPUs - so every
-// lane's reduction tree, and hence every result bit, is independent of how
-// groups are batched or sharded (hard part 2).
+// Each thread owns V consecutive lanes (V = 2 when S is even: one 16-byte
+// load per access, else V = 1) of one row; L = S / V threads cover a row,
+// rounded up to the power of two Lp so the per-lane reduction tree is a clean
+// binary tree.  A block of T threads covers a "tile" of R = T / Lp rows; each
+// group gets B blocks that grid-stride over its tiles.  V, Lp, R and B depend
+// only on (N, S) - never on the number of groups or GPUs - so every lane's
+// reduction tree, and hence every result bit, is independent of how groups
+// are batched or sharded (hard part 2).
 constexpr int kMaxBlocksPerGroup = 1184;  // 148 SMs x 8 resident 256-thread CTAs
+constexpr int kMaxLanes = 512;            // S <= 512 keeps Lp <= 256 = block size
 
 struct Geo {
   int S;          // lanes per group
-  int Sp;         // S rounded up to a power of two
+  int V;          // lanes per thread (1 or 2)
+  int L;          // threads per row = S / V
+  int Lp;         // L rounded up to a power of two
   int T;          // threads per block
   int R;          // rows per tile
   long long tiles;
   int B;          // blocks per group
+  int maxrow;     // longest graph row if known (0 = unknown): picks the unrolled SpMV
 };
 
-inline Geo make_geo(long long N, int S) {
+// UQG_LANES_PER_THREAD=1 forces V = 1 (tuning experiments only; V changes the
+// reduction tree, so results are reproducible per setting, not across them).
+inline int forced_v() {
+  static const int v = [] {
+    const char* e = getenv("UQG_LANES_PER_THREAD");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+inline Geo make_geo(long long N, int S, int maxrow = 0) {
   Geo g;
   g.S = S;
-  g.Sp = 1;
-  while (g.Sp < S) g.Sp <<= 1;
-  g.T = g.Sp > 256 ? g.Sp : 256;
-  g.R = g.T / g.Sp;
+  g.maxrow = maxrow;
+  g.V = (S % 2 == 0 && forced_v() != 1) ? 2 : 1;
+  g.L = S / g.V;
+  g.Lp = 1;
+  while (g.Lp < g.L) g.Lp <<= 1;
+  g.T = g.Lp > 256 ? g.Lp : 256;
+  g.R = g.T / g.Lp;
   g.tiles = (N + g.R - 1) / g.R;
   long long b = g.tiles < kMaxBlocksPerGroup ? g.tiles : kMaxBlocksPerGroup;
   g.B = b < 1 ? 1 : (int)b;
@@ -75,40 +94,81 @@ inline Geo make_geo(long long N, int S) {
 }
 
 // ---------------------------------------------------------------------------
+// V-lane vector access (16-byte loads/stores for V = 2).
+
+template <int V>
+__device__ __forceinline__ void ldv(const double* p, double (&o)[V]) {
+  if constexpr (V == 2) {
+    const double2 t = *reinterpret_cast<const double2*>(p);
+    o[0] = t.x;
+    o[1] = t.y;
+  } else {
+    o[0] = *p;
+  }
+}
+
+// read-only path (matrix values, dinv): non-coherent cache
+template <int V>
+__device__ __forceinline__ void ldgv(const double* p, double (&o)[V]) {
+  if constexpr (V == 2) {
+    const double2 t = __ldg(reinterpret_cast<const double2*>(p));
+    o[0] = t.x;
+    o[1] = t.y;
+  } else {
+    o[0] = __ldg(p);
+  }
+}
+
+template <int V>
+__device__ __forceinline__ void stv(double* p, const double (&o)[V]) {
+  if constexpr (V == 2) {
+    *reinterpret_cast<double2*>(p) = make_double2(o[0], o[1]);
+  } else {
+    *p = o[0];
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Deterministic per-lane block reduction + "last block finishes" pattern.
 //
-// Every block reduces NV per-thread values over its rows (fixed binary tree in
-// shared memory), writes one partial per (group, block, value, lane), and takes
-// a ticket.  The block that draws the last ticket sums the B partials of each
-// lane in a fixed order (strided sequential sums, then the same binary tree)
-// and returns true with the totals in red[v*T + s].  No floating-point atomics:
-// the result is a pure function of the inputs.
+// Every block reduces NV x V per-thread values over its rows (fixed binary
+// tree in shared memory), writes one partial per (group, block, value, lane),
+// and takes a ticket.  The block that draws the last ticket sums the B
+// partials of each lane in a fixed order (strided sequential sums, then the
+// same binary tree) and returns true with the total of value v, lane V*sl+j in
+// red[(v*V + j)*T + sl].  No floating-point atomics: the result is a pure
+// function of the inputs.
 
-template <int NV>
-__device__ __forceinline__ void tree_rows(double* red, int T, int Sp, int R, int t) {
+template <int NS>
+__device__ __forceinline__ void tree_rows(double* red, int T, int Lp, int R, int t) {
   for (int st = R >> 1; st > 0; st >>= 1) {
-    if ((t / Sp) < st) {
+    if ((t / Lp) < st) {
 #pragma unroll
-      for (int v = 0; v < NV; ++v) red[v * T + t] += red[v * T + t + st * Sp];
+      for (int v = 0; v < NS; ++v) red[v * T + t] += red[v * T + t + st * Lp];
     }
     __syncthreads();
   }
 }
 
-template <int NV>
-__device__ bool reduce_lanes(const double (&val)[NV], double* red, double* part,
+template <int NV, int V>
+__device__ bool reduce_lanes(const double (&val)[NV][V], double* red, double* part,
                              unsigned int* ticket, int g, const Geo& geo) {
+  constexpr int NS = NV * V;
   const int t = threadIdx.x;
-  const int T = geo.T, Sp = geo.Sp, R = geo.R, S = geo.S, B = geo.B;
+  const int T = geo.T, Lp = geo.Lp, R = geo.R, L = geo.L, S = geo.S, B = geo.B;
   const int b = blockIdx.x;
 #pragma unroll
-  for (int v = 0; v < NV; ++v) red[v * T + t] = val[v];
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int j = 0; j < V; ++j) red[(v * V + j) * T + t] = val[v][j];
   __syncthreads();
-  tree_rows<NV>(red, T, Sp, R, t);
-  if (t < S) {
+  tree_rows<NS>(red, T, Lp, R, t);
+  if (t < L) {
 #pragma unroll
     for (int v = 0; v < NV; ++v)
-      part[(((size_t)g * B + b) * NV + v) * S + t] = red[v * T + t];
+#pragma unroll
+      for (int j = 0; j < V; ++j)
+        part[(((size_t)g * B + b) * NV + v) * S + V * t + j] = red[(v * V + j) * T + t];
   }
   __shared__ int s_last;
   __threadfence();
@@ -120,23 +180,39 @@ __device__ bool reduce_lanes(const double (&val)[NV], double* red, double* part,
   __syncthreads();
   if (!s_last) return false;
   __threadfence();
-  const int s = t % Sp, j = t / Sp;
-  double acc[NV];
+  const int sl = t % Lp, jr = t / Lp;
+  double acc[NS];
 #pragma unroll
-  for (int v = 0; v < NV; ++v) acc[v] = 0.0;
-  if (s < S) {
-    for (int bb = j; bb < B; bb += R) {
+  for (int v = 0; v < NS; ++v) acc[v] = 0.0;
+  if (sl < L) {
+    for (int bb = jr; bb < B; bb += R) {
 #pragma unroll
       for (int v = 0; v < NV; ++v)
-        acc[v] += __ldcg(&part[(((size_t)g * B + bb) * NV + v) * S + s]);
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+          acc[v * V + j] += __ldcg(&part[(((size_t)g * B + bb) * NV + v) * S + V * sl + j]);
     }
   }
 #pragma unroll
-  for (int v = 0; v < NV; ++v) red[v * T + t] = acc[v];
+  for (int v = 0; v < NS; ++v) red[v * T + t] = acc[v];
   __syncthreads();
-  tree_rows<NV>(red, T, Sp, R, t);
+  tree_rows<NS>(red, T, Lp, R, t);
   if (t == 0) ticket[g] = 0u;  // ready for the next reduction on this counter
   return true;
+}
+
+// "last block of the group" without values (for state transitions).
+__device__ __forceinline__ bool last_block(unsigned int* ticket, int g, int B) {
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned int tk = atomicAdd(&ticket[g], 1u);
+    s_last = (tk == (unsigned)(B - 1));
+    if (s_last) ticket[g] = 0u;
+  }
+  __syncthreads();
+  return s_last;
 }
 
 }  // namespace uqg

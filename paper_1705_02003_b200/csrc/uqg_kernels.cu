@@ -160,239 +160,6 @@ __global__ void jacobi_dinv_kernel(long long N, int S, int G, long long nnz,
 }
 
 // ===========================================================================
-// SpMV.  Per (row, lane): acc = 0; acc = acc + v_k * x_{c_k} in CSR order with
-// separate roundings - scipy's csr_matvec order, so lanes match it bitwise.
-
-__device__ __forceinline__ double row_dot(const int* __restrict__ ci, const double* __restrict__ v,
-                                          const double* __restrict__ x, int k0, int k1, int S) {
-  double acc = 0.0;
-  for (int k = k0; k < k1; ++k) {
-    const int c = __ldg(&ci[k]);
-    acc = __dadd_rn(acc, __dmul_rn(__ldg(&v[(size_t)k * S]), x[(size_t)c * S]));
-  }
-  return acc;
-}
-
-__global__ void spmv_kernel(long long N, long long nnz, Geo geo, const int* __restrict__ ro,
-                            const int* __restrict__ ci, const double* __restrict__ vals,
-                            const double* __restrict__ x, double* __restrict__ y) {
-  const int g = blockIdx.y, t = threadIdx.x;
-  const int s = t % geo.Sp, rr = t / geo.Sp, S = geo.S;
-  if (s >= S) return;
-  const double* vg = vals + (size_t)g * nnz * S + s;
-  const double* xg = x + (size_t)g * N * S + s;
-  double* yg = y + (size_t)g * N * S + s;
-  for (long long tile = blockIdx.x; tile < geo.tiles; tile += geo.B) {
-    const long long row = tile * geo.R + rr;
-    if (row < N) yg[row * S] = row_dot(ci, vg, xg, __ldg(&ro[row]), __ldg(&ro[row + 1]), S);
-  }
-}
-
-// out[g][s] = sum_j a*b (lane_dot / qoi); fused multiply-add in the reduction
-// (reduction order is implementation-defined in the reference too).
-__global__ void lane_dot_kernel(long long N, Geo geo, const double* __restrict__ a,
-                                const double* __restrict__ b, double* __restrict__ out,
-                                double* part, unsigned int* ticket) {
-  extern __shared__ double red[];
-  const int g = blockIdx.y, t = threadIdx.x;
-  const int s = t % geo.Sp, rr = t / geo.Sp, S = geo.S;
-  double acc[1] = {0.0};
-  if (s < S) {
-    const double* ag = a + (size_t)g * N * S + s;
-    const double* bg = b + (size_t)g * N * S + s;
-    for (long long tile = blockIdx.x; tile < geo.tiles; tile += geo.B) {
-      const long long row = tile * geo.R + rr;
-      if (row < N) acc[0] = __fma_rn(ag[row * S], bg[row * S], acc[0]);
-    }
-  }
-  if (reduce_lanes<1>(acc, red, part, ticket, g, geo) && t < S) out[(size_t)g * S + t] = red[t];
-}
-
-// ===========================================================================
-// Ensemble PCG (ensemble.py:205-281).  Per-group device state:
-
-__global__ void pcg_init_kernel(long long N, Geo geo, PcgState st, const double* __restrict__ rhs,
-                                double rhs_const, const double* __restrict__ dinv, double tol,
-                                int maxit, double* __restrict__ x, double* __restrict__ r,
-                                double* __restrict__ p) {
-  extern __shared__ double red[];
-  const int g = blockIdx.y, t = threadIdx.x;
-  const int s = t % geo.Sp, rr = t / geo.Sp, S = geo.S;
-  double acc[2] = {0.0, 0.0};  // b.b, r.z
-  if (s < S) {
-    const size_t base = (size_t)g * N * S + s;
-    for (long long tile = blockIdx.x; tile < geo.tiles; tile += geo.B) {
-      const long long row = tile * geo.R + rr;
-      if (row < N) {
-        const size_t o = base + row * S;
-        const double bv = rhs ? rhs[o] : rhs_const;
-        const double zv = dinv ? __dmul_rn(bv, dinv[o]) : bv;
-        x[o] = 0.0;
-        r[o] = bv;
-        p[o] = zv;
-        acc[0] = __fma_rn(bv, bv, acc[0]);
-        acc[1] = __fma_rn(bv, zv, acc[1]);
-      }
-    }
-  }
-  if (!reduce_lanes<2>(acc, red, st.part, st.ticket, g, geo)) return;
-  __shared__ int s_all;
-  if (t == 0) s_all = 1;
-  __syncthreads();
-  if (t < S) {
-    const size_t l = (size_t)g * S + t;
-    const double bn = sqrt(red[t]);
-    const double thr = tol * bn;
-    const bool conv = bn <= thr;  // zero right-hand sides converge at iteration 0
-    st.thr[l] = thr;
-    st.rz[l] = red[geo.T + t];
-    st.conv[l] = conv;
-    st.frozen[l] = 0;
-    st.iters[l] = 0;
-    if (st.hist) st.hist[l] = bn;
-    if (!conv) s_all = 0;
-  }
-  __syncthreads();
-  if (t == 0) {
-    st.it[g] = 0;
-    st.status[g] = 0;
-    const int done = s_all || maxit == 0;
-    st.done[g] = done;
-    if (done) atomicAdd(st.ndone, 1);
-  }
-  if (t < S) {
-    // iterations[~converged] = it (=0) already; converged lanes have 0 too.
-  }
-}
-
-// Ap = A p, partial p.Ap; the last block freezes lanes and forms alpha.
-__global__ void pcg_spmv_kernel(long long N, long long nnz, Geo geo, PcgState st,
-                                const int* __restrict__ ro, const int* __restrict__ ci,
-                                const double* __restrict__ vals, const double* __restrict__ p,
-                                double* __restrict__ ap) {
-  extern __shared__ double red[];
-  const int g = blockIdx.y, t = threadIdx.x;
-  if (st.done[g]) return;
-  const int s = t % geo.Sp, rr = t / geo.Sp, S = geo.S;
-  double acc[1] = {0.0};
-  if (s < S) {
-    const double* vg = vals + (size_t)g * nnz * S + s;
-    const size_t base = (size_t)g * N * S + s;
-    const double* pg = p + base;
-    for (long long tile = blockIdx.x; tile < geo.tiles; tile += geo.B) {
-      const long long row = tile * geo.R + rr;
-      if (row < N) {
-        const double y = row_dot(ci, vg, pg, __ldg(&ro[row]), __ldg(&ro[row + 1]), S);
-        ap[base + row * S] = y;
-        acc[0] = __fma_rn(pg[row * S], y, acc[0]);
-      }
-    }
-  }
-  if (!reduce_lanes<1>(acc, red, st.part, st.ticket, g, geo)) return;
-  if (t < S) {
-    const size_t l = (size_t)g * S + t;
-    const double pap = red[t];
-    const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
-    st.frozen[l] = fr;
-    st.alpha[l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
-  }
-  if (t == 0) st.it[g] += 1;
-}
-
-// x += alpha p; r -= alpha Ap; partial r.r and r.z with z = dinv*r.
-// The last block tests convergence / breakdown / termination and forms beta.
-__global__ void pcg_update_kernel(long long N, Geo geo, PcgState st, const double* __restrict__ dinv,
-                                  int maxit, double* __restrict__ x, double* __restrict__ r,
-                                  const double* __restrict__ p, const double* __restrict__ ap) {
-  extern __shared__ double red[];
-  const int g = blockIdx.y, t = threadIdx.x;
-  if (st.done[g]) return;
-  const int s = t % geo.Sp, rr = t / geo.Sp, S = geo.S;
-  double acc[2] = {0.0, 0.0};
-  if (s < S) {
-    const double alpha = st.alpha[(size_t)g * S + s];
-    const size_t base = (size_t)g * N * S + s;
-    for (long long tile = blockIdx.x; tile < geo.tiles; tile += geo.B) {
-      const long long row = tile * geo.R + rr;
-      if (row < N) {
-        const size_t o = base + row * S;
-        x[o] = __dadd_rn(x[o], __dmul_rn(alpha, p[o]));
-        const double rv = __dsub_rn(r[o], __dmul_rn(alpha, ap[o]));
-        r[o] = rv;
-        const double zv = dinv ? __dmul_rn(rv, dinv[o]) : rv;
-        acc[0] = __fma_rn(rv, rv, acc[0]);
-        acc[1] = __fma_rn(rv, zv, acc[1]);
-      }
-    }
-  }
-  if (!reduce_lanes<2>(acc, red, st.part, st.ticket, g, geo)) return;
-  __shared__ int s_all, s_bad;
-  if (t == 0) { s_all = 1; s_bad = 0; }
-  __syncthreads();
-  const int it = st.it[g];
-  if (t < S) {
-    const size_t l = (size_t)g * S + t;
-    const double rn = sqrt(red[t]);
-    const double rz_new = red[geo.T + t];
-    if (st.hist) {
-      if (it <= st.hist_cap) st.hist[(size_t)it * st.G * S + l] = rn;
-      else atomicOr(st.overflow, 1);
-    }
-    const bool live = !st.frozen[l];
-    if (live && !isfinite(rn)) atomicOr(&s_bad, 1);
-    bool conv = st.conv[l];
-    if (live && !conv && rn <= st.thr[l]) {
-      st.iters[l] = it;
-      st.conv[l] = 1;
-      conv = true;
-    }
-    if (!(conv || !live)) atomicAnd(&s_all, 0);
-    const double rz_old = st.rz[l];
-    st.beta[l] = (live && rz_old > 0.0) ? __ddiv_rn(rz_new, rz_old) : 0.0;
-    st.rz[l] = rz_new;
-  }
-  __syncthreads();
-  const bool finish = s_bad || s_all || it >= maxit;
-  if (finish && t < S) {
-    const size_t l = (size_t)g * S + t;
-    if (!st.conv[l]) st.iters[l] = it;  // unconverged / frozen lanes report iterations run
-  }
-  if (finish && t == 0) {
-    if (s_bad) st.status[g] = 2;
-    st.done[g] = 1;
-    atomicAdd(st.ndone, 1);
-  }
-}
-
-// p = z + beta p with z = dinv * r.
-__global__ void pcg_dir_kernel(long long N, Geo geo, PcgState st, const double* __restrict__ dinv,
-                               const double* __restrict__ r, double* __restrict__ p) {
-  const int g = blockIdx.y, t = threadIdx.x;
-  if (st.done[g]) return;
-  const int s = t % geo.Sp, rr = t / geo.Sp, S = geo.S;
-  if (s >= S) return;
-  const double beta = st.beta[(size_t)g * S + s];
-  const size_t base = (size_t)g * N * S + s;
-  for (long long tile = blockIdx.x; tile < geo.tiles; tile += geo.B) {
-    const long long row = tile * geo.R + rr;
-    if (row < N) {
-      const size_t o = base + row * S;
-      const double zv = dinv ? __dmul_rn(r[o], dinv[o]) : r[o];
-      p[o] = __dadd_rn(zv, __dmul_rn(beta, p[o]));
-    }
-  }
-}
-
-// ensemble_iterations = max over lanes (ensemble.py:277)
-__global__ void pcg_finalize_kernel(PcgState st, int G, int S, int* ens_iters) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= G) return;
-  int mx = 0;
-  for (int s = 0; s < S; ++s) mx = max(mx, st.iters[(size_t)g * S + s]);
-  ens_iters[g] = mx;
-}
-
-// ===========================================================================
 // Grouping: stable rank sort + chunk/pad (grouping.py:83-122)
 
 // rank_i = #{j : k_j < k_i or (k_j == k_i and j < i)}; order[rank_i] = i.

@@ -1,9 +1,14 @@
-// uqg_kernels.cuh - kernel declarations and the PCG per-group device state.
+// uqg_kernels.cuh - kernel declarations, launchers and the PCG per-group state.
 #pragma once
 
 #include "uqg_common.cuh"
 
 namespace uqg {
+
+// group states of the device PCG loop
+constexpr int kRunning = 0;
+constexpr int kFinishing = 1;  // terminated; pcg_dir still owes the last x update
+constexpr int kDone = 2;
 
 // Per-lane / per-group solver state living in device memory (ctx scratch), so
 // the whole PCG loop - alpha, beta, freezing, convergence, termination - is
@@ -20,14 +25,15 @@ struct PcgState {
   unsigned char* conv;     // [G*S] -> caller's converged_per_lane
   unsigned char* frozen;   // [G*S] -> caller's frozen_lanes
   int* it;                 // [G] iterations run
-  int* done;               // [G] group terminated
+  int* done;               // [G] kRunning / kFinishing / kDone
   int* status;             // [G] 0 ok, 2 breakdown
-  int* ndone;              // [1] number of terminated groups (host polls it)
+  int* ndone;              // [1] number of DONE groups (host polls it)
   double* hist;            // [(hist_cap+1)][G][S] or nullptr
   int hist_cap;
   int* overflow;           // [1] history capacity exceeded
 };
 
+// uqg_kernels.cu: KL coefficient, assembly, diagonal, grouping
 __global__ void kl_sep2d_kernel(int n1, const double* table1d, const int* mode_p,
                                 const int* mode_q, const double* sqrt_lam, int M,
                                 const double* samples, const int* lane_ids, int G, int S,
@@ -42,22 +48,24 @@ __global__ void assemble_fv2d_kernel(int n, int G, int S, const double* a_nodes,
 __global__ void jacobi_dinv_kernel(long long N, int S, int G, long long nnz, const int* ro,
                                    const int* ci, const double* vals, double* dinv, int* status,
                                    int raw);
-__global__ void spmv_kernel(long long N, long long nnz, Geo geo, const int* ro, const int* ci,
-                            const double* vals, const double* x, double* y);
-__global__ void lane_dot_kernel(long long N, Geo geo, const double* a, const double* b,
-                                double* out, double* part, unsigned int* ticket);
-__global__ void pcg_init_kernel(long long N, Geo geo, PcgState st, const double* rhs,
-                                double rhs_const, const double* dinv, double tol, int maxit,
-                                double* x, double* r, double* p);
-__global__ void pcg_spmv_kernel(long long N, long long nnz, Geo geo, PcgState st, const int* ro,
-                                const int* ci, const double* vals, const double* p, double* ap);
-__global__ void pcg_update_kernel(long long N, Geo geo, PcgState st, const double* dinv,
-                                  int maxit, double* x, double* r, const double* p,
-                                  const double* ap);
-__global__ void pcg_dir_kernel(long long N, Geo geo, PcgState st, const double* dinv,
-                               const double* r, double* p);
-__global__ void pcg_finalize_kernel(PcgState st, int G, int S, int* ens_iters);
 __global__ void rank_sort_kernel(const double* keys, int n, int* order, int* status);
 __global__ void chunk_kernel(const int* order, int n, int S, int K, int* groups, int* pad);
+
+// uqg_pcg.cu: launchers of the V-templated streaming kernels
+void launch_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long long nnz, const int* ro,
+                 const int* ci, const double* vals, const double* x, double* y);
+void launch_lane_dot(const Geo& geo, int G, cudaStream_t s, long long N, const double* a,
+                     const double* b, double* out, double* part, unsigned* ticket);
+void launch_pcg_init(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,
+                     const double* rhs, double rhs_const, const double* dinv, double tol,
+                     int maxit, double* x, double* r, double* p);
+void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long long nnz,
+                     const PcgState& st, const int* ro, const int* ci, const double* vals,
+                     const double* p, double* ap);
+void launch_pcg_update(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,
+                       const double* dinv, int maxit, double* r, const double* ap);
+void launch_pcg_dir(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,
+                    const double* dinv, const double* r, double* x, double* p);
+void launch_pcg_finalize(int G, int S, cudaStream_t s, const PcgState& st, int* ens_iters);
 
 }  // namespace uqg

@@ -109,6 +109,12 @@ class EnsembleCsrMatrix:
     def width(self) -> int:
         return self._width
 
+    @property
+    def max_row_len(self) -> int:
+        if self.n_rows == 0:
+            return 0
+        return int(np.diff(self.row_offsets).max())
+
     # -- storage ------------------------------------------------------------
     def device(self):
         """(rowptr, col, vals[nnz][S]) device tensors, uploaded on first use."""
@@ -136,7 +142,8 @@ class EnsembleCsrMatrix:
         ro, ci, vals = self.device()
         dx = _lib.lanes_to_dev(x)
         dy = dx.new_empty(dx.shape)
-        _lib.call("uqg_spmv", _lib.ctx(), self.n_rows, self.nnz, self.width, 1, _lib.ptr(ro),
+        _lib.call("uqg_spmv", _lib.ctx(), self.n_rows, self.nnz, self.max_row_len, self.width, 1,
+                  _lib.ptr(ro),
                   _lib.ptr(ci), _lib.ptr(vals), _lib.ptr(dx), _lib.ptr(dy), _lib.stream())
         return _lib.dev_to_lanes(dy, self.width, self.n_rows)
 
@@ -254,7 +261,7 @@ def _as_matrix(mat) -> EnsembleCsrMatrix:
 
 
 def run_pcg(N, nnz, S, G, d_rowptr, d_col, d_vals, d_rhs, rhs_const, d_dinv, tol, maxit,
-            record_history=False):
+            record_history=False, max_row_len=0):
     """Batched device PCG over G groups; returns device/host result pieces."""
     torch = _lib._torch()
     dev = _lib.device()
@@ -268,7 +275,7 @@ def run_pcg(N, nnz, S, G, d_rowptr, d_col, d_vals, d_rhs, rhs_const, d_dinv, tol
         hist = np.empty(((cap + 1) * G * S,)) if record_history else None
         rows = ctypes.c_int(0)
         rc = _lib.load().uqg_pcg(
-            _lib.ctx(), N, nnz, S, G, _lib.ptr(d_rowptr), _lib.ptr(d_col), _lib.ptr(d_vals),
+            _lib.ctx(), N, nnz, int(max_row_len), S, G, _lib.ptr(d_rowptr), _lib.ptr(d_col), _lib.ptr(d_vals),
             _lib.ptr(d_rhs), float(rhs_const), _lib.ptr(d_dinv), float(tol), int(maxit),
             _lib.ptr(x), _lib.ptr(iters), _lib.ptr(conv), _lib.ptr(frz), _lib.ptr(ens),
             hist.ctypes.data if hist is not None else None, cap, ctypes.byref(rows), _lib.stream())
@@ -304,7 +311,7 @@ def ensemble_pcg(mat, rhs, precond=None, tol: float = 1e-7, maxit: int = 1000,
     ro, ci, vals = mat.device()
     d_b = _lib.lanes_to_dev(b)
     x, iters, conv, frz, ens, hist = run_pcg(n, mat.nnz, S, 1, ro, ci, vals, d_b, 0.0, d_dinv,
-                                             tol, maxit, record_history)
+                                             tol, maxit, record_history, mat.max_row_len)
     history = None
     if record_history:
         history = [hist[k, 0].copy() for k in range(hist.shape[0])]

@@ -117,7 +117,7 @@ class EnsembleSolver2D:
         self._workspace(G, S)
         x, iters, conv, frz, ens, hist = run_pcg(
             m.n_dofs, m.nnz, S, G, rowptr, col, vals, None, m.h * m.h, dinv, self.tol,
-            self.maxit, record_history)
+            self.maxit, record_history, max_row_len=5)
         q = torch.empty((G * S,), dtype=torch.float64, device=_lib.device())
         _lib.call("uqg_lane_dot", _lib.ctx(), m.n_dofs, S, G, _lib.ptr(x), _lib.ptr(x), _lib.ptr(q),
                   _lib.stream())

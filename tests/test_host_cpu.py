@@ -43,7 +43,7 @@ def test_library_is_sm100a_cubin():
 
 def test_null_args_rejected_without_device():
     lib = _lib.load()
-    rc = lib.uqg_spmv(None, 10, 10, 2, 1, None, None, None, None, None, None)
+    rc = lib.uqg_spmv(None, 10, 10, 0, 2, 1, None, None, None, None, None, None)
     assert rc == _lib.UQG_EINVAL and "NULL" in _lib.last_error()
 
 
