@@ -141,7 +141,7 @@ size_t pcg_layout(Carver& c, long long N, const Geo& geo, int G, PcgState* st, d
   double* aa = c.take<double>(vec);
   PcgState s{};
   s.G = G;
-  s.part = c.take<double>((size_t)G * geo.B * 2 * geo.S);
+  s.part = c.take<double>((size_t)G * geo.chunks * 2 * geo.S);
   s.ticket = c.take<unsigned int>(G);
   s.rz = c.take<double>(lanes);
   s.thr = c.take<double>(lanes);
@@ -351,11 +351,11 @@ int uqg_lane_dot(uqg_ctx* ctx, int N, int S, int G, const double* a, const doubl
   UQG_REQUIRE(N >= 0 && S >= 1 && S <= kMaxLanes && G >= 1, "uqg_lane_dot: bad sizes");
   cudaStream_t s = as_stream(stream);
   Geo geo = make_geo(N, S);
-  size_t need = (size_t)G * geo.B * geo.S * sizeof(double) + (size_t)G * sizeof(unsigned) + 1024;
+  size_t need = (size_t)G * geo.chunks * geo.S * sizeof(double) + (size_t)G * sizeof(unsigned) + 1024;
   int rc = ensure_ws(ctx, need);
   if (rc) return rc;
   Carver c{(char*)ws_base(ctx, need)};
-  double* part = c.take<double>((size_t)G * geo.B * geo.S);
+  double* part = c.take<double>((size_t)G * geo.chunks * geo.S);
   unsigned* ticket = c.take<unsigned>(G);
   UQG_TRY_CUDA(cudaMemsetAsync(ticket, 0, G * sizeof(unsigned), s));
   UQG_LAUNCH(UQG_K_DOT, s, launch_lane_dot(geo, G, s, N, a, b, out, part, ticket));

@@ -47,13 +47,19 @@ void set_error(const std::string& msg);
 // Each thread owns V consecutive lanes (V = 2 when S is even: one 16-byte
 // load per access, else V = 1) of one row; L = S / V threads cover a row,
 // rounded up to the power of two Lp so the per-lane reduction tree is a clean
-// binary tree.  A block of T threads covers a "tile" of R = T / Lp rows; each
-// group gets B blocks that grid-stride over its tiles.  V, Lp, R and B depend
-// only on (N, S) - never on the number of groups or GPUs - so every lane's
-// reduction tree, and hence every result bit, is independent of how groups
-// are batched or sharded (hard part 2).
-constexpr int kMaxBlocksPerGroup = 1184;  // 148 SMs x 8 resident 256-thread CTAs
-constexpr int kMaxLanes = 512;            // S <= 512 keeps Lp <= 256 = block size
+// binary tree.  A block of T threads covers a "tile" of R = T / Lp rows.
+//
+// Reductions are organised by CHUNKS of consecutive tiles: every chunk yields
+// one per-lane partial (fixed in-block tree), and the partials of a group are
+// summed in chunk order.  V, Lp, R, the chunk size and the chunk count depend
+// only on (N, S) - never on the number of groups, blocks or GPUs - so every
+// lane's reduction tree, and hence every result bit, is independent of how
+// groups are batched or sharded (hard part 2).  The number of
+// blocks per group (each grid-strides over chunks) is then free to be sized
+// for occupancy at launch time.
+constexpr int kMaxChunks = 512;        // partials per group and reduction
+constexpr int kTargetBlocks = 2368;    // ~2 waves of 148 SMs x 8 resident CTAs
+constexpr int kMaxLanes = 512;         // S <= 512 keeps Lp <= 256 = block size
 
 struct Geo {
   int S;          // lanes per group
@@ -63,7 +69,9 @@ struct Geo {
   int T;          // threads per block
   int R;          // rows per tile
   long long tiles;
-  int B;          // blocks per group
+  long long chunk_tiles;  // tiles per reduction chunk
+  int chunks;     // reduction chunks per group (<= kMaxChunks)
+  int B;          // blocks per group in the launch (set by with_groups)
   int maxrow;     // longest graph row if known (0 = unknown): picks the unrolled SpMV
 };
 
@@ -88,7 +96,21 @@ inline Geo make_geo(long long N, int S, int maxrow = 0) {
   g.T = g.Lp > 256 ? g.Lp : 256;
   g.R = g.T / g.Lp;
   g.tiles = (N + g.R - 1) / g.R;
-  long long b = g.tiles < kMaxBlocksPerGroup ? g.tiles : kMaxBlocksPerGroup;
+  if (g.tiles < 1) g.tiles = 1;
+  // aim for >= 64 chunks of <= 8 tiles (small N), at most kMaxChunks (large N)
+  long long ct = g.tiles / 64;
+  ct = ct < 1 ? 1 : (ct > 8 ? 8 : ct);
+  if ((g.tiles + ct - 1) / ct > kMaxChunks) ct = (g.tiles + kMaxChunks - 1) / kMaxChunks;
+  g.chunk_tiles = ct;
+  g.chunks = (int)((g.tiles + ct - 1) / ct);
+  g.B = g.chunks;
+  return g;
+}
+
+// Blocks per group for a launch over G groups: fill ~2 waves of the GPU.
+inline Geo with_groups(Geo g, int G) {
+  long long b = (kTargetBlocks + G - 1) / (G < 1 ? 1 : G);
+  if (b > g.chunks) b = g.chunks;
   g.B = b < 1 ? 1 : (int)b;
   return g;
 }
@@ -129,15 +151,15 @@ __device__ __forceinline__ void stv(double* p, const double (&o)[V]) {
 }
 
 // ---------------------------------------------------------------------------
-// Deterministic per-lane block reduction + "last block finishes" pattern.
+// Deterministic per-lane chunk reduction + "last chunk finishes" pattern.
 //
-// Every block reduces NV x V per-thread values over its rows (fixed binary
-// tree in shared memory), writes one partial per (group, block, value, lane),
-// and takes a ticket.  The block that draws the last ticket sums the B
-// partials of each lane in a fixed order (strided sequential sums, then the
-// same binary tree) and returns true with the total of value v, lane V*sl+j in
-// red[(v*V + j)*T + sl].  No floating-point atomics: the result is a pure
-// function of the inputs.
+// For one chunk, the block reduces NV x V per-thread values over the chunk's
+// rows (fixed binary tree in shared memory), writes one partial per (group,
+// chunk, value, lane), and takes a ticket.  The block that completes the last
+// chunk of the group sums the chunk partials of each lane in a fixed order
+// (strided sequential sums, then the same binary tree) and returns true with
+// the total of value v, lane V*sl+j in red[(v*V + j)*T + sl].  No
+// floating-point atomics: the result is a pure function of the inputs.
 
 template <int NS>
 __device__ __forceinline__ void tree_rows(double* red, int T, int Lp, int R, int t) {
@@ -152,11 +174,11 @@ __device__ __forceinline__ void tree_rows(double* red, int T, int Lp, int R, int
 
 template <int NV, int V>
 __device__ bool reduce_lanes(const double (&val)[NV][V], double* red, double* part,
-                             unsigned int* ticket, int g, const Geo& geo) {
+                             unsigned int* ticket, int g, int chunk, const Geo& geo) {
   constexpr int NS = NV * V;
   const int t = threadIdx.x;
-  const int T = geo.T, Lp = geo.Lp, R = geo.R, L = geo.L, S = geo.S, B = geo.B;
-  const int b = blockIdx.x;
+  const int T = geo.T, Lp = geo.Lp, R = geo.R, L = geo.L, S = geo.S, C = geo.chunks;
+  __syncthreads();  // red[] may still be read by the previous chunk's tree
 #pragma unroll
   for (int v = 0; v < NV; ++v)
 #pragma unroll
@@ -168,14 +190,14 @@ __device__ bool reduce_lanes(const double (&val)[NV][V], double* red, double* pa
     for (int v = 0; v < NV; ++v)
 #pragma unroll
       for (int j = 0; j < V; ++j)
-        part[(((size_t)g * B + b) * NV + v) * S + V * t + j] = red[(v * V + j) * T + t];
+        part[(((size_t)g * C + chunk) * NV + v) * S + V * t + j] = red[(v * V + j) * T + t];
   }
   __shared__ int s_last;
   __threadfence();
   __syncthreads();
   if (t == 0) {
     unsigned int tk = atomicAdd(&ticket[g], 1u);
-    s_last = (tk == (unsigned)(B - 1));
+    s_last = (tk == (unsigned)(C - 1));
   }
   __syncthreads();
   if (!s_last) return false;
@@ -185,12 +207,13 @@ __device__ bool reduce_lanes(const double (&val)[NV][V], double* red, double* pa
 #pragma unroll
   for (int v = 0; v < NS; ++v) acc[v] = 0.0;
   if (sl < L) {
-    for (int bb = jr; bb < B; bb += R) {
+#pragma unroll 4
+    for (int cc = jr; cc < C; cc += R) {
 #pragma unroll
       for (int v = 0; v < NV; ++v)
 #pragma unroll
         for (int j = 0; j < V; ++j)
-          acc[v * V + j] += __ldcg(&part[(((size_t)g * B + bb) * NV + v) * S + V * sl + j]);
+          acc[v * V + j] += __ldcg(&part[(((size_t)g * C + cc) * NV + v) * S + V * sl + j]);
     }
   }
 #pragma unroll

@@ -3,9 +3,9 @@
 //
 // One PCG iteration = three streaming kernels over every active group:
 //   pcg_spmv   Ap = A p (CSR order, no FMA: bitwise scipy), p.Ap
-//              last block: freeze (p.Ap <= DBL_MIN), alpha
+//              last chunk: freeze (p.Ap <= DBL_MIN), alpha
 //   pcg_update r -= alpha Ap, r.r and r.z (z = dinv r)
-//              last block: residual norm, history, breakdown, convergence,
+//              last chunk: residual norm, history, breakdown, convergence,
 //              termination, beta
 //   pcg_dir    x += alpha p ; p = z + beta p
 // x's update is deferred from pcg_update to pcg_dir (same operands, same
@@ -13,6 +13,9 @@
 // and pcg_dir 6 instead of 4.  A group that terminates in pcg_update is in
 // state FINISHING; its pcg_dir applies the last x update only and moves it to
 // DONE.  A DONE group turns every later launch into a no-op.
+//
+// Work distribution: blocks of group g (blockIdx.y) grid-stride over the
+// group's reduction chunks (consecutive tiles of rows); see Geo.
 
 #include <cuda_runtime.h>
 #include <float.h>
@@ -65,6 +68,18 @@ __device__ __forceinline__ void row_spmv(const int* __restrict__ ci, const doubl
   }
 }
 
+// rows [r0, r1) of a chunk for this thread: row = tile * R + rr
+struct ChunkRows {
+  long long t0, t1;
+};
+
+__device__ __forceinline__ ChunkRows chunk_tiles(const Geo& geo, int chunk) {
+  const long long t0 = (long long)chunk * geo.chunk_tiles;
+  long long t1 = t0 + geo.chunk_tiles;
+  if (t1 > geo.tiles) t1 = geo.tiles;
+  return {t0, t1};
+}
+
 // ---------------------------------------------------------------------------
 
 template <int V, int ML>
@@ -81,12 +96,15 @@ __global__ void __launch_bounds__(256) spmv_kernel(long long N, long long nnz, G
   const double* vg = vals + (size_t)g * nnz * S + o;
   const double* xg = x + (size_t)g * N * S + o;
   double* yg = y + (size_t)g * N * S + o;
-  for (long long tile = blockIdx.x; tile < geo.tiles; tile += geo.B) {
-    const long long row = tile * geo.R + rr;
-    if (row < N) {
-      double acc[V];
-      row_spmv<V, ML>(ci, vg, xg, __ldg(&ro[row]), __ldg(&ro[row + 1]), S, acc);
-      stv<V>(yg + row * S, acc);
+  for (int chunk = blockIdx.x; chunk < geo.chunks; chunk += gridDim.x) {
+    const ChunkRows cr = chunk_tiles(geo, chunk);
+    for (long long tile = cr.t0; tile < cr.t1; ++tile) {
+      const long long row = tile * geo.R + rr;
+      if (row < N) {
+        double acc[V];
+        row_spmv<V, ML>(ci, vg, xg, __ldg(&ro[row]), __ldg(&ro[row + 1]), S, acc);
+        stv<V>(yg + row * S, acc);
+      }
     }
   }
 }
@@ -100,23 +118,26 @@ __global__ void __launch_bounds__(256) lane_dot_kernel(long long N, Geo geo,
   extern __shared__ double red[];
   const int g = blockIdx.y, t = threadIdx.x;
   const int sl = t % geo.Lp, rr = t / geo.Lp, S = geo.S;
-  double acc[1][V] = {};
-  if (sl < geo.L) {
-    const size_t base = (size_t)g * N * S + V * sl;
-    for (long long tile = blockIdx.x; tile < geo.tiles; tile += geo.B) {
-      const long long row = tile * geo.R + rr;
-      if (row < N) {
-        double av[V], bv[V];
-        ldv<V>(a + base + row * S, av);
-        ldv<V>(b + base + row * S, bv);
+  const size_t base = (size_t)g * N * S + V * sl;
+  for (int chunk = blockIdx.x; chunk < geo.chunks; chunk += gridDim.x) {
+    double acc[1][V] = {};
+    if (sl < geo.L) {
+      const ChunkRows cr = chunk_tiles(geo, chunk);
+      for (long long tile = cr.t0; tile < cr.t1; ++tile) {
+        const long long row = tile * geo.R + rr;
+        if (row < N) {
+          double av[V], bv[V];
+          ldv<V>(a + base + row * S, av);
+          ldv<V>(b + base + row * S, bv);
 #pragma unroll
-        for (int j = 0; j < V; ++j) acc[0][j] = __fma_rn(av[j], bv[j], acc[0][j]);
+          for (int j = 0; j < V; ++j) acc[0][j] = __fma_rn(av[j], bv[j], acc[0][j]);
+        }
       }
     }
-  }
-  if (reduce_lanes<1, V>(acc, red, part, ticket, g, geo) && t < geo.L) {
+    if (reduce_lanes<1, V>(acc, red, part, ticket, g, chunk, geo) && t < geo.L) {
 #pragma unroll
-    for (int j = 0; j < V; ++j) out[(size_t)g * S + V * t + j] = red[j * geo.T + t];
+      for (int j = 0; j < V; ++j) out[(size_t)g * S + V * t + j] = red[j * geo.T + t];
+    }
   }
 }
 
@@ -135,68 +156,71 @@ __global__ void __launch_bounds__(256) pcg_init_kernel(long long N, Geo geo, Pcg
   extern __shared__ double red[];
   const int g = blockIdx.y, t = threadIdx.x;
   const int sl = t % geo.Lp, rr = t / geo.Lp, S = geo.S;
-  double acc[2][V] = {};  // b.b, r.z
-  if (sl < geo.L) {
-    const size_t base = (size_t)g * N * S + V * sl;
-    for (long long tile = blockIdx.x; tile < geo.tiles; tile += geo.B) {
-      const long long row = tile * geo.R + rr;
-      if (row < N) {
-        const size_t o = base + row * S;
-        double bv[V], zv[V], zero[V];
-        if (rhs) {
-          ldv<V>(rhs + o, bv);
-        } else {
+  const size_t base = (size_t)g * N * S + V * sl;
+  for (int chunk = blockIdx.x; chunk < geo.chunks; chunk += gridDim.x) {
+    double acc[2][V] = {};  // b.b, r.z
+    if (sl < geo.L) {
+      const ChunkRows cr = chunk_tiles(geo, chunk);
+      for (long long tile = cr.t0; tile < cr.t1; ++tile) {
+        const long long row = tile * geo.R + rr;
+        if (row < N) {
+          const size_t o = base + row * S;
+          double bv[V], zv[V], zero[V];
+          if (rhs) {
+            ldv<V>(rhs + o, bv);
+          } else {
 #pragma unroll
-          for (int j = 0; j < V; ++j) bv[j] = rhs_const;
+            for (int j = 0; j < V; ++j) bv[j] = rhs_const;
+          }
+          if (dinv) {
+            double dv[V];
+            ldgv<V>(dinv + o, dv);
+#pragma unroll
+            for (int j = 0; j < V; ++j) zv[j] = __dmul_rn(bv[j], dv[j]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < V; ++j) zv[j] = bv[j];
+          }
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            zero[j] = 0.0;
+            acc[0][j] = __fma_rn(bv[j], bv[j], acc[0][j]);
+            acc[1][j] = __fma_rn(bv[j], zv[j], acc[1][j]);
+          }
+          stv<V>(x + o, zero);
+          stv<V>(r + o, bv);
+          stv<V>(p + o, zv);
         }
-        if (dinv) {
-          double dv[V];
-          ldgv<V>(dinv + o, dv);
-#pragma unroll
-          for (int j = 0; j < V; ++j) zv[j] = __dmul_rn(bv[j], dv[j]);
-        } else {
-#pragma unroll
-          for (int j = 0; j < V; ++j) zv[j] = bv[j];
-        }
-#pragma unroll
-        for (int j = 0; j < V; ++j) {
-          zero[j] = 0.0;
-          acc[0][j] = __fma_rn(bv[j], bv[j], acc[0][j]);
-          acc[1][j] = __fma_rn(bv[j], zv[j], acc[1][j]);
-        }
-        stv<V>(x + o, zero);
-        stv<V>(r + o, bv);
-        stv<V>(p + o, zv);
       }
     }
-  }
-  if (!reduce_lanes<2, V>(acc, red, st.part, st.ticket, g, geo)) return;
-  __shared__ int s_all;
-  if (t == 0) s_all = 1;
-  __syncthreads();
-  if (t < geo.L) {
+    if (!reduce_lanes<2, V>(acc, red, st.part, st.ticket, g, chunk, geo)) continue;
+    __shared__ int s_all;
+    if (t == 0) s_all = 1;
+    __syncthreads();
+    if (t < geo.L) {
 #pragma unroll
-    for (int j = 0; j < V; ++j) {
-      const size_t l = (size_t)g * S + V * t + j;
-      const double bn = sqrt(red[j * geo.T + t]);
-      const double thr = tol * bn;
-      const bool conv = bn <= thr;  // zero right-hand sides converge at iteration 0
-      st.thr[l] = thr;
-      st.rz[l] = red[(V + j) * geo.T + t];
-      st.conv[l] = conv;
-      st.frozen[l] = 0;
-      st.iters[l] = 0;
-      if (st.hist) st.hist[l] = bn;
-      if (!conv) s_all = 0;
+      for (int j = 0; j < V; ++j) {
+        const size_t l = (size_t)g * S + V * t + j;
+        const double bn = sqrt(red[j * geo.T + t]);
+        const double thr = tol * bn;
+        const bool conv = bn <= thr;  // zero right-hand sides converge at iteration 0
+        st.thr[l] = thr;
+        st.rz[l] = red[(V + j) * geo.T + t];
+        st.conv[l] = conv;
+        st.frozen[l] = 0;
+        st.iters[l] = 0;
+        if (st.hist) st.hist[l] = bn;
+        if (!conv) s_all = 0;
+      }
     }
-  }
-  __syncthreads();
-  if (t == 0) {
-    st.it[g] = 0;
-    st.status[g] = 0;
-    const int done = s_all || maxit == 0;  // x = 0 is final: no pending update
-    st.done[g] = done ? kDone : kRunning;
-    if (done) atomicAdd(st.ndone, 1);
+    __syncthreads();
+    if (t == 0) {
+      st.it[g] = 0;
+      st.status[g] = 0;
+      const int done = s_all || maxit == 0;  // x = 0 is final: no pending update
+      st.done[g] = done ? kDone : kRunning;
+      if (done) atomicAdd(st.ndone, 1);
+    }
   }
 }
 
@@ -211,35 +235,38 @@ __global__ void __launch_bounds__(256) pcg_spmv_kernel(long long N, long long nn
   const int g = blockIdx.y, t = threadIdx.x;
   if (st.done[g] != kRunning) return;
   const int sl = t % geo.Lp, rr = t / geo.Lp, S = geo.S;
-  double acc[1][V] = {};
-  if (sl < geo.L) {
-    const double* vg = vals + (size_t)g * nnz * S + V * sl;
-    const size_t base = (size_t)g * N * S + V * sl;
-    const double* pg = p + base;
-    for (long long tile = blockIdx.x; tile < geo.tiles; tile += geo.B) {
-      const long long row = tile * geo.R + rr;
-      if (row < N) {
-        double y[V], pv[V];
-        row_spmv<V, ML>(ci, vg, pg, __ldg(&ro[row]), __ldg(&ro[row + 1]), S, y);
-        stv<V>(ap + base + row * S, y);
-        ldv<V>(pg + row * S, pv);
+  const double* vg = vals + (size_t)g * nnz * S + V * sl;
+  const size_t base = (size_t)g * N * S + V * sl;
+  const double* pg = p + base;
+  for (int chunk = blockIdx.x; chunk < geo.chunks; chunk += gridDim.x) {
+    double acc[1][V] = {};
+    if (sl < geo.L) {
+      const ChunkRows cr = chunk_tiles(geo, chunk);
+      for (long long tile = cr.t0; tile < cr.t1; ++tile) {
+        const long long row = tile * geo.R + rr;
+        if (row < N) {
+          double y[V], pv[V];
+          row_spmv<V, ML>(ci, vg, pg, __ldg(&ro[row]), __ldg(&ro[row + 1]), S, y);
+          stv<V>(ap + base + row * S, y);
+          ldv<V>(pg + row * S, pv);
 #pragma unroll
-        for (int j = 0; j < V; ++j) acc[0][j] = __fma_rn(pv[j], y[j], acc[0][j]);
+          for (int j = 0; j < V; ++j) acc[0][j] = __fma_rn(pv[j], y[j], acc[0][j]);
+        }
       }
     }
-  }
-  if (!reduce_lanes<1, V>(acc, red, st.part, st.ticket, g, geo)) return;
-  if (t < geo.L) {
+    if (!reduce_lanes<1, V>(acc, red, st.part, st.ticket, g, chunk, geo)) continue;
+    if (t < geo.L) {
 #pragma unroll
-    for (int j = 0; j < V; ++j) {
-      const size_t l = (size_t)g * S + V * t + j;
-      const double pap = red[j * geo.T + t];
-      const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
-      st.frozen[l] = fr;
-      st.alpha[l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
+      for (int j = 0; j < V; ++j) {
+        const size_t l = (size_t)g * S + V * t + j;
+        const double pap = red[j * geo.T + t];
+        const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
+        st.frozen[l] = fr;
+        st.alpha[l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
+      }
     }
+    if (t == 0) st.it[g] += 1;
   }
-  if (t == 0) st.it[g] += 1;
 }
 
 template <int V>
@@ -251,83 +278,86 @@ __global__ void __launch_bounds__(256) pcg_update_kernel(long long N, Geo geo, P
   const int g = blockIdx.y, t = threadIdx.x;
   if (st.done[g] != kRunning) return;
   const int sl = t % geo.Lp, rr = t / geo.Lp, S = geo.S;
-  double acc[2][V] = {};
-  if (sl < geo.L) {
-    double alpha[V];
+  const size_t base = (size_t)g * N * S + V * sl;
+  double alpha[V];
 #pragma unroll
-    for (int j = 0; j < V; ++j) alpha[j] = st.alpha[(size_t)g * S + V * sl + j];
-    const size_t base = (size_t)g * N * S + V * sl;
-    for (long long tile = blockIdx.x; tile < geo.tiles; tile += geo.B) {
-      const long long row = tile * geo.R + rr;
-      if (row < N) {
-        const size_t o = base + row * S;
-        double rv[V], av[V], zv[V];
-        ldv<V>(r + o, rv);
-        ldv<V>(ap + o, av);
+  for (int j = 0; j < V; ++j) alpha[j] = sl < geo.L ? st.alpha[(size_t)g * S + V * sl + j] : 0.0;
+  for (int chunk = blockIdx.x; chunk < geo.chunks; chunk += gridDim.x) {
+    double acc[2][V] = {};
+    if (sl < geo.L) {
+      const ChunkRows cr = chunk_tiles(geo, chunk);
+      for (long long tile = cr.t0; tile < cr.t1; ++tile) {
+        const long long row = tile * geo.R + rr;
+        if (row < N) {
+          const size_t o = base + row * S;
+          double rv[V], av[V], zv[V];
+          ldv<V>(r + o, rv);
+          ldv<V>(ap + o, av);
 #pragma unroll
-        for (int j = 0; j < V; ++j) rv[j] = __dsub_rn(rv[j], __dmul_rn(alpha[j], av[j]));
-        stv<V>(r + o, rv);
-        if (dinv) {
-          double dv[V];
-          ldgv<V>(dinv + o, dv);
+          for (int j = 0; j < V; ++j) rv[j] = __dsub_rn(rv[j], __dmul_rn(alpha[j], av[j]));
+          stv<V>(r + o, rv);
+          if (dinv) {
+            double dv[V];
+            ldgv<V>(dinv + o, dv);
 #pragma unroll
-          for (int j = 0; j < V; ++j) zv[j] = __dmul_rn(rv[j], dv[j]);
-        } else {
+            for (int j = 0; j < V; ++j) zv[j] = __dmul_rn(rv[j], dv[j]);
+          } else {
 #pragma unroll
-          for (int j = 0; j < V; ++j) zv[j] = rv[j];
+            for (int j = 0; j < V; ++j) zv[j] = rv[j];
+          }
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            acc[0][j] = __fma_rn(rv[j], rv[j], acc[0][j]);
+            acc[1][j] = __fma_rn(rv[j], zv[j], acc[1][j]);
+          }
         }
+      }
+    }
+    if (!reduce_lanes<2, V>(acc, red, st.part, st.ticket, g, chunk, geo)) continue;
+    __shared__ int s_all, s_bad;
+    if (t == 0) {
+      s_all = 1;
+      s_bad = 0;
+    }
+    __syncthreads();
+    const int it = st.it[g];
+    if (t < geo.L) {
 #pragma unroll
-        for (int j = 0; j < V; ++j) {
-          acc[0][j] = __fma_rn(rv[j], rv[j], acc[0][j]);
-          acc[1][j] = __fma_rn(rv[j], zv[j], acc[1][j]);
+      for (int j = 0; j < V; ++j) {
+        const size_t l = (size_t)g * S + V * t + j;
+        const double rn = sqrt(red[j * geo.T + t]);
+        const double rz_new = red[(V + j) * geo.T + t];
+        if (st.hist) {
+          if (it <= st.hist_cap) st.hist[(size_t)it * st.G * S + l] = rn;
+          else atomicOr(st.overflow, 1);
         }
+        const bool live = !st.frozen[l];
+        if (live && !isfinite(rn)) atomicOr(&s_bad, 1);
+        bool conv = st.conv[l];
+        if (live && !conv && rn <= st.thr[l]) {
+          st.iters[l] = it;
+          st.conv[l] = 1;
+          conv = true;
+        }
+        if (live && !conv) atomicAnd(&s_all, 0);
+        const double rz_old = st.rz[l];
+        st.beta[l] = (live && rz_old > 0.0) ? __ddiv_rn(rz_new, rz_old) : 0.0;
+        st.rz[l] = rz_new;
       }
     }
-  }
-  if (!reduce_lanes<2, V>(acc, red, st.part, st.ticket, g, geo)) return;
-  __shared__ int s_all, s_bad;
-  if (t == 0) {
-    s_all = 1;
-    s_bad = 0;
-  }
-  __syncthreads();
-  const int it = st.it[g];
-  if (t < geo.L) {
+    __syncthreads();
+    const bool finish = s_bad || s_all || it >= maxit;
+    if (finish && t < geo.L) {
 #pragma unroll
-    for (int j = 0; j < V; ++j) {
-      const size_t l = (size_t)g * S + V * t + j;
-      const double rn = sqrt(red[j * geo.T + t]);
-      const double rz_new = red[(V + j) * geo.T + t];
-      if (st.hist) {
-        if (it <= st.hist_cap) st.hist[(size_t)it * st.G * S + l] = rn;
-        else atomicOr(st.overflow, 1);
+      for (int j = 0; j < V; ++j) {
+        const size_t l = (size_t)g * S + V * t + j;
+        if (!st.conv[l]) st.iters[l] = it;  // unconverged / frozen lanes: iterations run
       }
-      const bool live = !st.frozen[l];
-      if (live && !isfinite(rn)) atomicOr(&s_bad, 1);
-      bool conv = st.conv[l];
-      if (live && !conv && rn <= st.thr[l]) {
-        st.iters[l] = it;
-        st.conv[l] = 1;
-        conv = true;
-      }
-      if (live && !conv) atomicAnd(&s_all, 0);
-      const double rz_old = st.rz[l];
-      st.beta[l] = (live && rz_old > 0.0) ? __ddiv_rn(rz_new, rz_old) : 0.0;
-      st.rz[l] = rz_new;
     }
-  }
-  __syncthreads();
-  const bool finish = s_bad || s_all || it >= maxit;
-  if (finish && t < geo.L) {
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-      const size_t l = (size_t)g * S + V * t + j;
-      if (!st.conv[l]) st.iters[l] = it;  // unconverged / frozen lanes: iterations run
+    if (finish && t == 0) {
+      if (s_bad) st.status[g] = 2;
+      st.done[g] = kFinishing;  // pcg_dir applies this iteration's x update, then DONE
     }
-  }
-  if (finish && t == 0) {
-    if (s_bad) st.status[g] = 2;
-    st.done[g] = kFinishing;  // pcg_dir applies this iteration's x update, then DONE
   }
 }
 
@@ -349,36 +379,39 @@ __global__ void __launch_bounds__(256) pcg_dir_kernel(long long N, Geo geo, PcgS
       beta[j] = st.beta[(size_t)g * S + V * sl + j];
     }
     const size_t base = (size_t)g * N * S + V * sl;
-    for (long long tile = blockIdx.x; tile < geo.tiles; tile += geo.B) {
-      const long long row = tile * geo.R + rr;
-      if (row < N) {
-        const size_t o = base + row * S;
-        double xv[V], pv[V];
-        ldv<V>(x + o, xv);
-        ldv<V>(p + o, pv);
+    for (int chunk = blockIdx.x; chunk < geo.chunks; chunk += gridDim.x) {
+      const ChunkRows cr = chunk_tiles(geo, chunk);
+      for (long long tile = cr.t0; tile < cr.t1; ++tile) {
+        const long long row = tile * geo.R + rr;
+        if (row < N) {
+          const size_t o = base + row * S;
+          double xv[V], pv[V];
+          ldv<V>(x + o, xv);
+          ldv<V>(p + o, pv);
 #pragma unroll
-        for (int j = 0; j < V; ++j) xv[j] = __dadd_rn(xv[j], __dmul_rn(alpha[j], pv[j]));
-        stv<V>(x + o, xv);
-        if (state == kRunning) {
-          double rv[V], zv[V];
-          ldv<V>(r + o, rv);
-          if (dinv) {
-            double dv[V];
-            ldgv<V>(dinv + o, dv);
+          for (int j = 0; j < V; ++j) xv[j] = __dadd_rn(xv[j], __dmul_rn(alpha[j], pv[j]));
+          stv<V>(x + o, xv);
+          if (state == kRunning) {
+            double rv[V], zv[V];
+            ldv<V>(r + o, rv);
+            if (dinv) {
+              double dv[V];
+              ldgv<V>(dinv + o, dv);
 #pragma unroll
-            for (int j = 0; j < V; ++j) zv[j] = __dmul_rn(rv[j], dv[j]);
-          } else {
+              for (int j = 0; j < V; ++j) zv[j] = __dmul_rn(rv[j], dv[j]);
+            } else {
 #pragma unroll
-            for (int j = 0; j < V; ++j) zv[j] = rv[j];
+              for (int j = 0; j < V; ++j) zv[j] = rv[j];
+            }
+#pragma unroll
+            for (int j = 0; j < V; ++j) pv[j] = __dadd_rn(zv[j], __dmul_rn(beta[j], pv[j]));
+            stv<V>(p + o, pv);
           }
-#pragma unroll
-          for (int j = 0; j < V; ++j) pv[j] = __dadd_rn(zv[j], __dmul_rn(beta[j], pv[j]));
-          stv<V>(p + o, pv);
         }
       }
     }
   }
-  if (state == kFinishing && last_block(st.ticket, g, geo.B) && t == 0) {
+  if (state == kFinishing && last_block(st.ticket, g, gridDim.x) && t == 0) {
     st.done[g] = kDone;
     atomicAdd(st.ndone, 1);
   }
@@ -394,7 +427,7 @@ __global__ void pcg_finalize_kernel(PcgState st, int G, int S, int* ens_iters) {
 }
 
 // ---------------------------------------------------------------------------
-// host-side dispatch on V
+// host-side dispatch on V (and the unrolled row length ML)
 
 #define UQG_DISPATCH_V(geo, KERNEL, GRID, SMEM, STREAM, ...)                     \
   do {                                                                           \
@@ -403,8 +436,6 @@ __global__ void pcg_finalize_kernel(PcgState st, int G, int S, int* ens_iters) {
     else                                                                         \
       KERNEL<1><<<(GRID), (geo).T, (SMEM), (STREAM)>>>(__VA_ARGS__);             \
   } while (0)
-
-static size_t red_bytes(const Geo& geo, int nv) { return (size_t)nv * geo.V * geo.T * sizeof(double); }
 
 #define UQG_DISPATCH_VML(geo, KERNEL, GRID, SMEM, STREAM, ...)                        \
   do {                                                                                \
@@ -418,40 +449,48 @@ static size_t red_bytes(const Geo& geo, int nv) { return (size_t)nv * geo.V * ge
     }                                                                                 \
   } while (0)
 
+static size_t red_bytes(const Geo& geo, int nv) { return (size_t)nv * geo.V * geo.T * sizeof(double); }
+
 void launch_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long long nnz, const int* ro,
                  const int* ci, const double* vals, const double* x, double* y) {
-  UQG_DISPATCH_VML(geo, spmv_kernel, dim3(geo.B, G), 0, s, N, nnz, geo, ro, ci, vals, x, y);
+  const Geo gl = with_groups(geo, G);
+  UQG_DISPATCH_VML(gl, spmv_kernel, dim3(gl.B, G), 0, s, N, nnz, gl, ro, ci, vals, x, y);
 }
 
 void launch_lane_dot(const Geo& geo, int G, cudaStream_t s, long long N, const double* a,
                      const double* b, double* out, double* part, unsigned* ticket) {
-  UQG_DISPATCH_V(geo, lane_dot_kernel, dim3(geo.B, G), red_bytes(geo, 1), s, N, geo, a, b, out,
-                 part, ticket);
+  const Geo gl = with_groups(geo, G);
+  UQG_DISPATCH_V(gl, lane_dot_kernel, dim3(gl.B, G), red_bytes(gl, 1), s, N, gl, a, b, out, part,
+                 ticket);
 }
 
 void launch_pcg_init(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,
                      const double* rhs, double rhs_const, const double* dinv, double tol,
                      int maxit, double* x, double* r, double* p) {
-  UQG_DISPATCH_V(geo, pcg_init_kernel, dim3(geo.B, G), red_bytes(geo, 2), s, N, geo, st, rhs,
+  const Geo gl = with_groups(geo, G);
+  UQG_DISPATCH_V(gl, pcg_init_kernel, dim3(gl.B, G), red_bytes(gl, 2), s, N, gl, st, rhs,
                  rhs_const, dinv, tol, maxit, x, r, p);
 }
 
 void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long long nnz,
                      const PcgState& st, const int* ro, const int* ci, const double* vals,
                      const double* p, double* ap) {
-  UQG_DISPATCH_VML(geo, pcg_spmv_kernel, dim3(geo.B, G), red_bytes(geo, 1), s, N, nnz, geo, st, ro,
-                 ci, vals, p, ap);
+  const Geo gl = with_groups(geo, G);
+  UQG_DISPATCH_VML(gl, pcg_spmv_kernel, dim3(gl.B, G), red_bytes(gl, 1), s, N, nnz, gl, st, ro,
+                   ci, vals, p, ap);
 }
 
 void launch_pcg_update(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,
                        const double* dinv, int maxit, double* r, const double* ap) {
-  UQG_DISPATCH_V(geo, pcg_update_kernel, dim3(geo.B, G), red_bytes(geo, 2), s, N, geo, st, dinv,
+  const Geo gl = with_groups(geo, G);
+  UQG_DISPATCH_V(gl, pcg_update_kernel, dim3(gl.B, G), red_bytes(gl, 2), s, N, gl, st, dinv,
                  maxit, r, ap);
 }
 
 void launch_pcg_dir(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,
                     const double* dinv, const double* r, double* x, double* p) {
-  UQG_DISPATCH_V(geo, pcg_dir_kernel, dim3(geo.B, G), 0, s, N, geo, st, dinv, r, x, p);
+  const Geo gl = with_groups(geo, G);
+  UQG_DISPATCH_V(gl, pcg_dir_kernel, dim3(gl.B, G), 0, s, N, gl, st, dinv, r, x, p);
 }
 
 void launch_pcg_finalize(int G, int S, cudaStream_t s, const PcgState& st, int* ens_iters) {
