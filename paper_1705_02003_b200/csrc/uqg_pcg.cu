@@ -417,6 +417,172 @@ __global__ void __launch_bounds__(256) pcg_dir_kernel(long long N, Geo geo, PcgS
   }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-staged PCG SpMV.  The matrix values of a tile of R consecutive rows are
+// one contiguous span of [nnz][S] (CSR rows are consecutive), so one elected
+// thread streams it into shared memory with a bulk async copy
+// (cp.async.bulk ... mbarrier::complete_tx) NST tiles ahead of the consumers;
+// threads then read values from shared memory and only gather p from global
+// memory (mostly L1/L2 hits: p rows are reused by the neighbouring rows of
+// the stencil).  Same arithmetic and order as pcg_spmv_kernel, so the results
+// are bit-identical; used when S is even, the longest row is <= ML and the
+// value array is 16-byte aligned.
+
+constexpr int kStages = 3;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// tile index of the i-th tile a block processes (its chunks b, b+B, ...)
+__device__ __forceinline__ long long block_tile(const Geo& geo, int i, int& chunk) {
+  const long long j = i / geo.chunk_tiles;
+  chunk = (int)(blockIdx.x + j * gridDim.x);
+  return (long long)chunk * geo.chunk_tiles + i % geo.chunk_tiles;
+}
+
+__device__ __forceinline__ int block_tile_count(const Geo& geo) {
+  const int nb = (geo.chunks - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  if (nb <= 0) return 0;
+  const int last = blockIdx.x + (nb - 1) * gridDim.x;
+  long long last_tiles = geo.tiles - (long long)last * geo.chunk_tiles;
+  if (last_tiles > geo.chunk_tiles) last_tiles = geo.chunk_tiles;
+  return (int)((nb - 1) * geo.chunk_tiles + last_tiles);
+}
+
+template <int ML>
+__global__ void __launch_bounds__(256) pcg_spmv_tma_kernel(long long N, long long nnz, Geo geo,
+                                                           PcgState st,
+                                                           const int* __restrict__ ro,
+                                                           const int* __restrict__ ci,
+                                                           const double* __restrict__ vals,
+                                                           const double* __restrict__ p,
+                                                           double* __restrict__ ap) {
+  constexpr int V = 2;
+  extern __shared__ __align__(128) double red[];
+  const int g = blockIdx.y, t = threadIdx.x;
+  if (st.done[g] != kRunning) return;
+  const int S = geo.S, R = geo.R;
+  const size_t stage_doubles = (size_t)R * ML * S;
+  double* stage = red + (size_t)V * geo.T;  // after the reduction scratch
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage + kStages * stage_doubles);
+  const double* vg = vals + (size_t)g * nnz * S;
+  const int n_tiles = block_tile_count(geo);
+
+  if (t == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto issue = [&](int i) {  // thread 0 only
+    int chunk;
+    const long long tile = block_tile(geo, i, chunk);
+    const long long r0 = tile * R;
+    const long long r1 = r0 + R < N ? r0 + R : N;
+    const int k0 = __ldg(&ro[r0]), k1 = __ldg(&ro[r1]);
+    const uint32_t bytes = (uint32_t)(k1 - k0) * (uint32_t)S * 8u;
+    uint64_t* bar = &bars[i % kStages];
+    fence_proxy_async();
+    mbar_expect_tx(bar, bytes);
+    if (bytes) bulk_g2s(stage + (size_t)(i % kStages) * stage_doubles, vg + (size_t)k0 * S, bytes, bar);
+  };
+  if (t == 0) {
+    for (int i = 0; i < kStages && i < n_tiles; ++i) issue(i);
+  }
+
+  const int sl = t % geo.Lp, rr = t / geo.Lp;
+  const size_t base = (size_t)g * N * S + V * sl;
+  const double* pg = p + base;
+  double acc[1][V] = {};
+  for (int i = 0; i < n_tiles; ++i) {
+    int chunk;
+    const long long tile = block_tile(geo, i, chunk);
+    mbar_wait(&bars[i % kStages], (uint32_t)((i / kStages) & 1));
+    if (sl < geo.L) {
+      const long long row = tile * R + rr;
+      if (row < N) {
+        const int kt0 = __ldg(&ro[tile * R]);
+        const int k0 = __ldg(&ro[row]), k1 = __ldg(&ro[row + 1]);
+        const double* sv = stage + (size_t)(i % kStages) * stage_doubles +
+                           (size_t)(k0 - kt0) * S + V * sl;
+        const int len = k1 - k0;
+        int c[ML];
+#pragma unroll
+        for (int e = 0; e < ML; ++e) c[e] = e < len ? __ldg(&ci[k0 + e]) : 0;
+        double b[ML][V];
+#pragma unroll
+        for (int e = 0; e < ML; ++e)
+          if (e < len) ldgv<V>(pg + (size_t)c[e] * S, b[e]);
+        double y[V] = {0.0, 0.0};
+#pragma unroll
+        for (int e = 0; e < ML; ++e) {
+          if (e < len) {
+            const double2 a = *reinterpret_cast<const double2*>(sv + (size_t)e * S);
+            y[0] = __dadd_rn(y[0], __dmul_rn(a.x, b[e][0]));
+            y[1] = __dadd_rn(y[1], __dmul_rn(a.y, b[e][1]));
+          }
+        }
+        stv<V>(ap + base + row * S, y);
+        double pv[V];
+        ldgv<V>(pg + row * S, pv);
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[0][j] = __fma_rn(pv[j], y[j], acc[0][j]);
+      }
+    }
+    __syncthreads();  // stage (i % kStages) fully consumed
+    if (t == 0 && i + kStages < n_tiles) issue(i + kStages);
+    const bool chunk_end = ((i + 1) % geo.chunk_tiles == 0) || (tile == geo.tiles - 1);
+    if (chunk_end) {
+      if (reduce_lanes<1, V>(acc, red, st.part, st.ticket, g, chunk, geo)) {
+        if (t < geo.L) {
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            const size_t l = (size_t)g * S + V * t + j;
+            const double pap = red[j * geo.T + t];
+            const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
+            st.frozen[l] = fr;
+            st.alpha[l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
+          }
+        }
+        if (t == 0) st.it[g] += 1;
+      }
+      acc[0][0] = acc[0][1] = 0.0;
+    }
+  }
+}
+
 // ensemble_iterations = max over lanes (ensemble.py:277)
 __global__ void pcg_finalize_kernel(PcgState st, int G, int S, int* ens_iters) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -472,10 +638,41 @@ void launch_pcg_init(const Geo& geo, int G, cudaStream_t s, long long N, const P
                  rhs_const, dinv, tol, maxit, x, r, p);
 }
 
+template <int ML>
+static void launch_spmv_tma(const Geo& gl, int G, cudaStream_t s, long long N, long long nnz,
+                            const PcgState& st, const int* ro, const int* ci, const double* vals,
+                            const double* p, double* ap) {
+  const size_t smem = (size_t)2 * gl.T * sizeof(double) +
+                      (size_t)kStages * gl.R * ML * gl.S * sizeof(double) + kStages * 8;
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaFuncSetAttribute(pcg_spmv_tma_kernel<ML>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    configured = smem;
+  }
+  pcg_spmv_tma_kernel<ML><<<dim3(gl.B, G), gl.T, smem, s>>>(N, nnz, gl, st, ro, ci, vals, p, ap);
+}
+
+bool spmv_tma_enabled() {
+  static const int on = [] {
+    const char* e = getenv("UQG_SPMV_TMA");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
+
 void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long long nnz,
                      const PcgState& st, const int* ro, const int* ci, const double* vals,
                      const double* p, double* ap) {
   const Geo gl = with_groups(geo, G);
+  const bool aligned = (reinterpret_cast<uintptr_t>(vals) & 15) == 0;
+  if (spmv_tma_enabled() && gl.V == 2 && aligned && gl.maxrow >= 1 && gl.maxrow <= 8) {
+    if (gl.maxrow <= 5)
+      launch_spmv_tma<5>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap);
+    else
+      launch_spmv_tma<8>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap);
+    return;
+  }
   UQG_DISPATCH_VML(gl, pcg_spmv_kernel, dim3(gl.B, G), red_bytes(gl, 1), s, N, nnz, gl, st, ro,
                    ci, vals, p, ap);
 }

@@ -400,3 +400,34 @@ def test_launch_accounting_and_profiling():
     lib.uqg_ctx_profile(ctx, 0)
     assert lib.uqg_ctx_launch_count(ctx) > before
     assert cnt[3] >= r.ensemble_iterations and ms[3] > 0.0
+
+
+_TMA_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1705_02003_b200 as uq
+cfg = uq.CONFIGS["C1"]
+f = uq.build_field(**cfg.field_kwargs())
+s = uq.EnsembleSolver2D(f, cfg.cells, cfg.tol, cfg.maxit)
+ys = np.random.default_rng(3).uniform(-1, 1, (4, cfg.ensemble_size, cfg.n_modes))
+r = s.solve_groups(ys)
+np.save(sys.argv[2], np.concatenate([r.iterations.ravel().astype(float), r.qoi.ravel()]))
+"""
+
+
+@pytest.mark.parametrize("lanes", ["2", "1"])
+def test_tma_staged_spmv_bitwise_equals_register_path(tmp_path, lanes):
+    """The TMA-staged SpMV (default for the stencil) and the register-gather
+    SpMV produce identical bits through a whole batched solve."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parents[1])
+    out = {}
+    for tma in ("1", "0"):
+        env = dict(os.environ, UQG_SPMV_TMA=tma, UQG_LANES_PER_THREAD=lanes)
+        dst = tmp_path / f"r{tma}.npy"
+        subprocess.run([sys.executable, "-c", _TMA_SCRIPT, root, str(dst)], env=env, check=True)
+        out[tma] = np.load(dst)
+    assert np.array_equal(out["1"], out["0"])
