@@ -41,7 +41,9 @@ struct uqg_ctx {
 
 namespace {
 
-constexpr int kEventPairs = 512;
+// Timing events are harvested lazily (end of a solve, profile_read, or a full
+// pool), so profiling adds two event records per launch and no host syncs.
+constexpr int kEventPairs = 16384;
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
@@ -413,20 +415,20 @@ int uqg_pcg(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const i
     UQG_TRY_CUDA(cudaMemcpyAsync(ctx->pinned, st.ndone, sizeof(int), cudaMemcpyDeviceToHost, s));
     UQG_TRY_CUDA(cudaEventRecord(ctx->ev, s));
     UQG_TRY_CUDA(cudaEventSynchronize(ctx->ev));
-    if (ctx->prof) {
-      rc = harvest(ctx);
-      if (rc) return rc;
-    }
     if (ctx->pinned[0] >= G) break;
     if (launched > (long long)maxit + 1) {
       set_error("uqg_pcg: device loop failed to terminate");
       return UQG_ECUDA;
     }
+    // Size blocks-per-group for the groups still running (finished groups'
+    // blocks exit at once); the reduction chunks - hence the results - do not
+    // depend on this.
+    const Geo gact = with_groups(geo, std::max(1, G - ctx->pinned[0]));
     for (int k = 0; k < chunk; ++k) {
       UQG_LAUNCH(UQG_K_PCG_SPMV, s,
-                 launch_pcg_spmv(geo, G, s, N, nnz, st, row_offsets, col_indices, vals, p, ap));
-      UQG_LAUNCH(UQG_K_PCG_UPDATE, s, launch_pcg_update(geo, G, s, N, st, dinv, maxit, r, ap));
-      UQG_LAUNCH(UQG_K_PCG_DIR, s, launch_pcg_dir(geo, G, s, N, st, dinv, r, x, p));
+                 launch_pcg_spmv(gact, G, s, N, nnz, st, row_offsets, col_indices, vals, p, ap));
+      UQG_LAUNCH(UQG_K_PCG_UPDATE, s, launch_pcg_update(gact, G, s, N, st, dinv, maxit, r, ap));
+      UQG_LAUNCH(UQG_K_PCG_DIR, s, launch_pcg_dir(gact, G, s, N, st, dinv, r, x, p));
     }
     launched += chunk;
     chunk = std::min(chunk * 2, 64);

@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(256) pcg_spmv_kernel(long long N, long long nn
 }
 
 template <int V>
-__global__ void __launch_bounds__(256) pcg_update_kernel(long long N, Geo geo, PcgState st,
+__global__ void __launch_bounds__(256, 3) pcg_update_kernel(long long N, Geo geo, PcgState st,
                                                          const double* __restrict__ dinv,
                                                          int maxit, double* __restrict__ r,
                                                          const double* __restrict__ ap) {
@@ -286,30 +286,34 @@ __global__ void __launch_bounds__(256) pcg_update_kernel(long long N, Geo geo, P
     double acc[2][V] = {};
     if (sl < geo.L) {
       const ChunkRows cr = chunk_tiles(geo, chunk);
-      for (long long tile = cr.t0; tile < cr.t1; ++tile) {
-        const long long row = tile * geo.R + rr;
-        if (row < N) {
-          const size_t o = base + row * S;
-          double rv[V], av[V], zv[V];
-          ldv<V>(r + o, rv);
-          ldv<V>(ap + o, av);
+      // two tiles per step: all loads of both are issued before any store
+      for (long long tile = cr.t0; tile < cr.t1; tile += 2) {
+        double rv[2][V], av[2][V], dv[2][V];
+        bool ok[2];
+        size_t o[2];
 #pragma unroll
-          for (int j = 0; j < V; ++j) rv[j] = __dsub_rn(rv[j], __dmul_rn(alpha[j], av[j]));
-          stv<V>(r + o, rv);
-          if (dinv) {
-            double dv[V];
-            ldgv<V>(dinv + o, dv);
-#pragma unroll
-            for (int j = 0; j < V; ++j) zv[j] = __dmul_rn(rv[j], dv[j]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < V; ++j) zv[j] = rv[j];
+        for (int u = 0; u < 2; ++u) {
+          const long long row = (tile + u) * geo.R + rr;
+          ok[u] = tile + u < cr.t1 && row < N;
+          o[u] = base + (ok[u] ? row : 0) * S;
+          if (ok[u]) {
+            ldv<V>(r + o[u], rv[u]);
+            ldv<V>(ap + o[u], av[u]);
+            if (dinv) ldgv<V>(dinv + o[u], dv[u]);
           }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (!ok[u]) continue;
+          double zv[V];
 #pragma unroll
           for (int j = 0; j < V; ++j) {
-            acc[0][j] = __fma_rn(rv[j], rv[j], acc[0][j]);
-            acc[1][j] = __fma_rn(rv[j], zv[j], acc[1][j]);
+            rv[u][j] = __dsub_rn(rv[u][j], __dmul_rn(alpha[j], av[u][j]));
+            zv[j] = dinv ? __dmul_rn(rv[u][j], dv[u][j]) : rv[u][j];
+            acc[0][j] = __fma_rn(rv[u][j], rv[u][j], acc[0][j]);
+            acc[1][j] = __fma_rn(rv[u][j], zv[j], acc[1][j]);
           }
+          stv<V>(r + o[u], rv[u]);
         }
       }
     }
@@ -362,7 +366,7 @@ __global__ void __launch_bounds__(256) pcg_update_kernel(long long N, Geo geo, P
 }
 
 template <int V>
-__global__ void __launch_bounds__(256) pcg_dir_kernel(long long N, Geo geo, PcgState st,
+__global__ void __launch_bounds__(256, 3) pcg_dir_kernel(long long N, Geo geo, PcgState st,
                                                       const double* __restrict__ dinv,
                                                       const double* __restrict__ r,
                                                       double* __restrict__ x,
@@ -379,33 +383,41 @@ __global__ void __launch_bounds__(256) pcg_dir_kernel(long long N, Geo geo, PcgS
       beta[j] = st.beta[(size_t)g * S + V * sl + j];
     }
     const size_t base = (size_t)g * N * S + V * sl;
+    const bool running = state == kRunning;
     for (int chunk = blockIdx.x; chunk < geo.chunks; chunk += gridDim.x) {
       const ChunkRows cr = chunk_tiles(geo, chunk);
-      for (long long tile = cr.t0; tile < cr.t1; ++tile) {
-        const long long row = tile * geo.R + rr;
-        if (row < N) {
-          const size_t o = base + row * S;
-          double xv[V], pv[V];
-          ldv<V>(x + o, xv);
-          ldv<V>(p + o, pv);
+      // two tiles per step: all loads of both are issued before any store
+      for (long long tile = cr.t0; tile < cr.t1; tile += 2) {
+        double xv[2][V], pv[2][V], rv[2][V], dv[2][V];
+        bool ok[2];
+        size_t o[2];
 #pragma unroll
-          for (int j = 0; j < V; ++j) xv[j] = __dadd_rn(xv[j], __dmul_rn(alpha[j], pv[j]));
-          stv<V>(x + o, xv);
-          if (state == kRunning) {
-            double rv[V], zv[V];
-            ldv<V>(r + o, rv);
-            if (dinv) {
-              double dv[V];
-              ldgv<V>(dinv + o, dv);
-#pragma unroll
-              for (int j = 0; j < V; ++j) zv[j] = __dmul_rn(rv[j], dv[j]);
-            } else {
-#pragma unroll
-              for (int j = 0; j < V; ++j) zv[j] = rv[j];
+        for (int u = 0; u < 2; ++u) {
+          const long long row = (tile + u) * geo.R + rr;
+          ok[u] = tile + u < cr.t1 && row < N;
+          o[u] = base + (ok[u] ? row : 0) * S;
+          if (ok[u]) {
+            ldv<V>(x + o[u], xv[u]);
+            ldv<V>(p + o[u], pv[u]);
+            if (running) {
+              ldv<V>(r + o[u], rv[u]);
+              if (dinv) ldgv<V>(dinv + o[u], dv[u]);
             }
+          }
+        }
 #pragma unroll
-            for (int j = 0; j < V; ++j) pv[j] = __dadd_rn(zv[j], __dmul_rn(beta[j], pv[j]));
-            stv<V>(p + o, pv);
+        for (int u = 0; u < 2; ++u) {
+          if (!ok[u]) continue;
+#pragma unroll
+          for (int j = 0; j < V; ++j) xv[u][j] = __dadd_rn(xv[u][j], __dmul_rn(alpha[j], pv[u][j]));
+          stv<V>(x + o[u], xv[u]);
+          if (running) {
+#pragma unroll
+            for (int j = 0; j < V; ++j) {
+              const double zv = dinv ? __dmul_rn(rv[u][j], dv[u][j]) : rv[u][j];
+              pv[u][j] = __dadd_rn(zv, __dmul_rn(beta[j], pv[u][j]));
+            }
+            stv<V>(p + o[u], pv[u]);
           }
         }
       }
@@ -664,7 +676,7 @@ bool spmv_tma_enabled() {
 void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long long nnz,
                      const PcgState& st, const int* ro, const int* ci, const double* vals,
                      const double* p, double* ap) {
-  const Geo gl = with_groups(geo, G);
+  const Geo& gl = geo;  // B preset by the caller (blocks per ACTIVE group)
   const bool aligned = (reinterpret_cast<uintptr_t>(vals) & 15) == 0;
   if (spmv_tma_enabled() && gl.V == 2 && aligned && gl.maxrow >= 1 && gl.maxrow <= 8) {
     if (gl.maxrow <= 5)
@@ -679,14 +691,14 @@ void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long lo
 
 void launch_pcg_update(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,
                        const double* dinv, int maxit, double* r, const double* ap) {
-  const Geo gl = with_groups(geo, G);
+  const Geo& gl = geo;  // B preset by the caller (blocks per ACTIVE group)
   UQG_DISPATCH_V(gl, pcg_update_kernel, dim3(gl.B, G), red_bytes(gl, 2), s, N, gl, st, dinv,
                  maxit, r, ap);
 }
 
 void launch_pcg_dir(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,
                     const double* dinv, const double* r, double* x, double* p) {
-  const Geo gl = with_groups(geo, G);
+  const Geo& gl = geo;  // B preset by the caller (blocks per ACTIVE group)
   UQG_DISPATCH_V(gl, pcg_dir_kernel, dim3(gl.B, G), 0, s, N, gl, st, dinv, r, x, p);
 }
 
