@@ -282,7 +282,15 @@ def main():
             dist.barrier()
 
     def step():
-        return solver.run_level_device(d_coords, n, S, d_keys)
+        out = solver.run_level_device(d_coords, n, S, d_keys)
+        if world > 1:
+            # the study's one collective: per-slot iterations + QoIs of every rank's
+            # groups allgathered (NCCL) for the surrogate refit (harness.py:658-660)
+            groups, pad, it, cv, en, q = out
+            mine = torch.cat([it.double(), q])
+            allv = torch.empty(world * mine.numel(), dtype=mine.dtype, device=dev)
+            dist.all_gather_into_tensor(allv, mine)
+        return out
 
     for _ in range(max(3, args.warmup)):
         step()
