@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--separate-kernel-timing", action="store_true",
+                    help="time `value` without per-launch events; kernel breakdown from a "
+                         "second, identical profiled pass (small configs: event overhead)")
     ap.add_argument("--wave", type=int, default=None,
                     help="max groups per device wave (default: as many as fit in HBM)")
     return ap.parse_args()
@@ -298,33 +301,45 @@ def main():
 
     import ctypes
     NK = 10
-    ms = (ctypes.c_double * NK)()
-    cnt = (ctypes.c_longlong * NK)()
-    lib.uqg_ctx_profile_read(ctx, ms, cnt, 1)
-    lib.uqg_ctx_profile(ctx, 1)
-    launches0 = lib.uqg_ctx_launch_count(ctx)
-    times, group_iters, n_groups = [], 0, 0
-    with ClockSampler(torch.cuda.current_device()) as clocks:
-        for _ in range(args.steps):
-            barrier()
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            groups, pad, it, cv, en, q = step()
-            e1.record(stream)
-            torch.cuda.synchronize()
-            t = e0.elapsed_time(e1)
-            if world > 1:
-                tt = torch.tensor([t], device=dev)
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-                t = float(tt.item())
-            times.append(t)
-            group_iters += int(en.sum().item())
-            n_groups = pad.numel()
-            barrier()
-    launches = lib.uqg_ctx_launch_count(ctx) - launches0
-    lib.uqg_ctx_profile_read(ctx, ms, cnt, 1)
-    lib.uqg_ctx_profile(ctx, 0)
+
+    def timed(profile: bool):
+        """K timed steps; per-launch CUDA-event kernel timing when `profile`."""
+        ms = (ctypes.c_double * NK)()
+        cnt = (ctypes.c_longlong * NK)()
+        lib.uqg_ctx_profile_read(ctx, ms, cnt, 1)
+        lib.uqg_ctx_profile(ctx, int(profile))
+        launches0 = lib.uqg_ctx_launch_count(ctx)
+        times, group_iters, last = [], 0, None
+        with ClockSampler(torch.cuda.current_device()) as clocks:
+            for _ in range(args.steps):
+                barrier()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                last = step()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                t = e0.elapsed_time(e1)
+                if world > 1:
+                    tt = torch.tensor([t], device=dev)
+                    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                    t = float(tt.item())
+                times.append(t)
+                group_iters += int(last[4].sum().item())
+                barrier()
+        launches = lib.uqg_ctx_launch_count(ctx) - launches0
+        lib.uqg_ctx_profile_read(ctx, ms, cnt, 1)
+        lib.uqg_ctx_profile(ctx, 0)
+        return times, group_iters, launches, ms, cnt, clocks, last
+
+    if args.separate_kernel_timing:
+        # value from un-instrumented steps; kernel shares from an identical profiled pass
+        times, group_iters, launches, _, _, clocks, last = timed(False)
+        _, prof_iters, _, ms, cnt, _, _ = timed(True)
+        assert prof_iters == group_iters
+    else:
+        times, group_iters, launches, ms, cnt, clocks, last = timed(True)
+    groups, pad, it, cv, en, q = last
     conv_all = bool(cv.all().item())
 
     # ---- end to end through the public API: host inputs, host results -------
