@@ -71,25 +71,27 @@ def make_workload(cfg, solver=None):
         z = np.load(path)
         keys = z["keys"] if z["keys"].size else None
         return z["ids"].tolist(), z["coords"], keys, json.loads(str(z["meta"]))
-    from paper_1705_02003_b200.driver import ITER, QOI, adaptive_run, sample_set
+    from paper_1705_02003_b200.driver import adaptive_run, sample_set
     if cfg.synthetic_samples:
         coords = sample_set(cfg)
         ids, keys, meta = list(range(len(coords))), None, {"source": "seeded U[-1,1]^M, rng 0"}
     else:
+        # the study's last level: its samples and the surrogate keys that grouped it
         t0 = time.time()
-        records, stop, grid = adaptive_run(cfg, solver, max_levels=cfg.max_levels - 1)
-        new, _ = grid.refine(cfg.tau, QOI, cfg.n_max)
-        start = len(grid) - len(new)
-        ids = list(range(start, len(grid)))
-        coords = grid.node_coords()[start:]
-        keys = grid.evaluate(ITER, coords, n_nodes=start)
-        meta = {"source": f"adaptive levels 1..{len(records)} solved on device "
-                          f"({[len(r.ids) for r in records]} samples, {time.time() - t0:.1f}s); "
-                          f"final level {len(records) + 1}",
-                "prior_levels": [len(r.ids) for r in records]}
-    WORKLOADS.mkdir(exist_ok=True)
-    np.savez(path, ids=np.array(ids), coords=coords,
-             keys=np.array([]) if keys is None else keys, meta=json.dumps(meta))
+        records, stop, grid = adaptive_run(cfg, solver)
+        last = records[-1]
+        ids, coords = list(last.ids), np.asarray(last.coords)
+        keys = None if last.predicted is None else np.asarray(last.predicted)
+        meta = {"source": f"adaptive study solved on device: levels "
+                          f"{[len(r.ids) for r in records]} samples ({stop}, "
+                          f"{time.time() - t0:.1f}s); workload = level {last.level}",
+                "levels": [len(r.ids) for r in records]}
+    if int(os.environ.get("RANK", "0")) == 0:  # every rank computes the same; one writes
+        WORKLOADS.mkdir(exist_ok=True)
+        tmp = path.with_suffix(".tmp.npz")
+        np.savez(tmp, ids=np.array(ids), coords=coords,
+                 keys=np.array([]) if keys is None else keys, meta=json.dumps(meta))
+        os.replace(tmp, path)
     return ids, coords, keys, meta
 
 

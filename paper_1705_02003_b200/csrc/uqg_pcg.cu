@@ -494,7 +494,7 @@ __device__ __forceinline__ int block_tile_count(const Geo& geo) {
 }
 
 template <int ML>
-__global__ void __launch_bounds__(256, 3) pcg_spmv_tma_kernel(long long N, long long nnz, Geo geo,
+__global__ void __launch_bounds__(256) pcg_spmv_tma_kernel(long long N, long long nnz, Geo geo,
                                                            PcgState st,
                                                            const int* __restrict__ ro,
                                                            const int* __restrict__ ci,
@@ -505,90 +505,34 @@ __global__ void __launch_bounds__(256, 3) pcg_spmv_tma_kernel(long long N, long 
   extern __shared__ __align__(128) double red[];
   const int g = blockIdx.y, t = threadIdx.x;
   if (st.done[g] != kRunning) return;
-  const int S = geo.S, R = geo.R, T = geo.T;
+  const int S = geo.S, R = geo.R;
   const size_t stage_doubles = (size_t)R * ML * S;
-  const int ro_stride = (R + 2) & ~1, col_stride = R * ML;
-  double* stage = red + (size_t)V * T;  // after the reduction scratch
-  int* ro_s = reinterpret_cast<int*>(stage + kStages * stage_doubles);  // [kStages][R+1]
-  int* col_s = ro_s + kStages * ro_stride;                              // [kStages][R*ML]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(col_s + kStages * col_stride);
+  double* stage = red + (size_t)V * geo.T;  // after the reduction scratch
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage + kStages * stage_doubles);
   const double* vg = vals + (size_t)g * nnz * S;
   const int n_tiles = block_tile_count(geo);
 
-  // Tile metadata (row offsets, column indices) is staged in shared memory one
-  // or two tiles ahead by all threads, so a row's critical path is only the p
-  // gather: row offsets of tile i+2 and column indices of tile i+1 are loaded
-  // into registers before tile i is computed and stored after it.
-  auto tile_r0 = [&](int i, long long& r0, int& nrow) {
+  if (t == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto issue = [&](int i) {  // thread 0 only
     int chunk;
     const long long tile = block_tile(geo, i, chunk);
-    r0 = tile * R;
-    nrow = (int)(r0 + R < N ? R : N - r0);
-  };
-  auto load_ro = [&](int i) -> int {  // thread t's share of ro[r0 .. r0+nrow]
-    long long r0;
-    int nrow;
-    tile_r0(i, r0, nrow);
-    return t <= nrow ? __ldg(&ro[r0 + t]) : 0;
-  };
-  auto store_ro = [&](int i, int v) {
-    long long r0;
-    int nrow;
-    tile_r0(i, r0, nrow);
-    if (t <= nrow) ro_s[(i % kStages) * ro_stride + t] = v;
-  };
-  auto load_col = [&](int i, int (&v)[2]) {  // needs ro_s of tile i
-    long long r0;
-    int nrow;
-    tile_r0(i, r0, nrow);
-    const int* rs = ro_s + (i % kStages) * ro_stride;
-    const int k0 = rs[0], cnt = rs[nrow] - k0;
-#pragma unroll
-    for (int u = 0; u < 2; ++u) v[u] = t + u * T < cnt ? __ldg(&ci[k0 + t + u * T]) : 0;
-  };
-  auto store_col = [&](int i, const int (&v)[2]) {
-    long long r0;
-    int nrow;
-    tile_r0(i, r0, nrow);
-    const int* rs = ro_s + (i % kStages) * ro_stride;
-    const int cnt = rs[nrow] - rs[0];
-#pragma unroll
-    for (int u = 0; u < 2; ++u)
-      if (t + u * T < cnt) col_s[(i % kStages) * col_stride + t + u * T] = v[u];
-  };
-  auto issue = [&](int i, int k0, int k1) {  // thread 0 only
+    const long long r0 = tile * R;
+    const long long r1 = r0 + R < N ? r0 + R : N;
+    const int k0 = __ldg(&ro[r0]), k1 = __ldg(&ro[r1]);
     const uint32_t bytes = (uint32_t)(k1 - k0) * (uint32_t)S * 8u;
     uint64_t* bar = &bars[i % kStages];
     fence_proxy_async();
     mbar_expect_tx(bar, bytes);
     if (bytes) bulk_g2s(stage + (size_t)(i % kStages) * stage_doubles, vg + (size_t)k0 * S, bytes, bar);
   };
-  auto tile_k = [&](int i, int& k0, int& k1) {  // thread 0: value range of tile i
-    long long r0;
-    int nrow;
-    tile_r0(i, r0, nrow);
-    k0 = __ldg(&ro[r0]);
-    k1 = __ldg(&ro[r0 + nrow]);
-  };
-
   if (t == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
-    fence_mbar_init();
-    for (int i = 0; i < kStages && i < n_tiles; ++i) {
-      int k0, k1;
-      tile_k(i, k0, k1);
-      issue(i, k0, k1);
-    }
+    for (int i = 0; i < kStages && i < n_tiles; ++i) issue(i);
   }
-  if (n_tiles > 0) store_ro(0, load_ro(0));
-  if (n_tiles > 1) store_ro(1, load_ro(1));
-  __syncthreads();
-  if (n_tiles > 0) {
-    int cv[2];
-    load_col(0, cv);
-    store_col(0, cv);
-  }
-  __syncthreads();
 
   const int sl = t % geo.Lp, rr = t / geo.Lp;
   const size_t base = (size_t)g * N * S + V * sl;
@@ -597,27 +541,18 @@ __global__ void __launch_bounds__(256, 3) pcg_spmv_tma_kernel(long long N, long 
   for (int i = 0; i < n_tiles; ++i) {
     int chunk;
     const long long tile = block_tile(geo, i, chunk);
-    // prefetch metadata of tiles i+2 (row offsets) and i+1 (columns), and the
-    // value range of tile i+kStages for the producer
-    const int ro_next = i + 2 < n_tiles ? load_ro(i + 2) : 0;
-    int col_next[2] = {0, 0};
-    if (i + 1 < n_tiles) load_col(i + 1, col_next);
-    int kn0 = 0, kn1 = 0;
-    if (t == 0 && i + kStages < n_tiles) tile_k(i + kStages, kn0, kn1);
     mbar_wait(&bars[i % kStages], (uint32_t)((i / kStages) & 1));
     if (sl < geo.L) {
       const long long row = tile * R + rr;
       if (row < N) {
-        const int* rs = ro_s + (i % kStages) * ro_stride;
-        const int* cs = col_s + (i % kStages) * col_stride;
-        const int kt0 = rs[0];
-        const int k0 = rs[rr], k1 = rs[rr + 1];
+        const int kt0 = __ldg(&ro[tile * R]);
+        const int k0 = __ldg(&ro[row]), k1 = __ldg(&ro[row + 1]);
         const double* sv = stage + (size_t)(i % kStages) * stage_doubles +
                            (size_t)(k0 - kt0) * S + V * sl;
         const int len = k1 - k0;
         int c[ML];
 #pragma unroll
-        for (int e = 0; e < ML; ++e) c[e] = e < len ? cs[k0 - kt0 + e] : 0;
+        for (int e = 0; e < ML; ++e) c[e] = e < len ? __ldg(&ci[k0 + e]) : 0;
         double b[ML][V];
 #pragma unroll
         for (int e = 0; e < ML; ++e)
@@ -638,10 +573,8 @@ __global__ void __launch_bounds__(256, 3) pcg_spmv_tma_kernel(long long N, long 
         for (int j = 0; j < V; ++j) acc[0][j] = __fma_rn(pv[j], y[j], acc[0][j]);
       }
     }
-    if (i + 2 < n_tiles) store_ro(i + 2, ro_next);
-    if (i + 1 < n_tiles) store_col(i + 1, col_next);
-    __syncthreads();  // stage (i % kStages) fully consumed; metadata of i+1, i+2 visible
-    if (t == 0 && i + kStages < n_tiles) issue(i + kStages, kn0, kn1);
+    __syncthreads();  // stage (i % kStages) fully consumed
+    if (t == 0 && i + kStages < n_tiles) issue(i + kStages);
     const bool chunk_end = ((i + 1) % geo.chunk_tiles == 0) || (tile == geo.tiles - 1);
     if (chunk_end) {
       if (reduce_lanes<1, V>(acc, red, st.part, st.ticket, g, chunk, geo)) {
@@ -722,9 +655,7 @@ static void launch_spmv_tma(const Geo& gl, int G, cudaStream_t s, long long N, l
                             const PcgState& st, const int* ro, const int* ci, const double* vals,
                             const double* p, double* ap) {
   const size_t smem = (size_t)2 * gl.T * sizeof(double) +
-                      (size_t)kStages * gl.R * ML * gl.S * sizeof(double) +
-                      (size_t)kStages * (((gl.R + 2) & ~1) + gl.R * ML) * sizeof(int) +
-                      kStages * 8;
+                      (size_t)kStages * gl.R * ML * gl.S * sizeof(double) + kStages * 8;
   static size_t configured = 0;
   if (smem > configured) {
     cudaFuncSetAttribute(pcg_spmv_tma_kernel<ML>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -747,10 +678,7 @@ void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long lo
                      const double* p, double* ap) {
   const Geo& gl = geo;  // B preset by the caller (blocks per ACTIVE group)
   const bool aligned = (reinterpret_cast<uintptr_t>(vals) & 15) == 0;
-  // TMA path: 16-byte value rows (S even), S >= 8 (tile metadata fits the
-  // block's threads), short rows
-  if (spmv_tma_enabled() && gl.V == 2 && gl.Lp >= 4 && aligned && gl.maxrow >= 1 &&
-      gl.maxrow <= 8) {
+  if (spmv_tma_enabled() && gl.V == 2 && aligned && gl.maxrow >= 1 && gl.maxrow <= 8) {
     if (gl.maxrow <= 5)
       launch_spmv_tma<5>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap);
     else
