@@ -101,6 +101,25 @@ int uqg_assemble_fv2d(uqg_ctx* ctx, int n_cells, int G, int S, const double* a_n
                       double a_y, int a2_same, const int* row_offsets, double* vals,
                       double* dinv, void* stream);
 
+/* 3D trilinear hex FEM (the reference's own operator, fem3d.py), m cells/dir.
+ * uqg_kl_eval_sep3d: a at the 8 Gauss points of every element, a_out
+ * [G][m^3*8][S] (element-major, q bit-ordered x,y,z), qtab [n_factors][2m] =
+ * 1D factors at the Gauss abscissae; mode_p/q/r [M] factor ids; other
+ * arguments as uqg_kl_eval_sep2d (random_field.py:145-166 at quad_points).
+ * uqg_assemble_fem3d: vals [G][nnz][S] on the 27-point graph (row_offsets
+ * [N+1], N=(m-1)^3), summing per nonzero the element matrices
+ * sum_q a_q dx_tab[q][a][b] + kyz_tab[a][b] in increasing element order
+ * (assemble, fem3d.py:138-175: einsum + bincount); dinv [G][N][S] = 1/diag
+ * (may be NULL).  dx_tab [8][8][8] = _elem_mats[0], kyz_tab [8][8]. */
+int uqg_kl_eval_sep3d(uqg_ctx* ctx, int m, const double* qtab, int n_factors, const int* mode_p,
+                      const int* mode_q, const int* mode_r, const double* sqrt_lam, int M,
+                      const double* samples, const int* lane_ids, int G, int S, double a_min,
+                      int a_hat_mode, double a_hat_value, int expansion, double* a_out,
+                      void* stream);
+int uqg_assemble_fem3d(uqg_ctx* ctx, int m, int G, int S, const double* a_q, const double* dx_tab,
+                       const double* kyz_tab, const int* row_offsets, double* vals, double* dinv,
+                       void* stream);
+
 /* Jacobi inverse diagonal from any shared-graph ensemble matrix
  * (EnsembleCsrMatrix.diagonal + jacobi_precond, ensemble.py:130-137,179-183).
  * Synchronises; returns UQG_EINVAL if any lane diagonal <= 0. */

@@ -19,11 +19,12 @@ from .errors import (DeviceError, EnsembleError, FemError, FieldError, GroupingE
                      NumericalBreakdownError)
 from .ensemble import (EnsembleCsrMatrix, IdentityPreconditioner, JacobiPreconditioner,
                        LaneSolveResult, ensemble_pcg, jacobi_precond, lane_dot, lane_norms)
-from .field import Eigenpair1D, KLField2D, build_field, eigenpairs_1d
+from .field import Eigenpair1D, KLField, KLField2D, build_field, eigenpairs_1d
 from .fv2d import AssembledEnsembleSystem, StructuredMesh2D, assemble, qoi
+from .fem3d import StructuredMesh3D
 from .grouping import GroupingPlan, group_by_key, group_natural
-from .solve import EnsembleSolver2D, LevelSolveResult
-from .configs import CONFIGS, StudyConfig
+from .solve import EnsembleSolver, EnsembleSolver2D, EnsembleSolver3D, LevelSolveResult
+from .configs import CONFIGS, PRESETS_3D, ReferencePreset, StudyConfig
 
 __version__ = "0.1.0"
 
@@ -33,6 +34,7 @@ __all__ = [
     "JacobiPreconditioner", "LaneSolveResult", "ensemble_pcg", "jacobi_precond", "lane_dot",
     "lane_norms", "Eigenpair1D", "KLField2D", "build_field", "eigenpairs_1d",
     "AssembledEnsembleSystem", "StructuredMesh2D", "assemble", "qoi", "GroupingPlan",
-    "group_by_key", "group_natural", "EnsembleSolver2D", "LevelSolveResult", "CONFIGS",
-    "StudyConfig", "__version__",
+    "group_by_key", "group_natural", "EnsembleSolver", "EnsembleSolver2D", "EnsembleSolver3D",
+    "LevelSolveResult", "CONFIGS", "PRESETS_3D", "ReferencePreset", "StudyConfig", "KLField",
+    "StructuredMesh3D", "__version__",
 ]

@@ -38,6 +38,9 @@ SIGNATURES = {
                                    _c_double, _c_int, _p, _p]),
     "uqg_assemble_fv2d": (_c_int, [_p, _c_int, _c_int, _c_int, _p, _c_double, _c_int, _p, _p, _p,
                                    _p]),
+    "uqg_kl_eval_sep3d": (_c_int, [_p, _c_int, _p, _c_int, _p, _p, _p, _p, _c_int, _p, _p, _c_int,
+                                   _c_int, _c_double, _c_int, _c_double, _c_int, _p, _p]),
+    "uqg_assemble_fem3d": (_c_int, [_p, _c_int, _c_int, _c_int, _p, _p, _p, _p, _p, _p, _p]),
     "uqg_jacobi_dinv": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _p, _p, _p, _p, _p]),
     "uqg_diagonal": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _p, _p, _p, _p, _p]),
     "uqg_spmv": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _c_int, _p, _p, _p, _p, _p, _p]),

@@ -66,6 +66,62 @@ class StudyConfig:
     def to_dict(self) -> dict:
         return asdict(self)
 
+    def make_solver(self, **kw):
+        from .field import build_field
+        from .solve import EnsembleSolver2D
+        return EnsembleSolver2D(build_field(**self.field_kwargs()), self.cells, self.tol,
+                                self.maxit, self.a2, **kw)
+
+
+@dataclass(frozen=True)
+class ReferencePreset:
+    """The reference's own 3D PDE presets (``harness.py:208-255``): trilinear FEM
+    on m^3 cells, kernel-convention sigma0 = sqrt(300), a_min = 0.1, four KL
+    modes, S = 4, tau = 1e-3 on the QoI, n_max = 600, initial level 1,
+    tol 1e-7, maxit 30000; no level cap (the loop stops on tau / budget)."""
+
+    name: str
+    a_hat_mode: str = "constant"
+    cells: int = 16
+    n_modes: int = 4
+    delta: float = 0.25
+    sigma0: float = 300.0 ** 0.5
+    a_min: float = 0.1
+    a_hat_value: float = 1.0
+    a_y: float = 1.0
+    a_z: float = 1.0
+    sigma0_convention: str = "kernel"
+    expansion: str = "log"
+    ensemble_size: int = 4
+    tau: float = 1e-3
+    n_max: int = 600
+    initial_level: int = 1
+    tol: float = 1e-7
+    maxit: int = 30000
+    max_levels: int = 10_000
+    synthetic_samples: int = 0
+
+    def field_kwargs(self) -> dict:
+        return dict(delta=self.delta, sigma0=self.sigma0, n_modes=self.n_modes, a_min=self.a_min,
+                    a_hat_mode=self.a_hat_mode, a_hat_value=self.a_hat_value, a_y=self.a_y,
+                    a_z=self.a_z, sigma0_convention=self.sigma0_convention,
+                    expansion=self.expansion, dim=3)
+
+    def to_dict(self) -> dict:
+        return asdict(self)
+
+    def make_solver(self, **kw):
+        from .field import build_field
+        from .solve import EnsembleSolver3D
+        return EnsembleSolver3D(build_field(**self.field_kwargs()), self.cells, self.tol,
+                                self.maxit, **kw)
+
+
+PRESETS_3D = {
+    "pde_test1": ReferencePreset("pde_test1"),
+    "pde_test2": ReferencePreset("pde_test2", a_hat_mode="test2"),
+}
+
 
 CONFIGS = {
     "C1": StudyConfig("C1", cells=64, n_modes=3, delta=0.2, sigma0=1.0, ensemble_size=8,
@@ -81,8 +137,11 @@ CONFIGS = {
 }
 
 
-def get(name: str) -> StudyConfig:
+def get(name: str):
+    if name in PRESETS_3D:
+        return PRESETS_3D[name]
     try:
         return CONFIGS[name.upper()]
     except KeyError:
-        raise KeyError(f"unknown config {name!r}; choose from {sorted(CONFIGS)}") from None
+        raise KeyError(f"unknown config {name!r}; choose from "
+                       f"{sorted(CONFIGS) + sorted(PRESETS_3D)}") from None

@@ -300,6 +300,41 @@ int uqg_assemble_fv2d(uqg_ctx* ctx, int n_cells, int G, int S, const double* a_n
   return UQG_OK;
 }
 
+int uqg_kl_eval_sep3d(uqg_ctx* ctx, int m, const double* qtab, int n_factors, const int* mode_p,
+                      const int* mode_q, const int* mode_r, const double* sqrt_lam, int M,
+                      const double* samples, const int* lane_ids, int G, int S, double a_min,
+                      int a_hat_mode, double a_hat_value, int expansion, double* a_out,
+                      void* stream) {
+  UQG_REQUIRE(ctx && qtab && mode_p && mode_q && mode_r && sqrt_lam && samples && a_out,
+              "uqg_kl_eval_sep3d: NULL argument");
+  UQG_REQUIRE(m >= 2 && n_factors >= 1 && M >= 1 && G >= 1 && S >= 1,
+              "uqg_kl_eval_sep3d: bad sizes");
+  UQG_REQUIRE(a_hat_mode == 0 || a_hat_mode == 1, "unknown a_hat mode");
+  UQG_REQUIRE(expansion == 0 || expansion == 1, "unknown expansion");
+  const long long total = (long long)G * 8 * m * m * m * S;
+  cudaStream_t s = as_stream(stream);
+  UQG_LAUNCH(UQG_K_KL, s,
+             kl_sep3d_kernel<<<grid_for(total, 256), 256, 0, s>>>(
+                 m, qtab, mode_p, mode_q, mode_r, sqrt_lam, M, samples, lane_ids, G, S, a_min,
+                 a_hat_mode, a_hat_value, expansion, a_out, ctx->status_dev));
+  return UQG_OK;
+}
+
+int uqg_assemble_fem3d(uqg_ctx* ctx, int m, int G, int S, const double* a_q, const double* dx_tab,
+                       const double* kyz_tab, const int* row_offsets, double* vals, double* dinv,
+                       void* stream) {
+  UQG_REQUIRE(ctx && a_q && dx_tab && kyz_tab && row_offsets && vals,
+              "uqg_assemble_fem3d: NULL argument");
+  UQG_REQUIRE(m >= 2 && G >= 1 && S >= 1, "uqg_assemble_fem3d: bad sizes");
+  const long long N = (long long)(m - 1) * (m - 1) * (m - 1);
+  const long long total = (long long)G * N * S;
+  cudaStream_t s = as_stream(stream);
+  UQG_LAUNCH(UQG_K_ASSEMBLE, s,
+             assemble_fem3d_kernel<<<grid_for(total, 256), 256, 0, s>>>(
+                 m, G, S, a_q, dx_tab, kyz_tab, row_offsets, vals, dinv));
+  return UQG_OK;
+}
+
 int uqg_jacobi_dinv(uqg_ctx* ctx, int N, int nnz, int S, int G, const int* row_offsets,
                     const int* col_indices, const double* vals, double* dinv, void* stream) {
   UQG_REQUIRE(ctx && row_offsets && dinv, "uqg_jacobi_dinv: NULL argument");

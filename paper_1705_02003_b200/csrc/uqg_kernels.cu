@@ -160,6 +160,112 @@ __global__ void jacobi_dinv_kernel(long long N, int S, int G, long long nnz,
 }
 
 // ===========================================================================
+// 3D trilinear FEM (reference fem3d.py): coefficient at the Gauss points and
+// gather-form assembly into the shared 27-point graph.
+
+// a_out [G][E*8][S]; element e = (ex*m + ey)*m + ez, Gauss point q bit-ordered
+// (x, y, z), z fastest; qtab[f][2*e_d + bit_d] = factor f at that abscissa.
+__global__ void kl_sep3d_kernel(int m, const double* __restrict__ qtab,
+                                const int* __restrict__ mode_p, const int* __restrict__ mode_q,
+                                const int* __restrict__ mode_r,
+                                const double* __restrict__ sqrt_lam, int M,
+                                const double* __restrict__ samples,
+                                const int* __restrict__ lane_ids, int G, int S, double a_min,
+                                int a_hat_mode, double a_hat_value, int expansion,
+                                double* __restrict__ a_out, int* status) {
+  const long long Q = 8LL * m * m * m;
+  const long long total = (long long)G * Q * S;
+  const int w = 2 * m;  // table row length
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(idx % S);
+    const long long gq = idx / S;
+    const long long eq = gq % Q;
+    const int g = (int)(gq / Q);
+    const long long e = eq >> 3;
+    const int q = (int)(eq & 7);
+    const int ez = (int)(e % m), ey = (int)((e / m) % m), ex = (int)(e / ((long long)m * m));
+    const int tx = 2 * ex + ((q >> 2) & 1), ty = 2 * ey + ((q >> 1) & 1), tz = 2 * ez + (q & 1);
+    const size_t lane = (size_t)g * S + s;
+    const double* y = samples + (lane_ids ? (size_t)__ldg(&lane_ids[lane]) : lane) * M;
+    double acc = 0.0;
+    for (int k = 0; k < M; ++k) {
+      const double mv =
+          __dmul_rn(__dmul_rn(__ldg(&qtab[(size_t)__ldg(&mode_p[k]) * w + tx]),
+                              __ldg(&qtab[(size_t)__ldg(&mode_q[k]) * w + ty])),
+                    __ldg(&qtab[(size_t)__ldg(&mode_r[k]) * w + tz]));
+      acc = __fma_rn(__dmul_rn(y[k], __ldg(&sqrt_lam[k])), mv, acc);
+    }
+    const double a = kl_finish(acc, expansion, a_min, a_hat_of(y, M, a_hat_mode, a_hat_value));
+    if (a <= 0.0) atomicOr(status, 1);
+    a_out[idx] = a;
+  }
+}
+
+// One thread per (group, row, lane).  For each neighbour j of row i (CSR
+// order = lexicographic (dx, dy, dz)), sum the contributions of the elements
+// holding both nodes in increasing element index (np.bincount's order over
+// the (element, a, b) pairs):  K_e(a,b) = (sum_q a_q Dx[q][a][b]) + Kyz[a][b].
+__global__ void assemble_fem3d_kernel(int m, int G, int S, const double* __restrict__ a_q,
+                                      const double* __restrict__ dx_tab,
+                                      const double* __restrict__ kyz_tab,
+                                      const int* __restrict__ row_offsets,
+                                      double* __restrict__ vals, double* __restrict__ dinv) {
+  const int k = m - 1;
+  const long long N = (long long)k * k * k;
+  const long long nnz = row_offsets[N];
+  const long long E = (long long)m * m * m;
+  const long long total = (long long)G * N * S;
+  __shared__ double sdx[512], skyz[64];
+  for (int i = threadIdx.x; i < 512; i += blockDim.x) sdx[i] = dx_tab[i];
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) skyz[i] = kyz_tab[i];
+  __syncthreads();
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(idx % S);
+    const long long gr = idx / S;
+    const long long row = gr % N;
+    const int g = (int)(gr / N);
+    const int iz = (int)(row % k) + 1, iy = (int)((row / k) % k) + 1,
+              ix = (int)(row / ((long long)k * k)) + 1;
+    const double* aq = a_q + (size_t)g * E * 8 * S + s;
+    double* v = vals + ((size_t)g * nnz + row_offsets[row]) * S + s;
+    int kk = 0;
+    double diag = 0.0;
+    for (int dx = -1; dx <= 1; ++dx) {
+      const int jx = ix + dx;
+      if (jx < 1 || jx > k) continue;
+      for (int dy = -1; dy <= 1; ++dy) {
+        const int jy = iy + dy;
+        if (jy < 1 || jy > k) continue;
+        for (int dz = -1; dz <= 1; ++dz) {
+          const int jz = iz + dz;
+          if (jz < 1 || jz > k) continue;
+          double sum = 0.0;
+          for (int ex = max(ix, jx) - 1; ex <= min(ix, jx); ++ex) {
+            for (int ey = max(iy, jy) - 1; ey <= min(iy, jy); ++ey) {
+              for (int ez = max(iz, jz) - 1; ez <= min(iz, jz); ++ez) {
+                const long long e = ((long long)ex * m + ey) * m + ez;
+                const int a = (ix - ex) * 4 + (iy - ey) * 2 + (iz - ez);
+                const int b = (jx - ex) * 4 + (jy - ey) * 2 + (jz - ez);
+                double kx = 0.0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                  kx = __dadd_rn(kx, __dmul_rn(aq[(size_t)(e * 8 + q) * S], sdx[q * 64 + a * 8 + b]));
+                sum = __dadd_rn(sum, __dadd_rn(kx, skyz[a * 8 + b]));
+              }
+            }
+          }
+          v[(size_t)(kk++) * S] = sum;
+          if (dx == 0 && dy == 0 && dz == 0) diag = sum;
+        }
+      }
+    }
+    if (dinv) dinv[idx] = __ddiv_rn(1.0, diag);
+  }
+}
+
+// ===========================================================================
 // Grouping: stable rank sort + chunk/pad (grouping.py:83-122)
 
 // rank_i = #{j : k_j < k_i or (k_j == k_i and j < i)}; order[rank_i] = i.

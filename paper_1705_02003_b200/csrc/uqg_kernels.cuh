@@ -48,6 +48,14 @@ __global__ void assemble_fv2d_kernel(int n, int G, int S, const double* a_nodes,
 __global__ void jacobi_dinv_kernel(long long N, int S, int G, long long nnz, const int* ro,
                                    const int* ci, const double* vals, double* dinv, int* status,
                                    int raw);
+__global__ void kl_sep3d_kernel(int m, const double* qtab, const int* mode_p, const int* mode_q,
+                                const int* mode_r, const double* sqrt_lam, int M,
+                                const double* samples, const int* lane_ids, int G, int S,
+                                double a_min, int a_hat_mode, double a_hat_value, int expansion,
+                                double* a_out, int* status);
+__global__ void assemble_fem3d_kernel(int m, int G, int S, const double* a_q, const double* dx_tab,
+                                      const double* kyz_tab, const int* row_offsets, double* vals,
+                                      double* dinv);
 __global__ void rank_sort_kernel(const double* keys, int n, int* order, int* status);
 __global__ void chunk_kernel(const int* order, int n, int S, int K, int* groups, int* pad);
 

@@ -49,12 +49,11 @@ def adaptive_run(cfg: StudyConfig, solver: EnsembleSolver2D | None = None, shard
     ``shard``: optional callable(plan, coords_by_id) -> (iters, qois, notes)
     replacing ``solver.solve_plan`` (multi-GPU sharded solve + allgather).
     """
-    if solver is None:
-        solver = EnsembleSolver2D(build_field(**cfg.field_kwargs()), cfg.cells, cfg.tol, cfg.maxit,
-                                  cfg.a2)
+    if solver is None and shard is None:
+        solver = cfg.make_solver()
     solve = shard or solver.solve_plan
     S = cfg.ensemble_size
-    grid = SparseGrid(cfg.n_dims if hasattr(cfg, "n_dims") else cfg.n_modes)
+    grid = SparseGrid(cfg.n_modes)
     batch = grid.add_initial_levels(cfg.initial_level)
     if len(batch) > cfg.n_max:
         raise ValueError(f"n_max={cfg.n_max} is smaller than the {len(batch)}-point initial grid")

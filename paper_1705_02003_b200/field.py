@@ -1,17 +1,20 @@
-"""Truncated-KL diffusion coefficient for the 2D ensemble operator.
+"""Truncated-KL diffusion coefficient (2D for the BASELINE operator, 3D for the
+reference's FEM presets).
 
 Host-side setup (one-time per field/mesh) plus the device
 evaluation of the coefficient (row 1):
 
 * ``eigenpairs_1d``  - Nystrom eigenpairs of exp(-|x-x'|/delta) on [0,1]
   (reference ``random_field.py:59-92``; dense ``scipy.linalg.eigh``, host);
-* ``build_field``    - 2D separable mode selection by descending product
-  eigenvalue, lexicographic (p, q) tie-break, with the reference's "enough 1D
-  modes" doubling rule (``random_field.py:174-251`` restated for pairs);
-* ``KLField2D.eval_a_batch`` - a(x, y) = a_min + a_hat(y) f(sum sqrt(lam) b(x) y)
+* ``build_field``    - separable mode selection by descending product
+  eigenvalue, lexicographic index tie-break, with the reference's "enough 1D
+  modes" doubling rule (``random_field.py:174-251``; pairs for dim=2, the
+  reference's own triples for dim=3);
+* ``KLField.eval_a_batch`` - a(x, y) = a_min + a_hat(y) f(sum sqrt(lam) b(x) y)
   on the GPU through ``uqg_kl_eval_table`` (``random_field.py:145-166``);
-* ``KLField2D.node_tables`` - the 1D factor values at the grid abscissae that
-  let ``uqg_kl_eval_sep2d`` rebuild every mode value on the fly.
+* ``KLField.node_tables`` / ``quad_tables`` - the 1D factor values at the grid
+  abscissae that let ``uqg_kl_eval_sep2d`` / ``uqg_kl_eval_sep3d`` rebuild every
+  mode value on the fly.
 """
 
 from __future__ import annotations
@@ -24,7 +27,10 @@ import scipy.linalg
 from . import _lib
 from .errors import FieldError
 
-__all__ = ["Eigenpair1D", "eigenpairs_1d", "KLField2D", "build_field"]
+__all__ = ["Eigenpair1D", "eigenpairs_1d", "KLField", "KLField2D", "build_field",
+           "GAUSS"]
+
+GAUSS = 1.0 / np.sqrt(3.0)  # 2-point Gauss abscissa (fem3d.py:26)
 
 
 @dataclass(frozen=True)
@@ -64,11 +70,13 @@ _EXPANSION = {"log": 0, "linear": 1}
 
 
 @dataclass(frozen=True)
-class KLField2D:
-    """2D analogue of ``KLDiffusionField`` (``random_field.py:95-171``).
+class KLField:
+    """Analogue of ``KLDiffusionField`` (``random_field.py:95-171``) in 2 or 3 dims.
 
-    ``modes[m] = (p, q)`` selects b_m(x) = e_p(x0) e_q(x1); eigenvalues carry
-    the sigma0 scaling; ``a_y`` is the constant second-direction coefficient.
+    ``modes[m]`` is a tuple of 1D factor ids (one per spatial dimension): the
+    m-th mode is b_m(x) = prod_d e_{modes[m][d]}(x_d); eigenvalues carry the
+    sigma0 scaling; ``a_y`` / ``a_z`` are the constant coefficients of the
+    other directions (only the first is random, ``fem3d.py:158-160``).
     """
 
     delta: float
@@ -81,10 +89,15 @@ class KLField2D:
     eigenvalues: np.ndarray
     modes: tuple
     factors: tuple
+    a_z: float = 1.0
 
     @property
     def n_modes(self) -> int:
         return len(self.modes)
+
+    @property
+    def dim(self) -> int:
+        return len(self.modes[0])
 
     def a_hat(self, y) -> np.ndarray:
         y = np.atleast_2d(np.asarray(y, dtype=float))
@@ -95,24 +108,26 @@ class KLField2D:
         return self.a_hat_value * np.where(r < d / 4.0, 1.0, np.where(r < d / 2.0, 100.0, 10.0))
 
     def mode_values(self, points) -> np.ndarray:
-        """(P, 2) -> (M, P) host table (setup, ``random_field.py:135-143``)."""
+        """(P, dim) -> (M, P) host table (setup, ``random_field.py:135-143``)."""
         pts = np.asarray(points, dtype=float)
-        if pts.ndim != 2 or pts.shape[1] != 2:
-            raise FieldError(f"points must have shape (P, 2), got {pts.shape}")
+        if pts.ndim != 2 or pts.shape[1] != self.dim:
+            raise FieldError(f"points must have shape (P, {self.dim}), got {pts.shape}")
         tab = np.empty((self.n_modes, len(pts)))
-        for m, (p, q) in enumerate(self.modes):
-            tab[m] = self.factors[p](pts[:, 0]) * self.factors[q](pts[:, 1])
+        for m, ids in enumerate(self.modes):
+            v = self.factors[ids[0]](pts[:, 0])
+            for d in range(1, self.dim):
+                v = v * self.factors[ids[d]](pts[:, d])
+            tab[m] = v
         return tab
 
     # -- device -------------------------------------------------------------
     def _device_consts(self):
         cache = self.__dict__.get("_dev_cache")
         if cache is None:
-            cache = {
-                "sqrt_lam": _lib.to_dev(np.sqrt(self.eigenvalues)),
-                "mode_p": _lib.to_dev(np.array([p for p, _ in self.modes], dtype=np.int32)),
-                "mode_q": _lib.to_dev(np.array([q for _, q in self.modes], dtype=np.int32)),
-            }
+            ids = np.array(self.modes, dtype=np.int32)  # (M, dim)
+            cache = {"sqrt_lam": _lib.to_dev(np.sqrt(self.eigenvalues))}
+            for d, name in enumerate(("mode_p", "mode_q", "mode_r")[: self.dim]):
+                cache[name] = _lib.to_dev(np.ascontiguousarray(ids[:, d]))
             object.__setattr__(self, "_dev_cache", cache)
         return cache
 
@@ -145,11 +160,24 @@ class KLField2D:
         x = np.arange(cells + 1) * (1.0 / cells)
         return np.stack([f(x) for f in self.factors])
 
+    def quad_tables(self, cells: int) -> np.ndarray:
+        """[n_factors][2*cells] factor values at the 1D Gauss abscissae of the
+        hex mesh: entry 2*e + bit is (e + 0.5) h + (+-1/sqrt3)(h/2), computed with
+        the reference's expression for quad_points (``fem3d.py:93-95``)."""
+        h = 1.0 / cells
+        centers = (np.arange(cells) + 0.5) * h
+        signs = np.array([-1.0, 1.0]) * GAUSS
+        x = (centers[:, None] + signs[None, :] * (h / 2.0)).ravel()
+        return np.stack([f(x) for f in self.factors])
+
+
+KLField2D = KLField  # backwards-compatible name for the 2D field
+
 
 def build_field(delta: float, sigma0: float, n_modes: int, a_min: float,
                 a_hat_mode: str = "constant", a_hat_value: float = 1.0, a_y: float = 1.0,
                 nystrom_points: int = 513, sigma0_convention: str = "stddev",
-                expansion: str = "log") -> KLField2D:
+                expansion: str = "log", dim: int = 2, a_z: float = 1.0) -> KLField:
     if n_modes < 1:
         raise FieldError(f"n_modes must be >= 1, got {n_modes}")
     if sigma0 < 0:
@@ -162,22 +190,29 @@ def build_field(delta: float, sigma0: float, n_modes: int, a_min: float,
         raise FieldError(f"unknown a_hat mode {a_hat_mode!r}")
     if expansion not in _EXPANSION:
         raise FieldError(f"unknown expansion {expansion!r}")
+    if dim not in (2, 3):
+        raise FieldError(f"dim must be 2 or 3, got {dim}")
     scale = sigma0 ** 2 if sigma0_convention == "stddev" else sigma0
     n1 = min(max(2, n_modes), nystrom_points)
     while True:
         facs = eigenpairs_1d(delta, n1, nystrom_points)
         lam = np.array([f.eigenvalue for f in facs])
-        ranked = sorted(((lam[p] * lam[q], (p, q)) for p in range(n1) for q in range(n1)),
-                        key=lambda e: (-e[0], e[1]))
+        if dim == 2:
+            ranked = [(lam[p] * lam[q], (p, q)) for p in range(n1) for q in range(n1)]
+        else:
+            ranked = [(lam[p] * lam[q] * lam[r], (p, q, r))
+                      for p in range(n1) for q in range(n1) for r in range(n1)]
+        ranked.sort(key=lambda e: (-e[0], e[1]))
         if len(ranked) < n_modes:
             if n1 == nystrom_points:
-                raise FieldError(f"cannot form {n_modes} 2D modes from {n1} 1D modes")
+                raise FieldError(f"cannot form {n_modes} {dim}D modes from {n1} 1D modes")
             n1 = min(2 * n1, nystrom_points)
             continue
         chosen = ranked[:n_modes]
-        if chosen[-1][0] >= lam[n1 - 1] * lam[0] or n1 == nystrom_points:
+        # an excluded product with an index >= n1 is at most lam[n1-1] * lam[0]^(dim-1)
+        if chosen[-1][0] >= lam[n1 - 1] * lam[0] ** (dim - 1) or n1 == nystrom_points:
             break
         n1 = min(2 * n1, nystrom_points)
-    return KLField2D(delta, sigma0, a_min, a_hat_mode, a_hat_value, a_y, expansion,
-                     np.array([scale * v for v, _ in chosen]), tuple(m for _, m in chosen),
-                     tuple(facs))
+    return KLField(delta, sigma0, a_min, a_hat_mode, a_hat_value, a_y, expansion,
+                   np.array([scale * v for v, _ in chosen]), tuple(m for _, m in chosen),
+                   tuple(facs), a_z)

@@ -25,9 +25,11 @@ import numpy as np
 from . import _lib
 from .ensemble import run_pcg
 from .errors import FemError
+from .fem3d import StructuredMesh3D
 from .fv2d import FieldTables, StructuredMesh2D, assemble_values, kl_nodes
 
-__all__ = ["LevelSolveResult", "EnsembleSolver2D"]
+__all__ = ["LevelSolveResult", "EnsembleSolver", "EnsembleSolver2D", "EnsembleSolver3D",
+           "FV2DOperator", "FEM3DOperator"]
 
 
 @dataclass
@@ -42,15 +44,79 @@ class LevelSolveResult:
     stats: dict = dc_field(default_factory=dict)
 
 
-class EnsembleSolver2D:
-    """Device solver for one (field, mesh, solver-config) triple."""
+# ---------------------------------------------------------------------------
+# operators: how a group's coefficient and matrix are built on the device
 
-    def __init__(self, field, cells: int, tol: float = 1e-8, maxit: int = 30000,
-                 a2: str = "const", mem_fraction: float = 0.8, max_groups_per_wave: int | None = None):
-        self.field = field
+class FV2DOperator:
+    """BASELINE.json's 2D 5-point FV operator (``fv2d.py``)."""
+
+    max_row_len = 5
+
+    def __init__(self, field, cells: int, a2: str = "const"):
+        if field.dim != 2:
+            raise FemError("the 2D operator needs a 2D field")
+        self.field, self.a2 = field, a2
         self.mesh = StructuredMesh2D(cells)
         self.tables = FieldTables(field, self.mesh)
-        self.tol, self.maxit, self.a2 = float(tol), int(maxit), a2
+        self.n_dofs, self.nnz, self.n_coef = self.mesh.n_dofs, self.mesh.nnz, self.mesh.n_nodes
+        self.rhs_const = self.mesh.h * self.mesh.h
+
+    def graph(self):
+        return self.mesh.device()
+
+    def coefficients(self, d_samples, lane_ids, G, S, out):
+        kl_nodes(self.tables, d_samples, G, S, out=out, lane_ids=lane_ids)
+
+    def assemble(self, a, G, S, vals, dinv):
+        assemble_values(self.mesh, a, G, S, self.field.a_y, self.a2, vals=vals, dinv=dinv)
+
+
+class FEM3DOperator:
+    """The reference's 3D trilinear FEM (``fem3d.py:138-175``), on the device."""
+
+    max_row_len = 27
+
+    def __init__(self, field, cells: int):
+        if field.dim != 3:
+            raise FemError("the 3D operator needs a 3D field")
+        if field.a_y <= 0 or field.a_z <= 0:
+            raise FemError("non-positive diffusion coefficient a_y / a_z")
+        self.field = field
+        self.mesh = m = StructuredMesh3D(cells)
+        self.n_dofs, self.nnz, self.n_coef = m.n_dofs, m.nnz, m.n_quad
+        self.rhs_const = m.load
+        self.qtab = _lib.to_dev(field.quad_tables(cells))
+        self.kyz = _lib.to_dev(np.ascontiguousarray(m.kyz(field.a_y, field.a_z)))
+        self.consts = field._device_consts()
+        self.codes = field.codes()
+
+    def graph(self):
+        rowptr, col, _ = self.mesh.device()
+        return rowptr, col
+
+    def coefficients(self, d_samples, lane_ids, G, S, out):
+        f, c = self.field, self.consts
+        _lib.call("uqg_kl_eval_sep3d", _lib.ctx(), self.mesh.cells, _lib.ptr(self.qtab),
+                  len(f.factors), _lib.ptr(c["mode_p"]), _lib.ptr(c["mode_q"]),
+                  _lib.ptr(c["mode_r"]), _lib.ptr(c["sqrt_lam"]), f.n_modes, _lib.ptr(d_samples),
+                  _lib.ptr(lane_ids), G, S, float(f.a_min), self.codes[0], float(f.a_hat_value),
+                  self.codes[1], _lib.ptr(out), _lib.stream(), invalid=FemError)
+
+    def assemble(self, a, G, S, vals, dinv):
+        rowptr, _, dx = self.mesh.device()
+        _lib.call("uqg_assemble_fem3d", _lib.ctx(), self.mesh.cells, G, S, _lib.ptr(a),
+                  _lib.ptr(dx), _lib.ptr(self.kyz), _lib.ptr(rowptr), _lib.ptr(vals),
+                  _lib.ptr(dinv), _lib.stream(), invalid=FemError)
+
+
+class EnsembleSolver:
+    """Device solver for one (operator, solver-config) pair."""
+
+    def __init__(self, operator, tol: float = 1e-8, maxit: int = 30000,
+                 mem_fraction: float = 0.8, max_groups_per_wave: int | None = None):
+        self.op = operator
+        self.field, self.mesh = operator.field, operator.mesh
+        self.tol, self.maxit = float(tol), int(maxit)
         self.mem_fraction = mem_fraction
         self.max_groups_per_wave = max_groups_per_wave
         self._bufs = {}
@@ -58,9 +124,9 @@ class EnsembleSolver2D:
 
     # -- memory planning ----------------------------------------------------
     def bytes_per_group(self, S: int) -> int:
-        m = self.mesh
-        per = 8 * S * (m.nnz + 2 * m.n_dofs + m.n_nodes)      # vals, dinv, x, a_nodes
-        per += _lib.load().uqg_pcg_workspace_bytes(m.n_dofs, m.nnz, S, 1)  # r, p, Ap, ...
+        o = self.op
+        per = 8 * S * (o.nnz + 2 * o.n_dofs + o.n_coef)      # vals, dinv, x, coefficient
+        per += _lib.load().uqg_pcg_workspace_bytes(o.n_dofs, o.nnz, S, 1)  # r, p, Ap, ...
         return int(per)
 
     def wave_size(self, S: int, K: int) -> int:
@@ -85,7 +151,7 @@ class EnsembleSolver2D:
 
     def _workspace(self, G, S):
         torch = _lib._torch()
-        m = self.mesh
+        m = self.op
         need = int(_lib.load().uqg_pcg_workspace_bytes(m.n_dofs, m.nnz, S, G)) + (1 << 20)
         if self._ws is None or self._ws.numel() < need:
             self._ws = None
@@ -107,19 +173,19 @@ class EnsembleSolver2D:
         Returns device tensors (iters, conv, frozen, ens, qoi, hist, x).
         """
         torch = _lib._torch()
-        m, f = self.mesh, self.field
-        a = self._buf("a", G * m.n_nodes * S, torch.float64)
-        vals = self._buf("vals", G * m.nnz * S, torch.float64)
-        dinv = self._buf("dinv", G * m.n_dofs * S, torch.float64)
-        kl_nodes(self.tables, d_samples, G, S, out=a, lane_ids=lane_ids)
-        assemble_values(m, a, G, S, f.a_y, self.a2, vals=vals, dinv=dinv)
-        rowptr, col = m.device()
+        o = self.op
+        a = self._buf("a", G * o.n_coef * S, torch.float64)
+        vals = self._buf("vals", G * o.nnz * S, torch.float64)
+        dinv = self._buf("dinv", G * o.n_dofs * S, torch.float64)
+        o.coefficients(d_samples, lane_ids, G, S, a)
+        o.assemble(a, G, S, vals, dinv)
+        rowptr, col = o.graph()
         self._workspace(G, S)
         x, iters, conv, frz, ens, hist = run_pcg(
-            m.n_dofs, m.nnz, S, G, rowptr, col, vals, None, m.h * m.h, dinv, self.tol,
-            self.maxit, record_history, max_row_len=5)
+            o.n_dofs, o.nnz, S, G, rowptr, col, vals, None, o.rhs_const, dinv, self.tol,
+            self.maxit, record_history, max_row_len=o.max_row_len)
         q = torch.empty((G * S,), dtype=torch.float64, device=_lib.device())
-        _lib.call("uqg_lane_dot", _lib.ctx(), m.n_dofs, S, G, _lib.ptr(x), _lib.ptr(x), _lib.ptr(q),
+        _lib.call("uqg_lane_dot", _lib.ctx(), o.n_dofs, S, G, _lib.ptr(x), _lib.ptr(x), _lib.ptr(q),
                   _lib.stream())
         if _lib.status_sync() & 1:
             raise FemError("non-positive diffusion coefficient at a mesh node")
@@ -241,3 +307,24 @@ class EnsembleSolver2D:
                     iters[sid] = int(res.iterations[k, s])
                     qois[sid] = float(res.qoi[k, s])
         return iters, qois, notes
+
+
+class EnsembleSolver2D(EnsembleSolver):
+    """Level-batched solver on BASELINE.json's 2D 5-point FV operator."""
+
+    def __init__(self, field, cells: int, tol: float = 1e-8, maxit: int = 30000,
+                 a2: str = "const", mem_fraction: float = 0.8,
+                 max_groups_per_wave: int | None = None):
+        super().__init__(FV2DOperator(field, cells, a2), tol, maxit, mem_fraction,
+                         max_groups_per_wave)
+        self.tables, self.a2 = self.op.tables, a2
+
+
+class EnsembleSolver3D(EnsembleSolver):
+    """Level-batched solver on the reference's 3D trilinear FEM operator
+    (``harness._PdeProblem``: ``fem3d.py`` + ``ensemble_pcg``)."""
+
+    def __init__(self, field, cells: int, tol: float = 1e-7, maxit: int = 30000,
+                 mem_fraction: float = 0.8, max_groups_per_wave: int | None = None):
+        super().__init__(FEM3DOperator(field, cells), tol, maxit, mem_fraction,
+                         max_groups_per_wave)

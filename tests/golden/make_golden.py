@@ -180,6 +180,77 @@ def reference_study(cfg, max_levels=None):
     return {"config": cfg.to_dict(), "levels": levels}
 
 
+def fem3d_cases():
+    """The reference's own 3D FEM: assembly, solves and the Laplacian centre value."""
+    from uqgroup import fem3d as rfem
+
+    fld = ref_rf.build_field(delta=0.25, sigma0=np.sqrt(300.0), n_modes=4, a_min=0.1,
+                             sigma0_convention="kernel")
+    mesh = rfem.StructuredMesh(6)
+    ys = np.array([[0.3, -0.7, 0.1, 0.9], [0.3, -0.7, 0.1, 0.9], [-1.0, 1.0, -1.0, 1.0]])
+    sysm = rfem.assemble(mesh, fld, ys)
+    res = ref_ens.ensemble_pcg(sysm.matrix, sysm.rhs, tol=1e-10, maxit=4000)
+    lap = ref_rf.build_field(delta=0.25, sigma0=0.0, n_modes=1, a_min=0.0, a_hat_value=1.0,
+                             expansion="linear")
+    mesh16 = rfem.StructuredMesh(16)
+    s16 = rfem.assemble(mesh16, lap, np.zeros((1, 1)))
+    r16 = ref_ens.ensemble_pcg(s16.matrix, s16.rhs, tol=1e-10, maxit=4000)
+    k16 = rfem.assemble(mesh16, fld, ys)
+    rk = ref_ens.ensemble_pcg(k16.matrix, k16.rhs, tol=1e-7, maxit=30000)
+    np.savez_compressed(
+        HERE / "fem3d.npz", samples=ys, a_q=fld.eval_a_batch(mesh.quad_points, ys),
+        values=sysm.matrix.values, rhs=sysm.rhs, row_offsets=mesh.row_offsets,
+        col_indices=mesh.col_indices, solution=res.solution, iterations=res.iterations_per_lane,
+        lap_centre=np.array(r16.solution[0][mesh16.center_dof()]),
+        lap_iterations=r16.iterations_per_lane, m16_iterations=rk.iterations_per_lane,
+        m16_qoi=np.array([rfem.qoi(u) for u in rk.solution]))
+
+
+def reference_study_3d(name):
+    """The reference's own adaptive loop on its own preset (harness.py:575-701,
+    exec plan 'sur'), recording per-sample iterations AND QoIs."""
+    from uqgroup import harness as H
+
+    cfg = H.preset_config(name)
+    prob = H._PdeProblem(cfg)
+    S = cfg.ensemble_size
+    grid = HierGrid(cfg.n_dims, domain=prob.box)
+    batch = grid.add_initial_levels(cfg.initial_level)
+    policy = RefinementPolicy(tau=cfg.tau, channel="qoi", max_points=cfg.n_max)
+    levels, level = [], 0
+    while True:
+        level += 1
+        start = len(grid) - len(batch)
+        ids = list(range(start, len(grid)))
+        coords = grid.node_coords()[start:]
+        coords_by_id = {sid: coords[i] for i, sid in enumerate(ids)}
+        predicted = None
+        if level == 1:
+            plan = ref_grp.group_natural(ids, S, level, "sur")
+        else:
+            predicted = grid.eval_many("iterations", coords, n_nodes=start)
+            plan = ref_grp.group_by_key(ids, {sid: float(predicted[i]) for i, sid in enumerate(ids)},
+                                        S, level, "sur")
+        iters, qois, notes = prob.solve_plan(plan, coords_by_id, None)
+        nodes = grid.nodes[start:]
+        grid.compute_surpluses("qoi", {nd: qois[sid] for nd, sid in zip(nodes, ids)})
+        grid.compute_surpluses("iterations", {nd: iters[sid] for nd, sid in zip(nodes, ids)})
+        levels.append({
+            "level": level, "ids": ids, "coords": coords.tolist(),
+            "predicted": None if predicted is None else predicted.tolist(),
+            "ensembles": [list(g) for g in plan.ensembles], "padding": list(plan.padding),
+            "iterations": [iters[sid] for sid in ids], "qoi": [qois[sid] for sid in ids],
+            "notes": notes,
+        })
+        print(f"  {name} level {level}: {len(ids)} samples", flush=True)
+        out = grid.refine(policy)
+        if not out.new_nodes:
+            stop = "budget_exhausted" if out.budget_exhausted else "tolerance_met"
+            break
+        batch = out.new_nodes
+    return {"preset": name, "stop": stop, "levels": levels}
+
+
 def c2_group():
     cfg = CONFIGS["C2"]
     fld = field2d.KL2D.select(**cfg.field_kwargs())
@@ -226,4 +297,10 @@ if __name__ == "__main__":
         (HERE / "c1_adaptive.json").write_text(json.dumps(doc))
     if "c2" in which:
         c2_group()
+    if "fem3d" in which:
+        fem3d_cases()
+    for preset in ("pde_test1", "pde_test2"):
+        if preset in which:
+            doc = reference_study_3d(preset)
+            (HERE / f"{preset}_study.json").write_text(json.dumps(doc))
     print("golden fixtures written to", HERE)
