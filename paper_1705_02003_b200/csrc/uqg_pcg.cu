@@ -478,10 +478,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // tile index of the i-th tile a block processes (its chunks b, b+B, ...)
+// (32-bit index math: tiles < 2^31, chunk_tiles <= tiles / kMaxChunks + 8)
 __device__ __forceinline__ long long block_tile(const Geo& geo, int i, int& chunk) {
-  const long long j = i / geo.chunk_tiles;
-  chunk = (int)(blockIdx.x + j * gridDim.x);
-  return (long long)chunk * geo.chunk_tiles + i % geo.chunk_tiles;
+  const int ct = (int)geo.chunk_tiles;
+  const int j = i / ct;
+  chunk = (int)blockIdx.x + j * (int)gridDim.x;
+  return (long long)chunk * ct + (i - j * ct);
 }
 
 __device__ __forceinline__ int block_tile_count(const Geo& geo) {
@@ -494,7 +496,7 @@ __device__ __forceinline__ int block_tile_count(const Geo& geo) {
 }
 
 template <int ML>
-__global__ void __launch_bounds__(256) pcg_spmv_tma_kernel(long long N, long long nnz, Geo geo,
+__global__ void __launch_bounds__(256, 3) pcg_spmv_tma_kernel(long long N, long long nnz, Geo geo,
                                                            PcgState st,
                                                            const int* __restrict__ ro,
                                                            const int* __restrict__ ci,
@@ -595,6 +597,161 @@ __global__ void __launch_bounds__(256) pcg_spmv_tma_kernel(long long N, long lon
   }
 }
 
+// Variant with the tile metadata (row offsets, column indices) also staged in
+// shared memory ahead of use by all threads, so a row's dependent chain is
+// only the p gather (row offsets of tile i+2 and columns of tile i+1 are
+// loaded before tile i is computed and stored after it).  Identical results.
+template <int ML>
+__global__ void __launch_bounds__(256, 3) pcg_spmv_tma_meta_kernel(
+    long long N, long long nnz, Geo geo, PcgState st, const int* __restrict__ ro,
+    const int* __restrict__ ci, const double* __restrict__ vals, const double* __restrict__ p,
+    double* __restrict__ ap) {
+  constexpr int V = 2;
+  extern __shared__ __align__(128) double red[];
+  const int g = blockIdx.y, t = threadIdx.x;
+  if (st.done[g] != kRunning) return;
+  const int S = geo.S, R = geo.R, T = geo.T;
+  const int stage_doubles = R * ML * S;
+  const int ro_stride = (R + 2) & ~1, col_stride = R * ML;
+  double* stage = red + V * T;
+  int* ro_s = reinterpret_cast<int*>(stage + kStages * stage_doubles);
+  int* col_s = ro_s + kStages * ro_stride;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(col_s + kStages * col_stride);
+  const double* vg = vals + (size_t)g * nnz * S;
+  const int n_tiles = block_tile_count(geo);
+  const int ct = (int)geo.chunk_tiles;
+  const long long tiles = geo.tiles;
+
+  auto tile_of = [&](int i) -> long long {
+    const int j = i / ct;
+    return ((long long)blockIdx.x + (long long)j * gridDim.x) * ct + (i - j * ct);
+  };
+  auto nrows = [&](long long tile) -> int {
+    const long long n = N - tile * R;
+    return n < R ? (int)n : R;
+  };
+  auto issue = [&](int i, int k0, int k1) {  // thread 0 only
+    const uint32_t bytes = (uint32_t)(k1 - k0) * (uint32_t)S * 8u;
+    uint64_t* bar = &bars[i % kStages];
+    fence_proxy_async();
+    mbar_expect_tx(bar, bytes);
+    if (bytes) bulk_g2s(stage + (i % kStages) * stage_doubles, vg + (size_t)k0 * S, bytes, bar);
+  };
+
+  // prologue: metadata of tiles 0, 1 and columns of tile 0; bulk copies 0..kStages-1
+  if (t == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  for (int i = 0; i < 2 && i < n_tiles; ++i) {
+    const long long tl = tile_of(i);
+    if (t <= nrows(tl)) ro_s[(i % kStages) * ro_stride + t] = __ldg(&ro[tl * R + t]);
+  }
+  __syncthreads();
+  if (n_tiles > 0) {
+    const int nr = nrows(tile_of(0));
+    const int k0 = ro_s[0], cnt = ro_s[nr] - k0;
+    for (int q = t; q < cnt; q += T) col_s[q] = __ldg(&ci[k0 + q]);
+  }
+  if (t == 0) {
+    for (int i = 0; i < kStages && i < n_tiles; ++i) {
+      const long long tl = tile_of(i);
+      const int nr = nrows(tl);
+      if (i < 2) {
+        issue(i, ro_s[(i % kStages) * ro_stride], ro_s[(i % kStages) * ro_stride + nr]);
+      } else {
+        issue(i, __ldg(&ro[tl * R]), __ldg(&ro[tl * R + nr]));
+      }
+    }
+  }
+  __syncthreads();
+
+  const int sl = t % geo.Lp, rr = t / geo.Lp;
+  const size_t base = (size_t)g * N * S + V * sl;
+  const double* pg = p + base;
+  double acc[1][V] = {};
+  long long tile = n_tiles > 0 ? tile_of(0) : 0;
+  long long tile1 = n_tiles > 1 ? tile_of(1) : 0;
+  for (int i = 0; i < n_tiles; ++i) {
+    const int s0 = i % kStages, s1 = (i + 1) % kStages, s2 = (i + 2) % kStages;
+    const long long tile2 = i + 2 < n_tiles ? tile_of(i + 2) : 0;
+    // prefetch: row offsets of tile i+2, columns of tile i+1, value range of i+kStages
+    int ro_next = 0, col_next[2] = {0, 0};
+    if (i + 2 < n_tiles && t <= nrows(tile2)) ro_next = __ldg(&ro[tile2 * R + t]);
+    int cnt1 = 0;
+    if (i + 1 < n_tiles) {
+      const int* rs1 = ro_s + s1 * ro_stride;
+      const int k01 = rs1[0];
+      cnt1 = rs1[nrows(tile1)] - k01;
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (t + u * T < cnt1) col_next[u] = __ldg(&ci[k01 + t + u * T]);
+    }
+    int kn0 = 0, kn1 = 0;
+    if (t == 0 && i + kStages < n_tiles) {
+      const long long tl3 = tile_of(i + kStages);
+      kn0 = __ldg(&ro[tl3 * R]);
+      kn1 = __ldg(&ro[tl3 * R + nrows(tl3)]);
+    }
+    mbar_wait(&bars[s0], (uint32_t)((i / kStages) & 1));
+    if (sl < geo.L && rr < nrows(tile)) {
+      const long long row = tile * R + rr;
+      const int* rs = ro_s + s0 * ro_stride;
+      const int* cs = col_s + s0 * col_stride;
+      const int kt0 = rs[0];
+      const int k0 = rs[rr] - kt0, len = rs[rr + 1] - rs[rr];
+      const double* sv = stage + s0 * stage_doubles + (size_t)k0 * S + V * sl;
+      int c[ML];
+#pragma unroll
+      for (int e = 0; e < ML; ++e) c[e] = e < len ? cs[k0 + e] : 0;
+      double b[ML][V];
+#pragma unroll
+      for (int e = 0; e < ML; ++e)
+        if (e < len) ldgv<V>(pg + (size_t)c[e] * S, b[e]);
+      double y[V] = {0.0, 0.0};
+#pragma unroll
+      for (int e = 0; e < ML; ++e) {
+        if (e < len) {
+          const double2 a = *reinterpret_cast<const double2*>(sv + (size_t)e * S);
+          y[0] = __dadd_rn(y[0], __dmul_rn(a.x, b[e][0]));
+          y[1] = __dadd_rn(y[1], __dmul_rn(a.y, b[e][1]));
+        }
+      }
+      stv<V>(ap + base + row * S, y);
+      double pv[V];
+      ldgv<V>(pg + row * S, pv);
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc[0][j] = __fma_rn(pv[j], y[j], acc[0][j]);
+    }
+    if (i + 2 < n_tiles && t <= nrows(tile2)) ro_s[s2 * ro_stride + t] = ro_next;
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (t + u * T < cnt1) col_s[s1 * col_stride + t + u * T] = col_next[u];
+    __syncthreads();  // stage s0 consumed; metadata of tiles i+1, i+2 visible
+    if (t == 0 && i + kStages < n_tiles) issue(i + kStages, kn0, kn1);
+    const bool chunk_end = ((i + 1) % ct == 0) || (tile == tiles - 1);
+    if (chunk_end) {
+      const int chunk = (int)(tile / ct);
+      if (reduce_lanes<1, V>(acc, red, st.part, st.ticket, g, chunk, geo)) {
+        if (t < geo.L) {
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            const size_t l = (size_t)g * S + V * t + j;
+            const double pap = red[j * geo.T + t];
+            const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
+            st.frozen[l] = fr;
+            st.alpha[l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
+          }
+        }
+        if (t == 0) st.it[g] += 1;
+      }
+      acc[0][0] = acc[0][1] = 0.0;
+    }
+    tile = tile1;
+    tile1 = tile2;
+  }
+}
+
 // ensemble_iterations = max over lanes (ensemble.py:277)
 __global__ void pcg_finalize_kernel(PcgState st, int G, int S, int* ens_iters) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -665,12 +822,32 @@ static void launch_spmv_tma(const Geo& gl, int G, cudaStream_t s, long long N, l
   pcg_spmv_tma_kernel<ML><<<dim3(gl.B, G), gl.T, smem, s>>>(N, nnz, gl, st, ro, ci, vals, p, ap);
 }
 
-bool spmv_tma_enabled() {
-  static const int on = [] {
+template <int ML>
+static void launch_spmv_tma_meta(const Geo& gl, int G, cudaStream_t s, long long N, long long nnz,
+                                 const PcgState& st, const int* ro, const int* ci,
+                                 const double* vals, const double* p, double* ap) {
+  const size_t smem = (size_t)2 * gl.T * sizeof(double) +
+                      (size_t)kStages * gl.R * ML * gl.S * sizeof(double) +
+                      (size_t)kStages * (((gl.R + 2) & ~1) + gl.R * ML) * sizeof(int) +
+                      kStages * 8;
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaFuncSetAttribute(pcg_spmv_tma_meta_kernel<ML>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = smem;
+  }
+  pcg_spmv_tma_meta_kernel<ML><<<dim3(gl.B, G), gl.T, smem, s>>>(N, nnz, gl, st, ro, ci, vals, p,
+                                                                 ap);
+}
+
+// UQG_SPMV_TMA: 0 = register-gather kernel, 1 = TMA-staged values,
+// 2 = TMA-staged values + shared-memory tile metadata (default)
+int spmv_tma_mode() {
+  static const int mode = [] {
     const char* e = getenv("UQG_SPMV_TMA");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 2;
   }();
-  return on != 0;
+  return mode;
 }
 
 void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long long nnz,
@@ -678,11 +855,19 @@ void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long lo
                      const double* p, double* ap) {
   const Geo& gl = geo;  // B preset by the caller (blocks per ACTIVE group)
   const bool aligned = (reinterpret_cast<uintptr_t>(vals) & 15) == 0;
-  if (spmv_tma_enabled() && gl.V == 2 && aligned && gl.maxrow >= 1 && gl.maxrow <= 8) {
-    if (gl.maxrow <= 5)
+  const int mode = spmv_tma_mode();
+  if (mode && gl.V == 2 && aligned && gl.maxrow >= 1 && gl.maxrow <= 8) {
+    // the metadata variant needs R + 1 <= T and R * ML <= 2T (S >= 8)
+    if (mode == 2 && gl.Lp >= 4) {
+      if (gl.maxrow <= 5)
+        launch_spmv_tma_meta<5>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap);
+      else
+        launch_spmv_tma_meta<8>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap);
+    } else if (gl.maxrow <= 5) {
       launch_spmv_tma<5>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap);
-    else
+    } else {
       launch_spmv_tma<8>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap);
+    }
     return;
   }
   UQG_DISPATCH_VML(gl, pcg_spmv_kernel, dim3(gl.B, G), red_bytes(gl, 1), s, N, nnz, gl, st, ro,
