@@ -840,12 +840,14 @@ static void launch_spmv_tma_meta(const Geo& gl, int G, cudaStream_t s, long long
                                                                  ap);
 }
 
-// UQG_SPMV_TMA: 0 = register-gather kernel, 1 = TMA-staged values,
-// 2 = TMA-staged values + shared-memory tile metadata (default)
+// UQG_SPMV_TMA: 0 = register-gather kernel, 1 = TMA-staged values (default;
+// fastest on B200: C2 4.55 TB/s), 2 = TMA-staged values + shared-memory tile
+// metadata (4.25 TB/s: the extra per-tile staging work outweighs the shorter
+// dependent-load chain).  All three give identical bits.
 int spmv_tma_mode() {
   static const int mode = [] {
     const char* e = getenv("UQG_SPMV_TMA");
-    return e ? atoi(e) : 2;
+    return e ? atoi(e) : 1;
   }();
   return mode;
 }

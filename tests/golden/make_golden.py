@@ -251,6 +251,48 @@ def reference_study_3d(name):
     return {"preset": name, "stop": stop, "levels": levels}
 
 
+def rounding_envelope(name, doc):
+    """The reference's own iteration-count reproducibility on its preset.
+
+    Lock-step over the golden study's plans, the reference's ensemble_pcg is
+    re-run (a) with per-lane dots summed in a different order (numpy pairwise
+    ``sum(x*y)`` instead of BLAS ``ddot``) and (b) with the assembled values
+    jittered by one ulp; the largest |iteration change| per level is the
+    envelope within which two correct FP64 implementations can disagree.
+    """
+    from uqgroup import fem3d as rfem
+    from uqgroup import harness as H
+
+    cfg = H.preset_config(name)
+    prob = H._PdeProblem(cfg)
+    rng = np.random.default_rng(1)
+    orig_dot = ref_ens.lane_dot
+    env = []
+    for lv in doc["levels"]:
+        coords = {s: np.array(c) for s, c in zip(lv["ids"], lv["coords"])}
+        gold = dict(zip(lv["ids"], lv["iterations"]))
+        worst = 0
+        for grp in lv["ensembles"]:
+            ys = np.array([coords[s] for s in grp])
+            sysm = rfem.assemble(prob.mesh, prob.field, ys, prob.mode_vals)
+            ref_ens.lane_dot = lambda x, y: np.array([np.sum(x[s] * y[s]) for s in range(x.shape[0])])
+            try:
+                a = ref_ens.ensemble_pcg(sysm.matrix, sysm.rhs, tol=cfg.solver.tol,
+                                         maxit=cfg.solver.maxit).iterations_per_lane
+            finally:
+                ref_ens.lane_dot = orig_dot
+            v = sysm.matrix.values
+            v = np.where(rng.random(v.shape) < 0.5, np.nextafter(v, np.inf), np.nextafter(v, -np.inf))
+            pm = ref_ens.EnsembleCsrMatrix(sysm.matrix.row_offsets, sysm.matrix.col_indices, v)
+            b = ref_ens.ensemble_pcg(pm, sysm.rhs, tol=cfg.solver.tol,
+                                     maxit=cfg.solver.maxit).iterations_per_lane
+            for s, sid in enumerate(grp):
+                worst = max(worst, abs(int(a[s]) - gold[sid]), abs(int(b[s]) - gold[sid]))
+        env.append(worst)
+        print(f"  {name} level {lv['level']}: reference rounding envelope +-{worst}", flush=True)
+    return env
+
+
 def c2_group():
     cfg = CONFIGS["C2"]
     fld = field2d.KL2D.select(**cfg.field_kwargs())
@@ -302,5 +344,6 @@ if __name__ == "__main__":
     for preset in ("pde_test1", "pde_test2"):
         if preset in which:
             doc = reference_study_3d(preset)
+            doc["envelope"] = rounding_envelope(preset, doc)
             (HERE / f"{preset}_study.json").write_text(json.dumps(doc))
     print("golden fixtures written to", HERE)

@@ -425,9 +425,10 @@ def test_tma_staged_spmv_bitwise_equals_register_path(tmp_path, lanes):
     from pathlib import Path
     root = str(Path(__file__).resolve().parents[1])
     out = {}
-    for tma in ("1", "0"):
+    for tma in ("1", "2", "0"):
         env = dict(os.environ, UQG_SPMV_TMA=tma, UQG_LANES_PER_THREAD=lanes)
         dst = tmp_path / f"r{tma}.npy"
         subprocess.run([sys.executable, "-c", _TMA_SCRIPT, root, str(dst)], env=env, check=True)
         out[tma] = np.load(dst)
     assert np.array_equal(out["1"], out["0"])
+    assert np.array_equal(out["2"], out["0"])
