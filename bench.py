@@ -258,9 +258,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # Test hook (not used by the driver): UQG_BENCH_SHARE_GPU=1 puts every rank on
+    # cuda:0 with gloo, to exercise the N>1 code path on a 1-GPU box (no rank's
+    # kernels ever wait on another rank's, so sharing a GPU is safe).
+    share = os.environ.get("UQG_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_1705_02003_b200 as uq
     from paper_1705_02003_b200 import _lib
@@ -277,6 +286,7 @@ def main():
     coords = reflect(coords, rank)
     n, S = len(ids), cfg.ensemble_size
     dev = _lib.device()
+    coll_dev = torch.device("cpu") if share else dev  # gloo test hook collects on the host
     d_coords = torch.from_numpy(np.ascontiguousarray(coords)).to(dev)
     d_keys = None if keys is None else torch.from_numpy(np.ascontiguousarray(keys)).to(dev)
     lib, ctx = _lib.load(), _lib.ctx()
@@ -292,8 +302,8 @@ def main():
             # the study's one collective: per-slot iterations + QoIs of every rank's
             # groups allgathered (NCCL) for the surrogate refit (harness.py:658-660)
             groups, pad, it, cv, en, q = out
-            mine = torch.cat([it.double(), q])
-            allv = torch.empty(world * mine.numel(), dtype=mine.dtype, device=dev)
+            mine = torch.cat([it.double(), q]).to(coll_dev)
+            allv = torch.empty(world * mine.numel(), dtype=mine.dtype, device=coll_dev)
             dist.all_gather_into_tensor(allv, mine)
         return out
 
@@ -323,7 +333,7 @@ def main():
                 torch.cuda.synchronize()
                 t = e0.elapsed_time(e1)
                 if world > 1:
-                    tt = torch.tensor([t], device=dev)
+                    tt = torch.tensor([t], device=coll_dev)
                     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
                     t = float(tt.item())
                 times.append(t)
@@ -355,7 +365,7 @@ def main():
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if world > 1:
-            tt = torch.tensor([dt], device=dev)
+            tt = torch.tensor([dt], device=coll_dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             dt = float(tt.item())
         e2e_t.append(dt)

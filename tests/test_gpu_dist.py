@@ -1,0 +1,54 @@
+"""Multi-rank path on the GPU box: the C1 study with each level's groups sharded
+over 2 ranks (one allgather per level) reproduces the single-rank reference
+golden; and `bench.py` runs under torchrun with N=2.  Both ranks share cuda:0
+with gloo (UQG_BENCH_SHARE_GPU=1) because the box has one GPU; no rank's
+kernels wait on another's, so this is safe."""
+
+import json
+import os
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return str(s.getsockname()[1])
+
+
+def _torchrun(args, env_extra, timeout=900):
+    env = dict(os.environ, UQG_BENCH_SHARE_GPU="1", **env_extra)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", _port(), *args]
+    return subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=timeout)
+
+
+def test_sharded_study_matches_single_rank_golden(tmp_path, c1_golden):
+    out = tmp_path / "dist.json"
+    r = _torchrun([str(ROOT / "tools" / "dist_study.py"), "--config", "C1", "--out", str(out)], {})
+    assert r.returncode == 0, r.stderr[-3000:]
+    doc = json.loads(out.read_text())
+    assert doc["world"] == 2
+    assert len(doc["levels"]) == len(c1_golden["levels"])
+    for got, gold in zip(doc["levels"], c1_golden["levels"]):
+        assert got["ids"] == gold["ids"]
+        assert got["ensembles"] == gold["ensembles"]
+        assert max(abs(a - b) for a, b in zip(got["iterations"], gold["iterations"])) <= 1
+        assert max(abs(a - b) / abs(b) for a, b in zip(got["qoi"], gold["qoi"])) <= 1e-8
+
+
+def test_bench_runs_with_two_ranks():
+    r = _torchrun([str(ROOT / "bench.py"), "--gpus", "2", "--config", "C1", "--steps", "2",
+                   "--warmup", "3"], {})
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
