@@ -43,6 +43,17 @@ int uqg_ctx_destroy(uqg_ctx* ctx);
  * ptr NULL detaches.  The buffer must outlive every call that uses it. */
 int uqg_ctx_set_workspace(uqg_ctx* ctx, void* ptr, long long bytes);
 
+/* Structure hint for banded graphs (stencils), used by uqg_pcg on this ctx
+ * until replaced (nbands = 0 clears): the columns of rows [r0, r0+R) lie in
+ * the row bands [r0 + starts[b], r0 + starts[b] + R + extras[b]).  With it the
+ * SpMV stages the p bands, values, columns and row offsets of each tile in
+ * shared memory by bulk async copies (TMA).  A column outside every band is
+ * read from global memory, so the hint never changes results.  graph_padded
+ * != 0 promises >= 4 readable ints after row_offsets[N] and after
+ * col_indices[nnz-1] (required for the staged path).  nbands <= 9. */
+int uqg_ctx_set_band_hint(uqg_ctx* ctx, int nbands, const int* starts_host,
+                          const int* extras_host, int graph_padded);
+
 /* Kernel classes for launch accounting / timing. */
 #define UQG_K_KL 0
 #define UQG_K_ASSEMBLE 1

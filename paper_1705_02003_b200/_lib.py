@@ -28,6 +28,7 @@ SIGNATURES = {
     "uqg_ctx_create": (_c_int, [_c_int, ctypes.POINTER(_p)]),
     "uqg_ctx_destroy": (_c_int, [_p]),
     "uqg_ctx_set_workspace": (_c_int, [_p, _p, _c_ll]),
+    "uqg_ctx_set_band_hint": (_c_int, [_p, _c_int, _p, _p, _c_int]),
     "uqg_ctx_profile": (_c_int, [_p, _c_int]),
     "uqg_ctx_profile_read": (_c_int, [_p, _p, _p, _c_int]),
     "uqg_ctx_launch_count": (_c_ll, [_p]),

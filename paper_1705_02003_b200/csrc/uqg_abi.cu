@@ -37,6 +37,7 @@ struct uqg_ctx {
   std::vector<cudaEvent_t> evpool;  // start/stop pairs
   std::vector<int> pend_kind;
   int pend = 0;
+  BandHint bands{};                 // uqg_ctx_set_band_hint (nb = 0: none)
 };
 
 namespace {
@@ -204,6 +205,22 @@ int uqg_ctx_set_workspace(uqg_ctx* ctx, void* ptr, long long bytes) {
   UQG_REQUIRE(ctx && bytes >= 0, "uqg_ctx_set_workspace: bad argument");
   ctx->ext = ptr;
   ctx->ext_bytes = ptr ? (size_t)bytes : 0;
+  return UQG_OK;
+}
+
+int uqg_ctx_set_band_hint(uqg_ctx* ctx, int nbands, const int* starts_host,
+                          const int* extras_host, int graph_padded) {
+  UQG_REQUIRE(ctx && nbands >= 0 && nbands <= kMaxBands, "uqg_ctx_set_band_hint: bad argument");
+  UQG_REQUIRE(nbands == 0 || (starts_host && extras_host), "uqg_ctx_set_band_hint: NULL bands");
+  BandHint h{};
+  h.nb = nbands;
+  for (int b = 0; b < nbands; ++b) {
+    UQG_REQUIRE(extras_host[b] >= 0 && extras_host[b] <= 64, "band extra rows out of range");
+    h.start[b] = starts_host[b];
+    h.extra[b] = extras_host[b];
+  }
+  h.padded = graph_padded != 0;
+  ctx->bands = h;
   return UQG_OK;
 }
 
@@ -461,7 +478,8 @@ int uqg_pcg(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const i
     const Geo gact = with_groups(geo, std::max(1, G - ctx->pinned[0]));
     for (int k = 0; k < chunk; ++k) {
       UQG_LAUNCH(UQG_K_PCG_SPMV, s,
-                 launch_pcg_spmv(gact, G, s, N, nnz, st, row_offsets, col_indices, vals, p, ap));
+                 launch_pcg_spmv(gact, G, s, N, nnz, st, row_offsets, col_indices, vals, p, ap,
+                                 ctx->bands.nb ? &ctx->bands : nullptr));
       UQG_LAUNCH(UQG_K_PCG_UPDATE, s, launch_pcg_update(gact, G, s, N, st, dinv, maxit, r, ap));
       UQG_LAUNCH(UQG_K_PCG_DIR, s, launch_pcg_dir(gact, G, s, N, st, dinv, r, x, p));
     }

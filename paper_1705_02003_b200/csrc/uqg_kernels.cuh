@@ -10,6 +10,21 @@ constexpr int kRunning = 0;
 constexpr int kFinishing = 1;  // terminated; pcg_dir still owes the last x update
 constexpr int kDone = 2;
 
+// Band hint for banded graphs (stencils): the columns of tile rows [r0, r0+R)
+// lie in nb row bands [r0 + start[b], r0 + start[b] + R + extra[b]).  With a
+// hint, the PCG SpMV stages those p bands (and the tile's values, columns and
+// row offsets) in shared memory by bulk async copies; a column outside every
+// band falls back to a global load, so any hint gives identical results.
+// padded != 0 promises >= 4 ints of readable slack after row_offsets[N] and
+// col_indices[nnz-1] (bulk copies move 16-byte aligned spans).
+constexpr int kMaxBands = 9;
+struct BandHint {
+  int nb;
+  int start[kMaxBands];
+  int extra[kMaxBands];
+  int padded;
+};
+
 // Per-lane / per-group solver state living in device memory (ctx scratch), so
 // the whole PCG loop - alpha, beta, freezing, convergence, termination - is
 // decided on the device.  Lane index l = g*S + s.
@@ -69,7 +84,7 @@ void launch_pcg_init(const Geo& geo, int G, cudaStream_t s, long long N, const P
                      int maxit, double* x, double* r, double* p);
 void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long long nnz,
                      const PcgState& st, const int* ro, const int* ci, const double* vals,
-                     const double* p, double* ap);
+                     const double* p, double* ap, const BandHint* bands);
 void launch_pcg_update(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,
                        const double* dinv, int maxit, double* r, const double* ap);
 void launch_pcg_dir(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,

@@ -752,6 +752,185 @@ __global__ void __launch_bounds__(256, 3) pcg_spmv_tma_meta_kernel(
   }
 }
 
+// Fully staged variant for banded graphs (BandHint): per tile, one elected
+// thread bulk-copies the tile's values, its column indices and row offsets
+// (16-byte aligned spans of the padded graph) and the nb p bands the tile's
+// rows reference; consumers then work from shared memory only (a column that
+// misses every band is read from global memory).  Same arithmetic and order
+// as pcg_spmv_kernel: identical bits.
+struct BandLayout {
+  int vals_d, band_d, col_i, ro_i, stage_d;
+  int rows[kMaxBands];
+  int off_d[kMaxBands];
+};
+
+__host__ __device__ inline BandLayout band_layout(const Geo& geo, const BandHint& bh, int ML) {
+  BandLayout L{};
+  const int R = geo.R, S = geo.S;
+  L.vals_d = R * ML * S;
+  int acc = 0;
+#pragma unroll
+  for (int b = 0; b < kMaxBands; ++b) {
+    const bool on = b < bh.nb;
+    L.rows[b] = on ? R + bh.extra[b] : 0;
+    L.off_d[b] = L.vals_d + acc;
+    acc += L.rows[b] * S;
+  }
+  L.band_d = acc;
+  L.col_i = ((R * ML + 8) + 3) & ~3;
+  L.ro_i = ((R + 1 + 8) + 3) & ~3;
+  L.stage_d = L.vals_d + L.band_d + (L.col_i + L.ro_i) / 2;
+  L.stage_d = (L.stage_d + 1) & ~1;  // 16-byte multiple
+  return L;
+}
+
+template <int ML>
+__global__ void __launch_bounds__(256, 2) pcg_spmv_band_kernel(
+    long long N, long long nnz, Geo geo, PcgState st, const int* __restrict__ ro,
+    const int* __restrict__ ci, const double* __restrict__ vals, const double* __restrict__ p,
+    double* __restrict__ ap, BandHint bh) {
+  constexpr int V = 2;
+  extern __shared__ __align__(128) double red[];
+  const int g = blockIdx.y, t = threadIdx.x;
+  if (st.done[g] != kRunning) return;
+  const int S = geo.S, R = geo.R, T = geo.T;
+  const BandLayout L = band_layout(geo, bh, ML);
+  double* stage = red + V * T;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage + kStages * L.stage_d);
+  const double* vg = vals + (size_t)g * nnz * S;
+  const double* pg_all = p + (size_t)g * N * S;
+  const int n_tiles = block_tile_count(geo);
+  const int ct = (int)geo.chunk_tiles;
+  const long long tiles = geo.tiles;
+
+  auto tile_of = [&](int i) -> long long {
+    const int j = i / ct;
+    return ((long long)blockIdx.x + (long long)j * gridDim.x) * ct + (i - j * ct);
+  };
+  auto col_stage = [&](int s) { return reinterpret_cast<int*>(stage + s * L.stage_d + L.vals_d + L.band_d); };
+  auto ro_stage = [&](int s) { return col_stage(s) + L.col_i; };
+
+  auto issue = [&](int i) {  // thread 0 only
+    const long long tile = tile_of(i);
+    const long long r0 = tile * R;
+    const int nr = (int)(N - r0 < R ? N - r0 : R);
+    const int k0 = __ldg(&ro[r0]), k1 = __ldg(&ro[r0 + nr]);
+    const int s = i % kStages;
+    double* sd = stage + s * L.stage_d;
+    const int ka = k0 & ~3, kb = (k1 + 3) & ~3;
+    const long long ra = r0 & ~3LL, rb = (r0 + nr + 1 + 3) & ~3LL;
+    uint32_t total = (uint32_t)(k1 - k0) * S * 8u + (uint32_t)(kb - ka) * 4u + (uint32_t)(rb - ra) * 4u;
+#pragma unroll
+    for (int b = 0; b < kMaxBands; ++b) {
+      if (b < bh.nb) {
+        const long long lo = r0 + bh.start[b], hi = lo + L.rows[b];
+        const long long lc = lo < 0 ? 0 : lo, hc = hi > N ? N : hi;
+        if (hc > lc) total += (uint32_t)(hc - lc) * S * 8u;
+      }
+    }
+    uint64_t* bar = &bars[s];
+    fence_proxy_async();
+    mbar_expect_tx(bar, total);
+    if (k1 > k0) bulk_g2s(sd, vg + (size_t)k0 * S, (uint32_t)(k1 - k0) * S * 8u, bar);
+    if (kb > ka) bulk_g2s(col_stage(s), ci + ka, (uint32_t)(kb - ka) * 4u, bar);
+    bulk_g2s(ro_stage(s), ro + ra, (uint32_t)(rb - ra) * 4u, bar);
+#pragma unroll
+    for (int b = 0; b < kMaxBands; ++b) {
+      if (b < bh.nb) {
+        const long long lo = r0 + bh.start[b], hi = lo + L.rows[b];
+        const long long lc = lo < 0 ? 0 : lo, hc = hi > N ? N : hi;
+        if (hc > lc)
+          bulk_g2s(sd + L.off_d[b] + (lc - lo) * S, pg_all + lc * S, (uint32_t)(hc - lc) * S * 8u,
+                   bar);
+      }
+    }
+  };
+
+  if (t == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    for (int i = 0; i < kStages && i < n_tiles; ++i) issue(i);
+  }
+  __syncthreads();
+
+  const int sl = t % geo.Lp, rr = t / geo.Lp;
+  const size_t base = (size_t)g * N * S + V * sl;
+  const double* pg = p + base;
+  double acc[1][V] = {};
+  for (int i = 0; i < n_tiles; ++i) {
+    const long long tile = tile_of(i);
+    const int s = i % kStages;
+    mbar_wait(&bars[s], (uint32_t)((i / kStages) & 1));
+    const long long r0 = tile * R;
+    if (sl < geo.L && r0 + rr < N) {
+      const long long row = r0 + rr;
+      const double* sd = stage + s * L.stage_d;
+      const int* rs = ro_stage(s) + (r0 - (r0 & ~3LL));
+      const int kt0 = rs[0];
+      const int* cs = col_stage(s) + (kt0 - (kt0 & ~3));
+      const int k0 = rs[rr] - kt0, len = rs[rr + 1] - rs[rr];
+      const double* sv = sd + (size_t)k0 * S + V * sl;
+      double y[V] = {0.0, 0.0};
+      double pv[V] = {0.0, 0.0};
+#pragma unroll
+      for (int e = 0; e < ML; ++e) {
+        if (e < len) {
+          const long long c = cs[k0 + e];
+          const double* src = nullptr;
+#pragma unroll
+          for (int b = kMaxBands - 1; b >= 0; --b) {  // first matching band wins
+            if (b < bh.nb) {
+              const long long d = c - (r0 + bh.start[b]);
+              if (d >= 0 && d < L.rows[b]) src = sd + L.off_d[b] + d * S + V * sl;
+            }
+          }
+          double2 bv;
+          if (src) bv = *reinterpret_cast<const double2*>(src);
+          else bv = __ldg(reinterpret_cast<const double2*>(pg + c * S));
+          const double2 a = *reinterpret_cast<const double2*>(sv + (size_t)e * S);
+          y[0] = __dadd_rn(y[0], __dmul_rn(a.x, bv.x));
+          y[1] = __dadd_rn(y[1], __dmul_rn(a.y, bv.y));
+          if (c == row) {
+            pv[0] = bv.x;
+            pv[1] = bv.y;
+          }
+        }
+      }
+      // p of the row itself (p.Ap); the diagonal entry normally provided it
+      bool have_diag = false;
+      for (int e = 0; e < len && e < ML; ++e) have_diag |= (cs[k0 + e] == row);
+      if (!have_diag) {
+        const double2 t2 = __ldg(reinterpret_cast<const double2*>(pg + row * S));
+        pv[0] = t2.x;
+        pv[1] = t2.y;
+      }
+      stv<V>(ap + base + row * S, y);
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc[0][j] = __fma_rn(pv[j], y[j], acc[0][j]);
+    }
+    __syncthreads();  // stage s consumed
+    if (t == 0 && i + kStages < n_tiles) issue(i + kStages);
+    const bool chunk_end = ((i + 1) % ct == 0) || (tile == tiles - 1);
+    if (chunk_end) {
+      const int chunk = (int)(tile / ct);
+      if (reduce_lanes<1, V>(acc, red, st.part, st.ticket, g, chunk, geo)) {
+        if (t < geo.L) {
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            const size_t l = (size_t)g * S + V * t + j;
+            const double pap = red[j * geo.T + t];
+            const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
+            st.frozen[l] = fr;
+            st.alpha[l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
+          }
+        }
+        if (t == 0) st.it[g] += 1;
+      }
+      acc[0][0] = acc[0][1] = 0.0;
+    }
+  }
+}
+
 // ensemble_iterations = max over lanes (ensemble.py:277)
 __global__ void pcg_finalize_kernel(PcgState st, int G, int S, int* ens_iters) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -852,12 +1031,40 @@ int spmv_tma_mode() {
   return mode;
 }
 
+template <int ML>
+static void launch_spmv_band(const Geo& gl, int G, cudaStream_t s, long long N, long long nnz,
+                             const PcgState& st, const int* ro, const int* ci, const double* vals,
+                             const double* p, double* ap, const BandHint& bh) {
+  const BandLayout L = band_layout(gl, bh, ML);
+  const size_t smem = (size_t)2 * gl.T * sizeof(double) +
+                      (size_t)kStages * L.stage_d * sizeof(double) + kStages * 8;
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaFuncSetAttribute(pcg_spmv_band_kernel<ML>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    configured = smem;
+  }
+  pcg_spmv_band_kernel<ML><<<dim3(gl.B, G), gl.T, smem, s>>>(N, nnz, gl, st, ro, ci, vals, p, ap,
+                                                             bh);
+}
+
 void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long long nnz,
                      const PcgState& st, const int* ro, const int* ci, const double* vals,
-                     const double* p, double* ap) {
+                     const double* p, double* ap, const BandHint* bands) {
   const Geo& gl = geo;  // B preset by the caller (blocks per ACTIVE group)
   const bool aligned = (reinterpret_cast<uintptr_t>(vals) & 15) == 0;
   const int mode = spmv_tma_mode();
+  const bool aligned_all = aligned && (reinterpret_cast<uintptr_t>(p) & 15) == 0 &&
+                           (reinterpret_cast<uintptr_t>(ro) & 15) == 0 &&
+                           (reinterpret_cast<uintptr_t>(ci) & 15) == 0;
+  if (mode && bands && bands->nb > 0 && bands->padded && gl.V == 2 && aligned_all &&
+      gl.maxrow >= 1 && gl.maxrow <= 8) {
+    if (gl.maxrow <= 5)
+      launch_spmv_band<5>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, *bands);
+    else
+      launch_spmv_band<8>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, *bands);
+    return;
+  }
   if (mode && gl.V == 2 && aligned && gl.maxrow >= 1 && gl.maxrow <= 8) {
     // the metadata variant needs R + 1 <= T and R * ML <= 2T (S >= 8)
     if (mode == 2 && gl.Lp >= 4) {

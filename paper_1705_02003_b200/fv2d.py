@@ -60,10 +60,23 @@ class StructuredMesh2D:
         return int(np.argmin(((c - 0.5) ** 2).sum(axis=1)))
 
     def device(self):
-        """(rowptr, col) on the device, uploaded once."""
+        """(rowptr, col) on the device, uploaded once.
+
+        Both arrays carry 4 ints of zeroed slack after their last entry (the
+        staged SpMV bulk-copies 16-byte aligned spans; ``band_hint``)."""
         if self._dev is None:
-            self._dev = (_lib.to_dev(self.row_offsets), _lib.to_dev(self.col_indices))
+            pad = np.zeros(4, dtype=np.int32)
+            ro = _lib.to_dev(np.concatenate([self.row_offsets, pad]))
+            ci = _lib.to_dev(np.concatenate([self.col_indices, pad]))
+            self._dev = (ro[: self.n_dofs + 1], ci[: self.nnz])
         return self._dev
+
+    def band_hint(self):
+        """Row bands holding the columns of a tile of rows [r0, r0+R): the
+        x-neighbours [r0-m, r0-m+R), the row and its y-neighbours
+        [r0-1, r0+R+1), [r0+m, r0+m+R) (m = cells - 1)."""
+        m = self.cells - 1
+        return [-m, -1, m], [0, 2, 0]
 
 
 @dataclass

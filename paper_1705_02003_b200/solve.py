@@ -18,6 +18,8 @@ first-occurrence rule for replica slots (``harness.py:427-430``) and the
 
 from __future__ import annotations
 
+import ctypes
+import os
 from dataclasses import dataclass, field as dc_field
 
 import numpy as np
@@ -63,6 +65,9 @@ class FV2DOperator:
 
     def graph(self):
         return self.mesh.device()
+
+    def band_hint(self):
+        return self.mesh.band_hint()
 
     def coefficients(self, d_samples, lane_ids, G, S, out):
         kl_nodes(self.tables, d_samples, G, S, out=out, lane_ids=lane_ids)
@@ -181,9 +186,22 @@ class EnsembleSolver:
         o.assemble(a, G, S, vals, dinv)
         rowptr, col = o.graph()
         self._workspace(G, S)
-        x, iters, conv, frz, ens, hist = run_pcg(
-            o.n_dofs, o.nnz, S, G, rowptr, col, vals, None, o.rhs_const, dinv, self.tol,
-            self.maxit, record_history, max_row_len=o.max_row_len)
+        # banded-graph hint for the fully staged SpMV (UQG_BAND_HINT=0 disables;
+        # results are identical either way)
+        hint = (o.band_hint() if hasattr(o, "band_hint") and
+                os.environ.get("UQG_BAND_HINT", "1") != "0" else None)
+        if hint:
+            starts, extras = hint
+            _lib.call("uqg_ctx_set_band_hint", _lib.ctx(), len(starts),
+                      (ctypes.c_int * len(starts))(*starts), (ctypes.c_int * len(extras))(*extras),
+                      1)
+        try:
+            x, iters, conv, frz, ens, hist = run_pcg(
+                o.n_dofs, o.nnz, S, G, rowptr, col, vals, None, o.rhs_const, dinv, self.tol,
+                self.maxit, record_history, max_row_len=o.max_row_len)
+        finally:
+            if hint:
+                _lib.call("uqg_ctx_set_band_hint", _lib.ctx(), 0, None, None, 0)
         q = torch.empty((G * S,), dtype=torch.float64, device=_lib.device())
         _lib.call("uqg_lane_dot", _lib.ctx(), o.n_dofs, S, G, _lib.ptr(x), _lib.ptr(x), _lib.ptr(q),
                   _lib.stream())

@@ -425,10 +425,10 @@ def test_tma_staged_spmv_bitwise_equals_register_path(tmp_path, lanes):
     from pathlib import Path
     root = str(Path(__file__).resolve().parents[1])
     out = {}
-    for tma in ("1", "2", "0"):
-        env = dict(os.environ, UQG_SPMV_TMA=tma, UQG_LANES_PER_THREAD=lanes)
-        dst = tmp_path / f"r{tma}.npy"
+    for tma, band in (("1", "1"), ("1", "0"), ("2", "0"), ("0", "0")):
+        env = dict(os.environ, UQG_SPMV_TMA=tma, UQG_BAND_HINT=band, UQG_LANES_PER_THREAD=lanes)
+        dst = tmp_path / f"r{tma}{band}.npy"
         subprocess.run([sys.executable, "-c", _TMA_SCRIPT, root, str(dst)], env=env, check=True)
-        out[tma] = np.load(dst)
-    assert np.array_equal(out["1"], out["0"])
-    assert np.array_equal(out["2"], out["0"])
+        out[tma + band] = np.load(dst)
+    for k in ("11", "10", "20"):  # band-staged, value-staged, metadata-staged vs register path
+        assert np.array_equal(out[k], out["00"]), k
