@@ -135,6 +135,22 @@ struct Carver {
   }
 };
 
+struct PersistBufs {
+  double* partA;
+  unsigned* bar;  // [G] counts, [G] generations, [1] abort flag
+};
+thread_local PersistBufs g_persist;
+
+// UQG_PCG_PERSISTENT: 1 = always (when co-resident), 0 = never, unset = auto
+// (small batches: the launch-per-phase loop would be latency-bound).
+int persistent_mode() {
+  static const int m = [] {
+    const char* e = getenv("UQG_PCG_PERSISTENT");
+    return e ? atoi(e) : -1;
+  }();
+  return m;
+}
+
 size_t pcg_layout(Carver& c, long long N, const Geo& geo, int G, PcgState* st, double** r,
                   double** p, double** ap) {
   const size_t vec = (size_t)G * N * geo.S;
@@ -155,10 +171,17 @@ size_t pcg_layout(Carver& c, long long N, const Geo& geo, int G, PcgState* st, d
   s.status = c.take<int>(G);
   s.ndone = c.take<int>(1);
   s.overflow = c.take<int>(1);
+  // persistent-path extras: phase-A partials, group barriers, abort flag
+  double* partA = c.take<double>((size_t)G * geo.chunks * geo.S);
+  unsigned* bar = c.take<unsigned>(2 * (size_t)G + 1);
   if (st) *st = s;
   if (r) *r = rr;
   if (p) *p = pp;
   if (ap) *ap = aa;
+  if (st) {
+    g_persist.partA = partA;
+    g_persist.bar = bar;
+  }
   return c.off + 256;
 }
 
@@ -456,14 +479,42 @@ int uqg_pcg(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const i
   UQG_TRY_CUDA(cudaMemsetAsync(st.ndone, 0, sizeof(int), s));
   UQG_TRY_CUDA(cudaMemsetAsync(st.overflow, 0, sizeof(int), s));
 
-  UQG_LAUNCH(UQG_K_PCG_INIT, s,
-             launch_pcg_init(geo, G, s, N, st, rhs, rhs_const, dinv, tol, maxit, x, r, p));
-  // Host polls the device done-counter between chunks of iterations.  Groups
-  // that have terminated turn every later launch into a no-op, so the extra
-  // launches of the last chunk cannot change any result.
+  // Small batches: one cooperative launch runs the whole solve (uqg_persistent.cu).
+  const int pmode = persistent_mode();
+  const double iter_bytes = 8.0 * S * ((double)nnz + 12.0 * N) * G;
+  const bool want_persist = pmode == 1 || (pmode < 0 && iter_bytes < 512e6);
+  const int pblocks = want_persist ? persistent_blocks(geo, G) : 0;
+  if (pblocks > 0) {
+    PersistBufs pb = g_persist;
+    UQG_TRY_CUDA(cudaMemsetAsync(pb.bar, 0, (2 * (size_t)G + 1) * sizeof(unsigned), s));
+    cudaError_t le = cudaSuccess;
+    UQG_LAUNCH(UQG_K_PCG_SPMV, s, {
+      le = launch_pcg_persistent(geo, G, pblocks, s, N, nnz, st, row_offsets, col_indices, vals,
+                                 rhs, rhs_const, dinv, tol, maxit, x, r, p, ap, pb.partA, st.part,
+                                 pb.bar, pb.bar + G, reinterpret_cast<int*>(pb.bar + 2 * G));
+    });
+    if (le != cudaSuccess) {
+      cudaGetLastError();
+      set_error(std::string("cooperative launch: ") + cudaGetErrorString(le));
+      return UQG_ECUDA;
+    }
+    UQG_TRY_CUDA(cudaMemcpyAsync(ctx->pinned + 2, pb.bar + 2 * G, sizeof(int),
+                                 cudaMemcpyDeviceToHost, s));
+    UQG_TRY_CUDA(cudaStreamSynchronize(s));
+    if (ctx->pinned[2]) {
+      set_error("uqg_pcg: persistent solve aborted (group barrier timeout)");
+      return UQG_ECUDA;
+    }
+  }
+  // Otherwise: host polls the device done-counter between chunks of
+  // iterations.  Groups that have terminated turn every later launch into a
+  // no-op, so the extra launches of the last chunk cannot change any result.
+  if (pblocks == 0)
+    UQG_LAUNCH(UQG_K_PCG_INIT, s,
+               launch_pcg_init(geo, G, s, N, st, rhs, rhs_const, dinv, tol, maxit, x, r, p));
   long long launched = 0;
   int chunk = 2;
-  for (;;) {
+  for (; pblocks == 0;) {
     UQG_TRY_CUDA(cudaMemcpyAsync(ctx->pinned, st.ndone, sizeof(int), cudaMemcpyDeviceToHost, s));
     UQG_TRY_CUDA(cudaEventRecord(ctx->ev, s));
     UQG_TRY_CUDA(cudaEventSynchronize(ctx->ev));

@@ -1,0 +1,52 @@
+"""The persistent cooperative PCG (one launch per solve, group barriers) is
+bit-identical to the launch-per-phase loop, for solves through the drop-in
+API (generic CSR, identity/Jacobi, history) and the level-batched solver."""
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+_SCRIPT = r"""
+import sys, numpy as np, scipy.sparse as sp
+sys.path.insert(0, sys.argv[1])
+import paper_1705_02003_b200 as uq
+out = []
+cfg = uq.CONFIGS["C1"]
+s = cfg.make_solver()
+ys = np.random.default_rng(3).uniform(-1, 1, (5, cfg.ensemble_size, cfg.n_modes))
+r = s.solve_groups(ys)
+out += [r.iterations.ravel().astype(float), r.qoi.ravel()]
+rng = np.random.default_rng(7)
+n = 60
+mask = np.triu(rng.random((n, n)) < 0.1, 1)
+base = np.where(mask, rng.uniform(-1, 1, (n, n)), 0.0); base = base + base.T
+lanes = []
+for _ in range(3):
+    v = base * rng.uniform(0.2, 1.0)
+    np.fill_diagonal(v, np.abs(v).sum(axis=1) + 1.0)
+    lanes.append(sp.csr_matrix(v))
+ens = uq.EnsembleCsrMatrix.from_scipy_lanes(lanes)
+res = uq.ensemble_pcg(ens, rng.standard_normal((3, n)), tol=1e-11, maxit=500, record_history=True)
+out += [res.solution.ravel(), res.iterations_per_lane.astype(float),
+        np.concatenate(res.residual_history)]
+np.save(sys.argv[2], np.concatenate(out))
+"""
+
+
+def test_persistent_bitwise_equals_launch_loop(tmp_path):
+    got = {}
+    for mode in ("1", "0"):
+        env = dict(os.environ, UQG_PCG_PERSISTENT=mode)
+        dst = tmp_path / f"p{mode}.npy"
+        subprocess.run([sys.executable, "-c", _SCRIPT, str(ROOT), str(dst)], env=env, check=True,
+                       timeout=600)
+        got[mode] = np.load(dst)
+    assert got["1"].shape == got["0"].shape
+    assert np.array_equal(got["1"], got["0"])
