@@ -32,6 +32,9 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 WORKLOADS = ROOT / "bench_workloads"
+# BASELINE.json's metric, verbatim (value = ensemble sample-solves/s; the
+# SpMV/PCG HBM GB/s vs peak part is reported in `roofline` / `pcg_loop`)
+METRIC = "ensemble sample-solves/s at 1/2/4/8 B200; SpMV+PCG HBM GB/s vs peak"
 
 
 def parse():
@@ -225,7 +228,7 @@ def run_reference(args, cfg):
     value = done / total
     S = cfg.ensemble_size
     line = {
-        "impl": "reference", "metric": "ensemble sample-solves/s", "value": value,
+        "impl": "reference", "metric": METRIC, "value": value,
         "unit": "sample-solves/s", "n_gpus": args.gpus, "steps": steps, "warmup": 0,
         "ms_per_step": 1e3 * total / steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -386,6 +389,10 @@ def main():
         peaks = json.loads(pk.read_text())
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    traffic = {}
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(cfg.name, {})
     spmv_ms = ms[3]
     spmv_gbs = group_iters * bm["spmv"] / (spmv_ms / 1e3) / 1e9 if spmv_ms else None
     loop_ms = ms[3] + ms[4] + ms[5]
@@ -395,7 +402,7 @@ def main():
         ["kl", "assemble", "pcg_init", "pcg_spmv", "pcg_update", "pcg_dir", "dot_qoi", "group",
          "spmv", "other"]) if cnt[k]}
     line = {
-        "metric": "ensemble sample-solves/s",
+        "metric": METRIC,
         "value": value,
         "unit": "sample-solves/s",
         "n_gpus": world,
@@ -420,7 +427,10 @@ def main():
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "roofline": {"bound": "hbm", "kernel": "pcg_spmv_kernel",
                      "achieved": spmv_gbs, "peak": peak, "unit": "GB/s",
-                     "frac": (spmv_gbs / peak) if spmv_gbs else None, "traffic": None,
+                     "frac": (spmv_gbs / peak) if spmv_gbs else None,
+                     "traffic": traffic.get("dram_bytes_per_launch"),
+                     "traffic_algorithmic_same_launch": traffic.get("algorithmic_bytes_per_launch"),
+                     "traffic_source": traffic.get("source"),
                      "peak_source": peak_src,
                      "bytes_per_group_launch": bm["spmv"],
                      "group_launches": group_iters},
