@@ -480,16 +480,29 @@ int uqg_pcg(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const i
   UQG_TRY_CUDA(cudaMemsetAsync(st.overflow, 0, sizeof(int), s));
 
   // Small batches: one cooperative launch runs the whole solve (uqg_persistent.cu).
+  // UQG_PCG_PERSISTENT: 2 = cluster-barrier kernel, 1 = cooperative kernel,
+  // 0 = launch loop; auto = cluster kernel for small batches (< 512 MB per
+  // iteration), launch loop otherwise.
   const int pmode = persistent_mode();
   const double iter_bytes = 8.0 * S * ((double)nnz + 12.0 * N) * G;
-  const bool want_persist = pmode == 1 || (pmode < 0 && iter_bytes < 512e6);
-  const int pblocks = want_persist ? persistent_blocks(geo, G) : 0;
+  const bool small = iter_bytes < 512e6;
+  bool use_cluster = false;
+  int pblocks = 0;
+  if (pmode == 2 || (pmode < 0 && small)) {
+    const int cs = persistent_cluster_size(geo);
+    if (cs >= 2) {
+      use_cluster = true;
+      pblocks = cs;
+    }
+  }
+  if (!use_cluster && (pmode == 1 || (pmode < 0 && small))) pblocks = persistent_blocks(geo, G);
   if (pblocks > 0) {
     PersistBufs pb = g_persist;
     UQG_TRY_CUDA(cudaMemsetAsync(pb.bar, 0, (2 * (size_t)G + 1) * sizeof(unsigned), s));
     cudaError_t le = cudaSuccess;
     UQG_LAUNCH(UQG_K_PCG_SPMV, s, {
-      le = launch_pcg_persistent(geo, G, pblocks, s, N, nnz, st, row_offsets, col_indices, vals,
+      le = launch_pcg_persistent(geo, G, pblocks, use_cluster, s, N, nnz, st, row_offsets,
+                                 col_indices, vals,
                                  rhs, rhs_const, dinv, tol, maxit, x, r, p, ap, pb.partA, st.part,
                                  pb.bar, pb.bar + G, reinterpret_cast<int*>(pb.bar + 2 * G));
     });

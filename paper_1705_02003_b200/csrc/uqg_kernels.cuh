@@ -93,11 +93,13 @@ void launch_pcg_finalize(int G, int S, cudaStream_t s, const PcgState& st, int* 
 
 // uqg_persistent.cu: whole-solve cooperative kernel for small batches
 int persistent_blocks(const Geo& geo, int G);
-cudaError_t launch_pcg_persistent(const Geo& geo, int G, int blocks, cudaStream_t s, long long N,
-                                  long long nnz, const PcgState& st, const int* ro, const int* ci,
-                                  const double* vals, const double* rhs, double rhs_const,
-                                  const double* dinv, double tol, int maxit, double* x, double* r,
-                                  double* p, double* ap, double* partA, double* partB,
-                                  unsigned* bar_count, unsigned* bar_gen, int* abort_flag);
+int persistent_cluster_size(const Geo& geo);
+cudaError_t launch_pcg_persistent(const Geo& geo, int G, int blocks, bool cluster, cudaStream_t s,
+                                  long long N, long long nnz, const PcgState& st, const int* ro,
+                                  const int* ci, const double* vals, const double* rhs,
+                                  double rhs_const, const double* dinv, double tol, int maxit,
+                                  double* x, double* r, double* p, double* ap, double* partA,
+                                  double* partB, unsigned* bar_count, unsigned* bar_gen,
+                                  int* abort_flag);
 
 }  // namespace uqg

@@ -72,6 +72,22 @@ __device__ bool group_sync(unsigned* count, unsigned* gen, unsigned nb, int* abo
   return s_abort == 0;
 }
 
+// CL: the group is one thread-block cluster and the barrier is the hardware
+// cluster barrier (release/acquire at cluster scope; no spinning, no atomics).
+template <bool CL>
+__device__ __forceinline__ bool sync_group(unsigned* count, unsigned* gen, unsigned nb,
+                                           int* abort_flag) {
+  if constexpr (CL) {
+    __threadfence();
+    asm volatile(
+        "barrier.cluster.arrive.release.aligned;\n\t"
+        "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    return true;
+  } else {
+    return group_sync(count, gen, nb, abort_flag);
+  }
+}
+
 // Per-chunk tree reduction (first half of reduce_lanes): writes the chunk's
 // per-lane partials, no ticket.
 template <int NV, int V>
@@ -133,7 +149,7 @@ struct LaneSmem {
   unsigned char *conv, *frozen;
 };
 
-template <int V>
+template <int V, bool CL>
 __global__ void __launch_bounds__(256) pcg_persistent_kernel(
     long long N, long long nnz, Geo geo, PcgState st, const int* __restrict__ ro,
     const int* __restrict__ ci, const double* __restrict__ vals, const double* __restrict__ rhs,
@@ -199,7 +215,7 @@ __global__ void __launch_bounds__(256) pcg_persistent_kernel(
     }
     chunk_partial<2, V>(acc, red, partB, g, chunk, geo);
   }
-  if (!group_sync(cnt, gen, nb, abort_flag)) return;
+  if (!sync_group<CL>(cnt, gen, nb, abort_flag)) return;
   final_partials<2, V>(red, partB, g, geo);
   if (t == 0) s_flags[0] = 1;
   __syncthreads();
@@ -254,7 +270,7 @@ __global__ void __launch_bounds__(256) pcg_persistent_kernel(
       }
       chunk_partial<1, V>(acc, red, partA, g, chunk, geo);
     }
-    if (!group_sync(cnt, gen, nb, abort_flag)) return;
+    if (!sync_group<CL>(cnt, gen, nb, abort_flag)) return;
     final_partials<1, V>(red, partA, g, geo);
     if (t < L) {
 #pragma unroll
@@ -304,7 +320,7 @@ __global__ void __launch_bounds__(256) pcg_persistent_kernel(
       }
       chunk_partial<2, V>(acc, red, partB, g, chunk, geo);
     }
-    if (!group_sync(cnt, gen, nb, abort_flag)) return;
+    if (!sync_group<CL>(cnt, gen, nb, abort_flag)) return;
     final_partials<2, V>(red, partB, g, geo);
     if (t == 0) {
       s_flags[0] = 1;
@@ -372,7 +388,7 @@ __global__ void __launch_bounds__(256) pcg_persistent_kernel(
         }
       }
     }
-    if (!finish && !group_sync(cnt, gen, nb, abort_flag)) return;
+    if (!finish && !sync_group<CL>(cnt, gen, nb, abort_flag)) return;
   }
   // ---- outputs (block 0 of the group)
   if (blockIdx.x == 0) {
@@ -401,6 +417,43 @@ size_t persistent_smem(const Geo& geo) {
          (size_t)geo.S * (sizeof(int) + 2) + 16;
 }
 
+template <bool CL>
+static const void* persistent_fn(int V) {
+  return V == 2 ? (const void*)pcg_persistent_kernel<2, CL> : (const void*)pcg_persistent_kernel<1, CL>;
+}
+
+// Cluster size (CTAs per group) for the cluster-barrier variant: up to 16
+// (non-portable) and at most the group's chunk count; 0 if not launchable.
+int persistent_cluster_size(const Geo& geo) {
+  static int cached[2] = {-1, -1};
+  const int vi = geo.V == 2;
+  if (cached[vi] < 0) {
+    const void* fn = persistent_fn<true>(geo.V);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(16, 1, 1);
+    cfg.blockDim = dim3(geo.T, 1, 1);
+    cfg.dynamicSmemBytes = 0;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 16;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int cs = 0;
+    if (cudaOccupancyMaxPotentialClusterSize(&cs, fn, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      cs = 8;
+    }
+    cached[vi] = cs;
+  }
+  int c = cached[vi];
+  if (c > 16) c = 16;
+  if (c > geo.chunks) c = geo.chunks;
+  return c;
+}
+
 // Blocks per group for a cooperative launch over G groups, or 0 if the
 // groups cannot all be co-resident.
 int persistent_blocks(const Geo& geo, int G) {
@@ -408,31 +461,43 @@ int persistent_blocks(const Geo& geo, int G) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t smem = persistent_smem(geo);
-  if (geo.V == 2)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_persistent_kernel<2>, geo.T, smem);
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_persistent_kernel<1>, geo.T, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, persistent_fn<false>(geo.V), geo.T, smem);
   const long long cap = (long long)per_sm * sms;
   long long b = cap / (G < 1 ? 1 : G);
   if (b > geo.chunks) b = geo.chunks;
   return b < 1 ? 0 : (int)b;
 }
 
-cudaError_t launch_pcg_persistent(const Geo& geo, int G, int blocks, cudaStream_t s, long long N,
-                                  long long nnz, const PcgState& st, const int* ro, const int* ci,
-                                  const double* vals, const double* rhs, double rhs_const,
-                                  const double* dinv, double tol, int maxit, double* x, double* r,
-                                  double* p, double* ap, double* partA, double* partB,
-                                  unsigned* bar_count, unsigned* bar_gen, int* abort_flag) {
+cudaError_t launch_pcg_persistent(const Geo& geo, int G, int blocks, bool cluster, cudaStream_t s,
+                                  long long N, long long nnz, const PcgState& st, const int* ro,
+                                  const int* ci, const double* vals, const double* rhs,
+                                  double rhs_const, const double* dinv, double tol, int maxit,
+                                  double* x, double* r, double* p, double* ap, double* partA,
+                                  double* partB, unsigned* bar_count, unsigned* bar_gen,
+                                  int* abort_flag) {
   Geo gl = geo;
   gl.B = blocks;
   void* args[] = {&N,   &nnz,       &gl,   (void*)&st, &ro,    &ci,    &vals,
                   &rhs, &rhs_const, &dinv, &tol,       &maxit, &x,     &r,
                   &p,   &ap,        &partA, &partB,    &bar_count, &bar_gen, &abort_flag};
   const size_t smem = persistent_smem(gl);
-  const void* fn = gl.V == 2 ? (const void*)pcg_persistent_kernel<2>
-                             : (const void*)pcg_persistent_kernel<1>;
-  return cudaLaunchCooperativeKernel(fn, dim3(blocks, G), dim3(gl.T), args, smem, s);
+  if (!cluster)
+    return cudaLaunchCooperativeKernel(persistent_fn<false>(gl.V), dim3(blocks, G), dim3(gl.T),
+                                       args, smem, s);
+  // one thread-block cluster per group: hardware cluster barriers
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks, G, 1);
+  cfg.blockDim = dim3(gl.T, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = blocks;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, persistent_fn<true>(gl.V), args);
 }
 
 }  // namespace uqg

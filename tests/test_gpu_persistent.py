@@ -42,7 +42,7 @@ np.save(sys.argv[2], np.concatenate(out))
 
 def test_persistent_bitwise_equals_launch_loop(tmp_path):
     got = {}
-    for mode in ("1", "0"):
+    for mode in ("2", "1", "0"):  # cluster barriers, cooperative barriers, launch loop
         env = dict(os.environ, UQG_PCG_PERSISTENT=mode)
         dst = tmp_path / f"p{mode}.npy"
         subprocess.run([sys.executable, "-c", _SCRIPT, str(ROOT), str(dst)], env=env, check=True,
@@ -50,3 +50,4 @@ def test_persistent_bitwise_equals_launch_loop(tmp_path):
         got[mode] = np.load(dst)
     assert got["1"].shape == got["0"].shape
     assert np.array_equal(got["1"], got["0"])
+    assert np.array_equal(got["2"], got["0"])
