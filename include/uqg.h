@@ -176,6 +176,25 @@ int uqg_pcg(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const i
 /* Device bytes of scratch uqg_pcg needs for (N, S, G) (r, p, Ap, partials). */
 long long uqg_pcg_workspace_bytes(int N, int nnz, int S, int G);
 
+/* Grouping keys on the device.
+ * uqg_surrogate_eval: out[i] = sum_j prod_d max(0, 1 - |y[i][d] - c[j][d]| / w[j][d])
+ * * surplus[j] (HierGrid.eval_many / _basis_block, hier_grid.py:317-359);
+ * points [n][dim] canonical coordinates, centers/widths [n_nodes][dim],
+ * dim <= 64.  On the iteration channel the result is exact (dyadic data), so it
+ * equals the host's BLAS value bit for bit.
+ * uqg_anisotropy_indicator: per sample l, max over P points of
+ * max(a, a_hi) / min(a, a_lo) with a the KL coefficient from the dense mode
+ * table modes [M][P] (anisotropy_indicator, random_field.py:254-270, with
+ * a_hi = max(a_y, a_z), a_lo = min(a_y, a_z)); out [L].  Synchronises;
+ * UQG_EINVAL if a coefficient bound is <= 0. */
+int uqg_surrogate_eval(uqg_ctx* ctx, const double* points, int n, int dim, const double* centers,
+                       const double* widths, const double* surplus, int n_nodes, double* out,
+                       void* stream);
+int uqg_anisotropy_indicator(uqg_ctx* ctx, const double* modes, int P, int M,
+                             const double* sqrt_lam, const double* samples, int L, double a_min,
+                             int a_hat_mode, double a_hat_value, int expansion, double a_hi,
+                             double a_lo, double* out, void* stream);
+
 /* Stable ascending sort of keys[n] (ties keep generation order) and chunking
  * into width-S groups, the short last group padded with its last sample
  * (group_by_key/_chunk, grouping.py:83-95,105-122).  keys NULL = natural

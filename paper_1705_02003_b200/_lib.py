@@ -51,6 +51,10 @@ SIGNATURES = {
                          ctypes.POINTER(_c_int), _p]),
     "uqg_pcg_workspace_bytes": (_c_ll, [_c_int, _c_int, _c_int, _c_int]),
     "uqg_group_sort": (_c_int, [_p, _p, _c_int, _c_int, _p, _p, _p, _p]),
+    "uqg_surrogate_eval": (_c_int, [_p, _p, _c_int, _c_int, _p, _p, _p, _c_int, _p, _p]),
+    "uqg_anisotropy_indicator": (_c_int, [_p, _p, _c_int, _c_int, _p, _p, _c_int, _c_double,
+                                          _c_int, _c_double, _c_int, _c_double, _c_double, _p,
+                                          _p]),
 }
 
 _lock = threading.Lock()

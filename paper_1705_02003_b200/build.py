@@ -10,7 +10,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libuqg.so"
-SOURCES = ["uqg_abi.cu", "uqg_kernels.cu", "uqg_pcg.cu", "uqg_persistent.cu"]
+SOURCES = ["uqg_abi.cu", "uqg_kernels.cu", "uqg_pcg.cu", "uqg_persistent.cu", "uqg_surrogate.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

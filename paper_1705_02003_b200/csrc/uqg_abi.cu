@@ -588,6 +588,40 @@ int uqg_pcg(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const i
   return UQG_OK;
 }
 
+int uqg_surrogate_eval(uqg_ctx* ctx, const double* points, int n, int dim, const double* centers,
+                       const double* widths, const double* surplus, int n_nodes, double* out,
+                       void* stream) {
+  UQG_REQUIRE(ctx && out && (n == 0 || points), "uqg_surrogate_eval: NULL argument");
+  UQG_REQUIRE(n >= 0 && dim >= 1 && dim <= 64 && n_nodes >= 0, "uqg_surrogate_eval: bad sizes");
+  UQG_REQUIRE(n_nodes == 0 || (centers && widths && surplus), "uqg_surrogate_eval: NULL nodes");
+  if (n == 0) return UQG_OK;
+  cudaStream_t s = as_stream(stream);
+  UQG_LAUNCH(UQG_K_GROUP, s,
+             launch_surrogate_eval(s, points, n, dim, centers, widths, surplus, n_nodes, out));
+  return UQG_OK;
+}
+
+int uqg_anisotropy_indicator(uqg_ctx* ctx, const double* modes, int P, int M,
+                             const double* sqrt_lam, const double* samples, int L, double a_min,
+                             int a_hat_mode, double a_hat_value, int expansion, double a_hi,
+                             double a_lo, double* out, void* stream) {
+  UQG_REQUIRE(ctx && modes && sqrt_lam && samples && out, "uqg_anisotropy_indicator: NULL argument");
+  UQG_REQUIRE(P >= 1 && M >= 1 && L >= 1, "uqg_anisotropy_indicator: bad sizes");
+  UQG_REQUIRE(a_hat_mode == 0 || a_hat_mode == 1, "unknown a_hat mode");
+  UQG_REQUIRE(expansion == 0 || expansion == 1, "unknown expansion");
+  int st = 0;
+  int rc = uqg_status_sync(ctx, stream, &st);
+  if (rc) return rc;
+  cudaStream_t s = as_stream(stream);
+  UQG_LAUNCH(UQG_K_KL, s,
+             launch_anisotropy(s, modes, P, M, sqrt_lam, samples, L, a_min, a_hat_mode,
+                               a_hat_value, expansion, a_hi, a_lo, out, ctx->status_dev));
+  rc = uqg_status_sync(ctx, stream, &st);
+  if (rc) return rc;
+  UQG_REQUIRE(!(st & 1), "anisotropy indicator needs strictly positive coefficients");
+  return UQG_OK;
+}
+
 int uqg_group_sort(uqg_ctx* ctx, const double* keys, int n, int S, int* order, int* groups,
                    int* pad, void* stream) {
   UQG_REQUIRE(ctx && groups && pad, "uqg_group_sort: NULL argument");

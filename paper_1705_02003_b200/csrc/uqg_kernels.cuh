@@ -91,6 +91,15 @@ void launch_pcg_dir(const Geo& geo, int G, cudaStream_t s, long long N, const Pc
                     const double* dinv, const double* r, double* x, double* p);
 void launch_pcg_finalize(int G, int S, cudaStream_t s, const PcgState& st, int* ens_iters);
 
+// uqg_surrogate.cu: grouping keys on the device
+void launch_surrogate_eval(cudaStream_t s, const double* points, int n, int dim,
+                           const double* centers, const double* widths, const double* surplus,
+                           int n_nodes, double* out);
+void launch_anisotropy(cudaStream_t s, const double* modes, int P, int M, const double* sqrt_lam,
+                       const double* samples, int L, double a_min, int a_hat_mode,
+                       double a_hat_value, int expansion, double a_hi, double a_lo, double* out,
+                       int* status);
+
 // uqg_persistent.cu: whole-solve cooperative kernel for small batches
 int persistent_blocks(const Geo& geo, int G);
 int persistent_cluster_size(const Geo& geo);

@@ -43,11 +43,13 @@ def sample_set(cfg: StudyConfig) -> np.ndarray:
 
 
 def adaptive_run(cfg: StudyConfig, solver: EnsembleSolver2D | None = None, shard=None,
-                 max_levels: int | None = None):
+                 max_levels: int | None = None, device_keys: bool = False):
     """Run the grouped adaptive loop; returns (records, stop_reason, grid).
 
     ``shard``: optional callable(plan, coords_by_id) -> (iters, qois, notes)
     replacing ``solver.solve_plan`` (multi-GPU sharded solve + allgather).
+    ``device_keys``: evaluate the iteration surrogate on the GPU
+    (``SparseGrid.evaluate_device``; bit-identical keys on this channel).
     """
     if solver is None and shard is None:
         solver = cfg.make_solver()
@@ -69,7 +71,8 @@ def adaptive_run(cfg: StudyConfig, solver: EnsembleSolver2D | None = None, shard
         if level == 1:
             plan = group_natural(ids, S, level, "sur")
         else:
-            predicted = grid.evaluate(ITER, coords, n_nodes=start)
+            predicted = (grid.evaluate_device if device_keys else grid.evaluate)(
+                ITER, coords, n_nodes=start)
             plan = group_by_key(ids, {sid: float(predicted[i]) for i, sid in enumerate(ids)}, S,
                                 level, "sur")
         iters, qois, notes = solve(plan, coords_by_id)

@@ -174,6 +174,36 @@ class KLField:
 KLField2D = KLField  # backwards-compatible name for the 2D field
 
 
+def anisotropy_indicators(field: KLField, samples, probe_points, mode_vals=None) -> np.ndarray:
+    """Worst local anisotropy ratio per sample on the GPU (batched form of
+    ``anisotropy_indicator``, ``random_field.py:254-270``): for each sample
+    row, max over the probe points of max(a, a_hi) / min(a, a_lo) with
+    a_hi = max(a_y, a_z), a_lo = min(a_y, a_z) (a_z only in 3D)."""
+    ys = np.atleast_2d(np.asarray(samples, dtype=float))
+    if ys.shape[1] != field.n_modes:
+        raise FieldError(f"samples must have {field.n_modes} columns, got {ys.shape[1]}")
+    if mode_vals is None:
+        mode_vals = field.mode_values(probe_points)
+    others = (field.a_y, field.a_z) if field.dim == 3 else (field.a_y,)
+    ahat_code, exp_code = field.codes()
+    P = mode_vals.shape[1]
+    d_modes = _lib.to_dev(np.ascontiguousarray(mode_vals, dtype=np.float64))
+    d_y = _lib.to_dev(ys)
+    out = d_y.new_empty((len(ys),))
+    _lib.call("uqg_anisotropy_indicator", _lib.ctx(), _lib.ptr(d_modes), P, field.n_modes,
+              _lib.ptr(field._device_consts()["sqrt_lam"]), _lib.ptr(d_y), len(ys),
+              float(field.a_min), ahat_code, float(field.a_hat_value), exp_code,
+              float(max(others)), float(min(others)), _lib.ptr(out), _lib.stream(),
+              invalid=FieldError)
+    return out.cpu().numpy()
+
+
+def anisotropy_indicator(field: KLField, y, probe_points, mode_vals=None) -> float:
+    """Single-sample drop-in for ``anisotropy_indicator`` (``random_field.py:254``)."""
+    return float(anisotropy_indicators(field, np.asarray(y, dtype=float)[None, :], probe_points,
+                                       mode_vals)[0])
+
+
 def build_field(delta: float, sigma0: float, n_modes: int, a_min: float,
                 a_hat_mode: str = "constant", a_hat_value: float = 1.0, a_y: float = 1.0,
                 nystrom_points: int = 513, sigma0_convention: str = "stddev",

@@ -149,6 +149,29 @@ class SparseGrid:
             raise ValueError(f"channel {channel!r} has unfitted surpluses")
         return self.basis(self.to_canonical(np.asarray(points, dtype=float)), np.arange(n)) @ c
 
+    def evaluate_device(self, channel: str, points, n_nodes: int | None = None) -> np.ndarray:
+        """``evaluate`` on the GPU (``uqg_surrogate_eval``).  On the iteration
+        channel (integer data on the dyadic grid) every term is exact, so the
+        keys equal the host's bit for bit; on other channels they agree to
+        rounding."""
+        from . import _lib
+
+        c = self.surplus[channel]
+        n = len(self.nodes) if n_nodes is None else n_nodes
+        c = c[:n]
+        if not np.all(np.isfinite(c)):
+            raise ValueError(f"channel {channel!r} has unfitted surpluses")
+        pts = np.ascontiguousarray(self.to_canonical(np.asarray(points, dtype=float)))
+        d_pts = _lib.to_dev(pts)
+        out = d_pts.new_empty((len(pts),))
+        if n == 0:
+            return np.zeros(len(pts))
+        _lib.call("uqg_surrogate_eval", _lib.ctx(), _lib.ptr(d_pts), len(pts), self.dim,
+                  _lib.ptr(_lib.to_dev(np.ascontiguousarray(self._ctr[:n]))),
+                  _lib.ptr(_lib.to_dev(np.ascontiguousarray(self._hw[:n]))),
+                  _lib.ptr(_lib.to_dev(np.ascontiguousarray(c))), n, _lib.ptr(out), _lib.stream())
+        return out.cpu().numpy()
+
     def error_indicator(self, channel: str) -> float:
         if not self.frontier:
             return 0.0
