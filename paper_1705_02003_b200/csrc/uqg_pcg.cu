@@ -467,6 +467,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -502,12 +505,14 @@ __global__ void __launch_bounds__(256, 3) pcg_spmv_tma_kernel(long long N, long 
                                                            const int* __restrict__ ci,
                                                            const double* __restrict__ vals,
                                                            const double* __restrict__ p,
-                                                           double* __restrict__ ap) {
+                                                           double* __restrict__ ap,
+                                                           BandHint bh) {
   constexpr int V = 2;
   extern __shared__ __align__(128) double red[];
   const int g = blockIdx.y, t = threadIdx.x;
   if (st.done[g] != kRunning) return;
   const int S = geo.S, R = geo.R;
+  const double* pg_all = p + (size_t)g * N * S;
   const size_t stage_doubles = (size_t)R * ML * S;
   double* stage = red + (size_t)V * geo.T;  // after the reduction scratch
   uint64_t* bars = reinterpret_cast<uint64_t*>(stage + kStages * stage_doubles);
@@ -531,6 +536,17 @@ __global__ void __launch_bounds__(256, 3) pcg_spmv_tma_kernel(long long N, long 
     fence_proxy_async();
     mbar_expect_tx(bar, bytes);
     if (bytes) bulk_g2s(stage + (size_t)(i % kStages) * stage_doubles, vg + (size_t)k0 * S, bytes, bar);
+    // banded graph: pull the p rows this tile will gather into L2 ahead of use
+    // (the +m band is read here for the first time - a DRAM miss otherwise)
+#pragma unroll
+    for (int b = 0; b < kMaxBands; ++b) {
+      if (b < bh.nb) {
+        long long lo = r0 + bh.start[b], hi = lo + R + bh.extra[b];
+        lo = lo < 0 ? 0 : lo;
+        hi = hi > N ? N : hi;
+        if (hi > lo) bulk_prefetch_l2(pg_all + lo * S, (uint32_t)(hi - lo) * S * 8u);
+      }
+    }
   };
   if (t == 0) {
     for (int i = 0; i < kStages && i < n_tiles; ++i) issue(i);
@@ -989,7 +1005,7 @@ void launch_pcg_init(const Geo& geo, int G, cudaStream_t s, long long N, const P
 template <int ML>
 static void launch_spmv_tma(const Geo& gl, int G, cudaStream_t s, long long N, long long nnz,
                             const PcgState& st, const int* ro, const int* ci, const double* vals,
-                            const double* p, double* ap) {
+                            const double* p, double* ap, const BandHint* bands) {
   const size_t smem = (size_t)2 * gl.T * sizeof(double) +
                       (size_t)kStages * gl.R * ML * gl.S * sizeof(double) + kStages * 8;
   static size_t configured = 0;
@@ -998,7 +1014,10 @@ static void launch_spmv_tma(const Geo& gl, int G, cudaStream_t s, long long N, l
                          (int)smem);
     configured = smem;
   }
-  pcg_spmv_tma_kernel<ML><<<dim3(gl.B, G), gl.T, smem, s>>>(N, nnz, gl, st, ro, ci, vals, p, ap);
+  BandHint bh{};  // L2 prefetch of the p bands (p must be 16-byte aligned)
+  if (bands && (reinterpret_cast<uintptr_t>(p) & 15) == 0 && gl.S % 2 == 0) bh = *bands;
+  pcg_spmv_tma_kernel<ML><<<dim3(gl.B, G), gl.T, smem, s>>>(N, nnz, gl, st, ro, ci, vals, p, ap,
+                                                            bh);
 }
 
 template <int ML>
@@ -1020,9 +1039,11 @@ static void launch_spmv_tma_meta(const Geo& gl, int G, cudaStream_t s, long long
 }
 
 // UQG_SPMV_TMA: 0 = register-gather kernel, 1 = TMA-staged values (default;
-// fastest on B200: C2 4.55 TB/s), 2 = TMA-staged values + shared-memory tile
-// metadata (4.25 TB/s: the extra per-tile staging work outweighs the shorter
-// dependent-load chain).  All three give identical bits.
+// fastest on B200: C2 4.55 TB/s; with a band hint it also bulk-prefetches the
+// tile's p bands into L2), 2 = TMA-staged values + shared-memory tile metadata
+// (4.25 TB/s: the extra per-tile staging work outweighs the shorter
+// dependent-load chain), 3 = everything incl. the p bands staged in shared
+// memory (needs a band hint; 1.9 TB/s).  All give identical bits.
 int spmv_tma_mode() {
   static const int mode = [] {
     const char* e = getenv("UQG_SPMV_TMA");
@@ -1057,7 +1078,8 @@ void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long lo
   const bool aligned_all = aligned && (reinterpret_cast<uintptr_t>(p) & 15) == 0 &&
                            (reinterpret_cast<uintptr_t>(ro) & 15) == 0 &&
                            (reinterpret_cast<uintptr_t>(ci) & 15) == 0;
-  if (mode && bands && bands->nb > 0 && bands->padded && gl.V == 2 && aligned_all &&
+  // mode 3: fully band-staged kernel (needs the band hint + padded graph)
+  if (mode == 3 && bands && bands->nb > 0 && bands->padded && gl.V == 2 && aligned_all &&
       gl.maxrow >= 1 && gl.maxrow <= 8) {
     if (gl.maxrow <= 5)
       launch_spmv_band<5>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, *bands);
@@ -1073,9 +1095,9 @@ void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long lo
       else
         launch_spmv_tma_meta<8>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap);
     } else if (gl.maxrow <= 5) {
-      launch_spmv_tma<5>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap);
+      launch_spmv_tma<5>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
     } else {
-      launch_spmv_tma<8>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap);
+      launch_spmv_tma<8>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
     }
     return;
   }

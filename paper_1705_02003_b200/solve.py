@@ -186,11 +186,11 @@ class EnsembleSolver:
         o.assemble(a, G, S, vals, dinv)
         rowptr, col = o.graph()
         self._workspace(G, S)
-        # banded-graph hint for the fully staged SpMV (opt-in, UQG_BAND_HINT=1:
-        # measured slower than the value-staged kernel on C2/C3, 1.9 vs 4.6 TB/s;
-        # results are identical either way)
+        # banded-graph hint: the SpMV bulk-prefetches each tile's p bands into L2
+        # (UQG_SPMV_TMA=3 stages them in shared memory instead); UQG_BAND_HINT=0
+        # disables it.  Results are identical either way.
         hint = (o.band_hint() if hasattr(o, "band_hint") and
-                os.environ.get("UQG_BAND_HINT", "0") == "1" else None)
+                os.environ.get("UQG_BAND_HINT", "1") != "0" else None)
         if hint:
             starts, extras = hint
             _lib.call("uqg_ctx_set_band_hint", _lib.ctx(), len(starts),
