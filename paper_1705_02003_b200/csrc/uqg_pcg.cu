@@ -768,6 +768,204 @@ __global__ void __launch_bounds__(256, 3) pcg_spmv_tma_meta_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialized variant: one producer warp streams the tiles' values into a
+// 4-stage ring (full/empty mbarrier pair per stage) while 8 consumer warps
+// compute; a consumer warp releases a stage with one mbarrier arrive, so there
+// is no CTA-wide barrier per tile and warps drift independently.  Chunk-end
+// reductions synchronise the consumers only (named barrier 1, 256 threads).
+
+constexpr int kWsStages = 4;
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+template <int NS>
+__device__ __forceinline__ void tree_rows_c(double* red, int T, int Lp, int R, int t) {
+  for (int st = R >> 1; st > 0; st >>= 1) {
+    if ((t / Lp) < st) {
+#pragma unroll
+      for (int v = 0; v < NS; ++v) red[v * T + t] += red[v * T + t + st * Lp];
+    }
+    consumer_sync();
+  }
+}
+
+// reduce_lanes with consumer-only barriers (same arithmetic and order)
+template <int NV, int V>
+__device__ bool reduce_lanes_c(const double (&val)[NV][V], double* red, double* part,
+                               unsigned int* ticket, int g, int chunk, const Geo& geo,
+                               int* s_last) {
+  constexpr int NS = NV * V;
+  const int t = threadIdx.x;
+  const int T = geo.T, Lp = geo.Lp, R = geo.R, L = geo.L, S = geo.S, C = geo.chunks;
+  consumer_sync();
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int j = 0; j < V; ++j) red[(v * V + j) * T + t] = val[v][j];
+  consumer_sync();
+  tree_rows_c<NS>(red, T, Lp, R, t);
+  if (t < L) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+      for (int j = 0; j < V; ++j)
+        part[(((size_t)g * C + chunk) * NV + v) * S + V * t + j] = red[(v * V + j) * T + t];
+  }
+  __threadfence();
+  consumer_sync();
+  if (t == 0) {
+    unsigned int tk = atomicAdd(&ticket[g], 1u);
+    *s_last = (tk == (unsigned)(C - 1));
+  }
+  consumer_sync();
+  if (!*s_last) return false;
+  __threadfence();
+  const int sl = t % Lp, jr = t / Lp;
+  double acc[NS];
+#pragma unroll
+  for (int v = 0; v < NS; ++v) acc[v] = 0.0;
+  if (sl < L) {
+#pragma unroll 4
+    for (int cc = jr; cc < C; cc += R) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+          acc[v * V + j] += __ldcg(&part[(((size_t)g * C + cc) * NV + v) * S + V * sl + j]);
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < NS; ++v) red[v * T + t] = acc[v];
+  consumer_sync();
+  tree_rows_c<NS>(red, T, Lp, R, t);
+  if (t == 0) ticket[g] = 0u;
+  return true;
+}
+
+template <int ML>
+__global__ void __launch_bounds__(288, 2) pcg_spmv_ws_kernel(
+    long long N, long long nnz, Geo geo, PcgState st, const int* __restrict__ ro,
+    const int* __restrict__ ci, const double* __restrict__ vals, const double* __restrict__ p,
+    double* __restrict__ ap, BandHint bh) {
+  constexpr int V = 2;
+  extern __shared__ __align__(128) double red[];
+  __shared__ int s_last;
+  const int g = blockIdx.y, t = threadIdx.x;
+  if (st.done[g] != kRunning) return;
+  const int S = geo.S, R = geo.R, T = geo.T;  // T = 256 consumer threads
+  const int stage_doubles = R * ML * S;
+  double* stage = red + V * T;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage + kWsStages * stage_doubles);
+  uint64_t* empty = full + kWsStages;
+  const double* vg = vals + (size_t)g * nnz * S;
+  const double* pg_all = p + (size_t)g * N * S;
+  const int n_tiles = block_tile_count(geo);
+  const int ct = (int)geo.chunk_tiles;
+  auto tile_of = [&](int i) -> long long {
+    const int j = i / ct;
+    return ((long long)blockIdx.x + (long long)j * gridDim.x) * ct + (i - j * ct);
+  };
+  if (t == 0) {
+    for (int s = 0; s < kWsStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (t >= 256) {  // ---- producer warp
+    if (t == 256) {
+      for (int i = 0; i < n_tiles; ++i) {
+        const int s = i % kWsStages;
+        if (i >= kWsStages) mbar_wait(&empty[s], (uint32_t)(((i / kWsStages) - 1) & 1));
+        const long long r0 = tile_of(i) * R;
+        const long long r1 = r0 + R < N ? r0 + R : N;
+        const int k0 = __ldg(&ro[r0]), k1 = __ldg(&ro[r1]);
+        const uint32_t bytes = (uint32_t)(k1 - k0) * (uint32_t)S * 8u;
+        fence_proxy_async();
+        mbar_expect_tx(&full[s], bytes);
+        if (bytes) bulk_g2s(stage + s * stage_doubles, vg + (size_t)k0 * S, bytes, &full[s]);
+#pragma unroll
+        for (int b = 0; b < kMaxBands; ++b) {
+          if (b < bh.nb) {
+            long long lo = r0 + bh.start[b], hi = lo + R + bh.extra[b];
+            lo = lo < 0 ? 0 : lo;
+            hi = hi > N ? N : hi;
+            if (hi > lo) bulk_prefetch_l2(pg_all + lo * S, (uint32_t)(hi - lo) * S * 8u);
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- consumer warps
+  const int sl = t % geo.Lp, rr = t / geo.Lp, lane = t & 31;
+  const size_t base = (size_t)g * N * S + V * sl;
+  const double* pg = p + base;
+  double acc[1][V] = {};
+  for (int i = 0; i < n_tiles; ++i) {
+    const long long tile = tile_of(i);
+    const int s = i % kWsStages;
+    mbar_wait(&full[s], (uint32_t)((i / kWsStages) & 1));
+    if (sl < geo.L) {
+      const long long row = tile * R + rr;
+      if (row < N) {
+        const int kt0 = __ldg(&ro[tile * R]);
+        const int k0 = __ldg(&ro[row]), k1 = __ldg(&ro[row + 1]);
+        const double* sv = stage + s * stage_doubles + (size_t)(k0 - kt0) * S + V * sl;
+        const int len = k1 - k0;
+        int c[ML];
+#pragma unroll
+        for (int e = 0; e < ML; ++e) c[e] = e < len ? __ldg(&ci[k0 + e]) : 0;
+        double b[ML][V];
+#pragma unroll
+        for (int e = 0; e < ML; ++e)
+          if (e < len) ldgv<V>(pg + (size_t)c[e] * S, b[e]);
+        double y[V] = {0.0, 0.0};
+#pragma unroll
+        for (int e = 0; e < ML; ++e) {
+          if (e < len) {
+            const double2 a = *reinterpret_cast<const double2*>(sv + (size_t)e * S);
+            y[0] = __dadd_rn(y[0], __dmul_rn(a.x, b[e][0]));
+            y[1] = __dadd_rn(y[1], __dmul_rn(a.y, b[e][1]));
+          }
+        }
+        stv<V>(ap + base + row * S, y);
+        double pv[V];
+        ldgv<V>(pg + row * S, pv);
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[0][j] = __fma_rn(pv[j], y[j], acc[0][j]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
+    const bool chunk_end = ((i + 1) % ct == 0) || (tile == geo.tiles - 1);
+    if (chunk_end) {
+      const int chunk = (int)(tile / ct);
+      if (reduce_lanes_c<1, V>(acc, red, st.part, st.ticket, g, chunk, geo, &s_last)) {
+        if (t < geo.L) {
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            const size_t l = (size_t)g * S + V * t + j;
+            const double pap = red[j * geo.T + t];
+            const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
+            st.frozen[l] = fr;
+            st.alpha[l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
+          }
+        }
+        if (t == 0) st.it[g] += 1;
+      }
+      acc[0][0] = acc[0][1] = 0.0;
+    }
+  }
+}
+
 // Fully staged variant for banded graphs (BandHint): per tile, one elected
 // thread bulk-copies the tile's values, its column indices and row offsets
 // (16-byte aligned spans of the padded graph) and the nb p bands the tile's
@@ -1021,6 +1219,23 @@ static void launch_spmv_tma(const Geo& gl, int G, cudaStream_t s, long long N, l
 }
 
 template <int ML>
+static void launch_spmv_ws(const Geo& gl, int G, cudaStream_t s, long long N, long long nnz,
+                           const PcgState& st, const int* ro, const int* ci, const double* vals,
+                           const double* p, double* ap, const BandHint* bands) {
+  const size_t smem = (size_t)2 * gl.T * sizeof(double) +
+                      (size_t)kWsStages * gl.R * ML * gl.S * sizeof(double) + 2 * kWsStages * 8;
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaFuncSetAttribute(pcg_spmv_ws_kernel<ML>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    configured = smem;
+  }
+  BandHint bh{};
+  if (bands && (reinterpret_cast<uintptr_t>(p) & 15) == 0) bh = *bands;
+  pcg_spmv_ws_kernel<ML><<<dim3(gl.B, G), 288, smem, s>>>(N, nnz, gl, st, ro, ci, vals, p, ap, bh);
+}
+
+template <int ML>
 static void launch_spmv_tma_meta(const Geo& gl, int G, cudaStream_t s, long long N, long long nnz,
                                  const PcgState& st, const int* ro, const int* ci,
                                  const double* vals, const double* p, double* ap) {
@@ -1089,7 +1304,12 @@ void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long lo
   }
   if (mode && gl.V == 2 && aligned && gl.maxrow >= 1 && gl.maxrow <= 8) {
     // the metadata variant needs R + 1 <= T and R * ML <= 2T (S >= 8)
-    if (mode == 2 && gl.Lp >= 4) {
+    if (mode == 4 && gl.T == 256) {
+      if (gl.maxrow <= 5)
+        launch_spmv_ws<5>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
+      else
+        launch_spmv_ws<8>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
+    } else if (mode == 2 && gl.Lp >= 4) {
       if (gl.maxrow <= 5)
         launch_spmv_tma_meta<5>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap);
       else

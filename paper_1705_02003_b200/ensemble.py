@@ -20,7 +20,6 @@ CPU callback inside the device loop, which this build deliberately lacks.
 from __future__ import annotations
 
 import ctypes
-from dataclasses import dataclass
 from typing import Sequence
 
 import numpy as np
