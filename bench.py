@@ -61,10 +61,13 @@ def bytes_model(cfg):
     """Algorithmic bytes per group per launch (DESIGN.md / SURVEY.md 8d)."""
     S, N, nnz = cfg.ensemble_size, cfg.n_dofs, cfg.nnz
     spmv = 8 * S * nnz + 4 * nnz + 4 * (N + 1) + 16 * S * N
-    update = 7 * 8 * S * N
-    direction = 4 * 8 * S * N
+    update = 4 * 8 * S * N      # read r, Ap, dinv; write r
+    direction = 6 * 8 * S * N   # read x, p, r, dinv; write x, p (x += alpha p deferred here)
     return {"spmv": spmv, "update": update, "dir": direction,
-            "pcg_iter": 8 * S * (nnz + 13 * N) + 4 * (nnz + N + 1)}
+            # SURVEY 8d's algorithmic bytes per PCG iteration (13 vector passes) and
+            # the bytes this implementation actually moves (12 passes)
+            "pcg_iter": 8 * S * (nnz + 13 * N) + 4 * (nnz + N + 1),
+            "pcg_iter_moved": spmv + update + direction}
 
 
 def make_workload(cfg, solver=None):
@@ -435,7 +438,10 @@ def main():
                      "bytes_per_group_launch": bm["spmv"],
                      "group_launches": group_iters},
         "pcg_loop": {"achieved_gbs": loop_gbs, "frac": loop_gbs / peak if loop_gbs else None,
-                     "bytes_per_group_iter": bm["pcg_iter"], "step_gbs": step_gbs,
+                     "bytes_per_group_iter": bm["pcg_iter"],
+                     "moved_gbs": (loop_gbs * bm["pcg_iter_moved"] / bm["pcg_iter"])
+                     if loop_gbs else None,
+                     "moved_bytes_per_group_iter": bm["pcg_iter_moved"], "step_gbs": step_gbs,
                      "group_iterations": group_iters},
         "kernels": kern,
         "all_converged": conv_all,
