@@ -49,6 +49,11 @@ def parse():
     ap.add_argument("--separate-kernel-timing", action="store_true",
                     help="time `value` without per-launch events; kernel breakdown from a "
                          "second, identical profiled pass (small configs: event overhead)")
+    ap.add_argument("--max-iters", type=int, default=None,
+                    help="throughput mode: run exactly this many PCG iterations per group "
+                         "(value = sample-iterations/s); for C4/C5 where full solves take minutes")
+    ap.add_argument("--max-samples", type=int, default=None,
+                    help="use only the first samples of the workload")
     ap.add_argument("--wave", type=int, default=None,
                     help="max groups per device wave (default: as many as fit in HBM)")
     return ap.parse_args()
@@ -287,6 +292,15 @@ def main():
     solver = uq.EnsembleSolver2D(field, cfg.cells, cfg.tol, cfg.maxit, cfg.a2,
                                  max_groups_per_wave=args.wave)
     ids, coords, keys, meta = make_workload(cfg, solver)
+    if args.max_iters:
+        # throughput mode (C4/C5: a full solve of a level takes minutes): every
+        # group runs exactly max_iters PCG iterations; `value` then counts
+        # sample-iterations, not sample-solves, and says so in `unit`
+        solver.maxit = args.max_iters
+        solver.tol = 1e-300
+    if args.max_samples and len(ids) > args.max_samples:
+        ids, coords = ids[: args.max_samples], coords[: args.max_samples]
+        keys = None if keys is None else keys[: args.max_samples]
     # weak scaling: rank r solves the mirror images of the level's samples and
     # groups them by the keys of their originals (same sort work, same costs shape)
     coords = reflect(coords, rank)
@@ -385,6 +399,10 @@ def main():
         return
     total_ms = sum(times)
     value = world * n * len(times) / (total_ms / 1e3)
+    unit = "sample-solves/s"
+    if args.max_iters:  # throughput mode: sample-iterations per second
+        value *= args.max_iters
+        unit = f"sample-iterations/s (throughput mode: {args.max_iters} PCG iterations per group)"
     bm = bytes_model(cfg)
     peaks = {}
     pk = ROOT / "MEASURED_PEAKS.json"
@@ -407,7 +425,7 @@ def main():
     line = {
         "metric": METRIC,
         "value": value,
-        "unit": "sample-solves/s",
+        "unit": unit,
         "n_gpus": world,
         "steps": len(times),
         "warmup": max(3, args.warmup),
@@ -426,7 +444,8 @@ def main():
                          f"{solver.bytes_per_group(S) * K / 1e9:.1f} GB per step)",
                    "workload_source": meta.get("source")},
         "gpu_launches": int(launches),
-        "e2e": {"value": world * n * len(e2e_t) / sum(e2e_t), "unit": "sample-solves/s",
+        "e2e": {"value": world * n * len(e2e_t) / sum(e2e_t) * (args.max_iters or 1),
+                "unit": unit,
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "roofline": {"bound": "hbm", "kernel": "pcg_spmv_kernel",
                      "achieved": spmv_gbs, "peak": peak, "unit": "GB/s",
