@@ -166,10 +166,13 @@ class SparseGrid:
         out = d_pts.new_empty((len(pts),))
         if n == 0:
             return np.zeros(len(pts))
+        # keep the device copies referenced until the kernel has run (a temporary
+        # freed before the launch could be handed to the next allocation)
+        d_ctr = _lib.to_dev(np.ascontiguousarray(self._ctr[:n]))
+        d_hw = _lib.to_dev(np.ascontiguousarray(self._hw[:n]))
+        d_c = _lib.to_dev(np.ascontiguousarray(c))
         _lib.call("uqg_surrogate_eval", _lib.ctx(), _lib.ptr(d_pts), len(pts), self.dim,
-                  _lib.ptr(_lib.to_dev(np.ascontiguousarray(self._ctr[:n]))),
-                  _lib.ptr(_lib.to_dev(np.ascontiguousarray(self._hw[:n]))),
-                  _lib.ptr(_lib.to_dev(np.ascontiguousarray(c))), n, _lib.ptr(out), _lib.stream())
+                  _lib.ptr(d_ctr), _lib.ptr(d_hw), _lib.ptr(d_c), n, _lib.ptr(out), _lib.stream())
         return out.cpu().numpy()
 
     def error_indicator(self, channel: str) -> float:
