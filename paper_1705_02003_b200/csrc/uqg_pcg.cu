@@ -769,6 +769,151 @@ __global__ void __launch_bounds__(256, 3) pcg_spmv_tma_meta_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// Paired variant: a step covers two consecutive tiles of a chunk (one bulk
+// copy of 2R rows' values, 2 stages), and every thread computes its row in
+// both tiles with all gathers of both rows issued before the ordered sums -
+// two independent dependent-load chains per thread and half the CTA barriers
+// per row.  The per-thread accumulation still runs tile by tile, so results
+// are identical.
+constexpr int kPairStages = 2;
+
+template <int ML>
+__global__ void __launch_bounds__(256, 2) pcg_spmv_pair_kernel(
+    long long N, long long nnz, Geo geo, PcgState st, const int* __restrict__ ro,
+    const int* __restrict__ ci, const double* __restrict__ vals, const double* __restrict__ p,
+    double* __restrict__ ap, BandHint bh) {
+  constexpr int V = 2;
+  extern __shared__ __align__(128) double red[];
+  const int g = blockIdx.y, t = threadIdx.x;
+  if (st.done[g] != kRunning) return;
+  const int S = geo.S, R = geo.R;
+  const int stage_doubles = 2 * R * ML * S;
+  double* stage = red + V * geo.T;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage + kPairStages * stage_doubles);
+  const double* vg = vals + (size_t)g * nnz * S;
+  const double* pg_all = p + (size_t)g * N * S;
+  const int n_tiles = block_tile_count(geo);
+  const int ct = (int)geo.chunk_tiles;
+  const long long tiles = geo.tiles;
+  auto tile_of = [&](int i) -> long long {
+    const int j = i / ct;
+    return ((long long)blockIdx.x + (long long)j * gridDim.x) * ct + (i - j * ct);
+  };
+  // tiles in the step starting at block-tile index i: 2 if tile i+1 is in the same chunk
+  auto step_len = [&](int i) -> int {
+    return (i + 1 < n_tiles && (i % ct) + 1 < ct) ? 2 : 1;
+  };
+  auto issue = [&](int k, int i) {  // thread 0: step k starts at block-tile i
+    const int u = step_len(i);
+    const long long r0 = tile_of(i) * R;
+    long long r1 = r0 + (long long)u * R;
+    r1 = r1 < N ? r1 : N;
+    const int k0 = __ldg(&ro[r0]), k1 = __ldg(&ro[r1]);
+    const uint32_t bytes = (uint32_t)(k1 - k0) * (uint32_t)S * 8u;
+    uint64_t* bar = &bars[k % kPairStages];
+    fence_proxy_async();
+    mbar_expect_tx(bar, bytes);
+    if (bytes) bulk_g2s(stage + (k % kPairStages) * stage_doubles, vg + (size_t)k0 * S, bytes, bar);
+#pragma unroll
+    for (int b = 0; b < kMaxBands; ++b) {
+      if (b < bh.nb) {
+        long long lo = r0 + bh.start[b], hi = lo + (long long)u * R + bh.extra[b];
+        lo = lo < 0 ? 0 : lo;
+        hi = hi > N ? N : hi;
+        if (hi > lo) bulk_prefetch_l2(pg_all + lo * S, (uint32_t)(hi - lo) * S * 8u);
+      }
+    }
+    return i + u;
+  };
+  int next_issue_tile = 0, next_issue_step = 0;
+  if (t == 0) {
+    for (int s = 0; s < kPairStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    while (next_issue_step < kPairStages && next_issue_tile < n_tiles)
+      next_issue_tile = issue(next_issue_step++, next_issue_tile);
+  }
+  __syncthreads();
+
+  const int sl = t % geo.Lp, rr = t / geo.Lp;
+  const size_t base = (size_t)g * N * S + V * sl;
+  const double* pg = p + base;
+  double acc[1][V] = {};
+  int i = 0;
+  for (int k = 0; i < n_tiles; ++k) {
+    const int u = step_len(i);
+    const long long tile = tile_of(i);
+    const int s = k % kPairStages;
+    mbar_wait(&bars[s], (uint32_t)((k / kPairStages) & 1));
+    if (sl < geo.L) {
+      const long long r0 = tile * R;
+      const int kt0 = __ldg(&ro[r0]);
+      int c[2][ML], len[2], kr[2];
+      bool ok[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const long long row = r0 + (long long)q * R + rr;
+        ok[q] = q < u && row < N;
+        kr[q] = ok[q] ? __ldg(&ro[row]) : 0;
+        len[q] = ok[q] ? __ldg(&ro[row + 1]) - kr[q] : 0;
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int e = 0; e < ML; ++e) c[q][e] = e < len[q] ? __ldg(&ci[kr[q] + e]) : 0;
+      double b[2][ML][V];
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int e = 0; e < ML; ++e)
+          if (e < len[q]) ldgv<V>(pg + (size_t)c[q][e] * S, b[q][e]);
+      double pv[2][V];
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        if (ok[q]) ldgv<V>(pg + (size_t)(r0 + (long long)q * R + rr) * S, pv[q]);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (!ok[q]) continue;
+        const double* sv = stage + s * stage_doubles + (size_t)(kr[q] - kt0) * S + V * sl;
+        double y[V] = {0.0, 0.0};
+#pragma unroll
+        for (int e = 0; e < ML; ++e) {
+          if (e < len[q]) {
+            const double2 a = *reinterpret_cast<const double2*>(sv + (size_t)e * S);
+            y[0] = __dadd_rn(y[0], __dmul_rn(a.x, b[q][e][0]));
+            y[1] = __dadd_rn(y[1], __dmul_rn(a.y, b[q][e][1]));
+          }
+        }
+        stv<V>(ap + base + (size_t)(r0 + (long long)q * R + rr) * S, y);
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[0][j] = __fma_rn(pv[q][j], y[j], acc[0][j]);
+      }
+    }
+    __syncthreads();  // stage s consumed
+    if (t == 0 && next_issue_tile < n_tiles) next_issue_tile = issue(next_issue_step++, next_issue_tile);
+    const long long last_tile = tile + u - 1;
+    i += u;
+    const bool chunk_end = (i % ct == 0) || (last_tile == tiles - 1);
+    if (chunk_end) {
+      const int chunk = (int)(last_tile / ct);
+      if (reduce_lanes<1, V>(acc, red, st.part, st.ticket, g, chunk, geo)) {
+        if (t < geo.L) {
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            const size_t l = (size_t)g * S + V * t + j;
+            const double pap = red[j * geo.T + t];
+            const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
+            st.frozen[l] = fr;
+            st.alpha[l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
+          }
+        }
+        if (t == 0) st.it[g] += 1;
+      }
+      acc[0][0] = acc[0][1] = 0.0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Warp-specialized variant: one producer warp streams the tiles' values into a
 // 4-stage ring (full/empty mbarrier pair per stage) while 8 consumer warps
 // compute; a consumer warp releases a stage with one mbarrier arrive, so there
@@ -1219,6 +1364,25 @@ static void launch_spmv_tma(const Geo& gl, int G, cudaStream_t s, long long N, l
 }
 
 template <int ML>
+static void launch_spmv_pair(const Geo& gl, int G, cudaStream_t s, long long N, long long nnz,
+                             const PcgState& st, const int* ro, const int* ci, const double* vals,
+                             const double* p, double* ap, const BandHint* bands) {
+  const size_t smem = (size_t)2 * gl.T * sizeof(double) +
+                      (size_t)kPairStages * 2 * gl.R * ML * gl.S * sizeof(double) +
+                      kPairStages * 8;
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaFuncSetAttribute(pcg_spmv_pair_kernel<ML>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    configured = smem;
+  }
+  BandHint bh{};
+  if (bands && (reinterpret_cast<uintptr_t>(p) & 15) == 0) bh = *bands;
+  pcg_spmv_pair_kernel<ML><<<dim3(gl.B, G), gl.T, smem, s>>>(N, nnz, gl, st, ro, ci, vals, p, ap,
+                                                             bh);
+}
+
+template <int ML>
 static void launch_spmv_ws(const Geo& gl, int G, cudaStream_t s, long long N, long long nnz,
                            const PcgState& st, const int* ro, const int* ci, const double* vals,
                            const double* p, double* ap, const BandHint* bands) {
@@ -1309,6 +1473,11 @@ void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long lo
         launch_spmv_ws<5>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
       else
         launch_spmv_ws<8>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
+    } else if (mode == 5) {
+      if (gl.maxrow <= 5)
+        launch_spmv_pair<5>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
+      else
+        launch_spmv_pair<8>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
     } else if (mode == 2 && gl.Lp >= 4) {
       if (gl.maxrow <= 5)
         launch_spmv_tma_meta<5>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap);
