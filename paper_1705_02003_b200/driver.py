@@ -16,9 +16,8 @@ from dataclasses import dataclass, field as dc_field
 import numpy as np
 
 from .configs import StudyConfig
-from .field import build_field
 from .grouping import group_by_key, group_natural
-from .solve import EnsembleSolver2D
+from .solve import EnsembleSolver
 from .sparse_grid import SparseGrid
 
 QOI, ITER = "qoi", "iterations"
@@ -42,7 +41,7 @@ def sample_set(cfg: StudyConfig) -> np.ndarray:
     return np.random.default_rng(0).uniform(-1.0, 1.0, (cfg.synthetic_samples, cfg.n_modes))
 
 
-def adaptive_run(cfg: StudyConfig, solver: EnsembleSolver2D | None = None, shard=None,
+def adaptive_run(cfg: StudyConfig, solver: EnsembleSolver | None = None, shard=None,
                  max_levels: int | None = None, device_keys: bool = False):
     """Run the grouped adaptive loop; returns (records, stop_reason, grid).
 
