@@ -62,17 +62,27 @@ def parse():
 # ---------------------------------------------------------------------------
 # workload
 
-def bytes_model(cfg):
-    """Algorithmic bytes per group per launch (DESIGN.md / SURVEY.md 8d)."""
+def bytes_model(cfg, op=None):
+    """Algorithmic bytes per group per launch (DESIGN.md / SURVEY.md 8d).
+
+    CSR operator: the SURVEY 8d figures.  Face-form FV2D operator (``op.faces``):
+    the operator stream is ``op.n_op`` doubles per lane (faces) instead of nnz
+    values + the int32 graph - the same formula with the smaller operator.
+    """
     S, N, nnz = cfg.ensemble_size, cfg.n_dofs, cfg.nnz
-    spmv = 8 * S * nnz + 4 * nnz + 4 * (N + 1) + 16 * S * N
+    if op is not None and getattr(op, "faces", False):
+        n_op, graph = op.n_op, 0
+    else:
+        n_op, graph = nnz, 4 * nnz + 4 * (N + 1)
+    spmv = 8 * S * n_op + graph + 16 * S * N
     update = 4 * 8 * S * N      # read r, Ap, dinv; write r
     direction = 6 * 8 * S * N   # read x, p, r, dinv; write x, p (x += alpha p deferred here)
     return {"spmv": spmv, "update": update, "dir": direction,
             # SURVEY 8d's algorithmic bytes per PCG iteration (13 vector passes) and
             # the bytes this implementation actually moves (12 passes)
-            "pcg_iter": 8 * S * (nnz + 13 * N) + 4 * (nnz + N + 1),
-            "pcg_iter_moved": spmv + update + direction}
+            "pcg_iter": 8 * S * (n_op + 13 * N) + graph,
+            "pcg_iter_moved": spmv + update + direction,
+            "operator": "fv2d faces" if graph == 0 else "csr"}
 
 
 def make_workload(cfg, solver=None):
@@ -403,7 +413,7 @@ def main():
     if args.max_iters:  # throughput mode: sample-iterations per second
         value *= args.max_iters
         unit = f"sample-iterations/s (throughput mode: {args.max_iters} PCG iterations per group)"
-    bm = bytes_model(cfg)
+    bm = bytes_model(cfg, solver.op)
     peaks = {}
     pk = ROOT / "MEASURED_PEAKS.json"
     if pk.exists():
@@ -413,7 +423,8 @@ def main():
     traffic = {}
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
-        traffic = json.loads(tf.read_text()).get(cfg.name, {})
+        key = cfg.name if bm["operator"] == "csr" else f"{cfg.name}:faces"
+        traffic = json.loads(tf.read_text()).get(key, {})
     spmv_ms = ms[3]
     spmv_gbs = group_iters * bm["spmv"] / (spmv_ms / 1e3) / 1e9 if spmv_ms else None
     loop_ms = ms[3] + ms[4] + ms[5]
@@ -447,7 +458,10 @@ def main():
         "e2e": {"value": world * n * len(e2e_t) / sum(e2e_t) * (args.max_iters or 1),
                 "unit": unit,
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
-        "roofline": {"bound": "hbm", "kernel": "pcg_spmv_kernel",
+        "roofline": {"bound": "hbm",
+                     "kernel": ("pcg_spmv_fv2d_kernel" if bm["operator"] != "csr"
+                                else "pcg_spmv_tma_kernel"),
+                     "operator": bm["operator"],
                      "achieved": spmv_gbs, "peak": peak, "unit": "GB/s",
                      "frac": (spmv_gbs / peak) if spmv_gbs else None,
                      "traffic": traffic.get("dram_bytes_per_launch"),

@@ -176,6 +176,30 @@ int uqg_pcg(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const i
 /* Device bytes of scratch uqg_pcg needs for (N, S, G) (r, p, Ap, partials). */
 long long uqg_pcg_workspace_bytes(int N, int nnz, int S, int G);
 
+/* Face form of the 2D 5-point FV operator (same matrix as uqg_assemble_fv2d,
+ * stored once per face instead of once per CSR entry; fv2d.py:46-80 values).
+ * With m = n_cells - 1 and N = m*m unknowns:
+ *   tx [G][(m+1)*m][S]: x-face f*m + (j-1) between cell rows f, f+1 at column
+ *      j, i.e. row (i,j) has Tw = tx[row], Te = tx[row + m];
+ *   ty [G][m*(m+1)][S]: y-face (i-1)*(m+1) + k between columns k, k+1 of row
+ *      i (Ts = ty[row + i - 1], Tn = ty[row + i]); only when a2_same, else
+ *      NULL and the y-faces are the constant a_y;
+ *   dinv [G][N][S] = 1/diag (may be NULL).
+ * uqg_spmv_fv2d / uqg_pcg_fv2d apply it with the products of the CSR row in
+ * CSR column order: results are bit-identical to uqg_spmv / uqg_pcg on the
+ * CSR form (arguments otherwise as uqg_pcg; the workspace size is
+ * uqg_pcg_workspace_bytes(m*m, 0, S, G)). */
+int uqg_assemble_fv2d_faces(uqg_ctx* ctx, int n_cells, int G, int S, const double* a_nodes,
+                            double a_y, int a2_same, double* tx, double* ty, double* dinv,
+                            void* stream);
+int uqg_spmv_fv2d(uqg_ctx* ctx, int n_cells, int S, int G, const double* tx, const double* ty,
+                  double a_y, const double* x, double* y, void* stream);
+int uqg_pcg_fv2d(uqg_ctx* ctx, int n_cells, int S, int G, const double* tx, const double* ty,
+                 double a_y, const double* rhs, double rhs_const, const double* dinv, double tol,
+                 int maxit, double* x, int* iters, unsigned char* converged,
+                 unsigned char* frozen, int* ens_iters, double* hist_host, int hist_cap,
+                 int* hist_rows_host, void* stream);
+
 /* Grouping keys on the device.
  * uqg_surrogate_eval: out[i] = sum_j prod_d max(0, 1 - |y[i][d] - c[j][d]| / w[j][d])
  * * surplus[j] (HierGrid.eval_many / _basis_block, hier_grid.py:317-359);

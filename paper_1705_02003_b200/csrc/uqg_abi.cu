@@ -447,6 +447,28 @@ long long uqg_pcg_workspace_bytes(int N, int nnz, int S, int G) {
   return (long long)pcg_layout(c, N, geo, G, nullptr, nullptr, nullptr, nullptr);
 }
 
+}  // extern "C"
+
+namespace {
+
+// The operator of a PCG solve: shared-graph CSR (row_offsets / col_indices /
+// vals) or the face form of the 2D FV operator (fv.tx != nullptr).
+struct SpOp {
+  const int* ro;
+  const int* ci;
+  const double* vals;
+  Fv2dOp fv;
+};
+
+int pcg_impl(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const SpOp& op,
+             const double* rhs, double rhs_const, const double* dinv, double tol, int maxit,
+             double* x, int* iters, unsigned char* converged, unsigned char* frozen,
+             int* ens_iters, double* hist_host, int hist_cap, int* hist_rows_host, void* stream);
+
+}  // namespace
+
+extern "C" {
+
 int uqg_pcg(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const int* row_offsets,
             const int* col_indices, const double* vals, const double* rhs, double rhs_const,
             const double* dinv, double tol, int maxit, double* x, int* iters,
@@ -455,6 +477,61 @@ int uqg_pcg(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const i
   UQG_REQUIRE(ctx && row_offsets && x && iters && converged && frozen && ens_iters,
               "uqg_pcg: NULL argument");
   UQG_REQUIRE(N >= 0 && nnz >= 0 && S >= 1 && S <= kMaxLanes && G >= 1, "uqg_pcg: bad sizes");
+  SpOp op{row_offsets, col_indices, vals, Fv2dOp{0, nullptr, nullptr, 0.0}};
+  return pcg_impl(ctx, N, nnz, max_row_len, S, G, op, rhs, rhs_const, dinv, tol, maxit, x, iters,
+                  converged, frozen, ens_iters, hist_host, hist_cap, hist_rows_host, stream);
+}
+
+int uqg_assemble_fv2d_faces(uqg_ctx* ctx, int n_cells, int G, int S, const double* a_nodes,
+                            double a_y, int a2_same, double* tx, double* ty, double* dinv,
+                            void* stream) {
+  UQG_REQUIRE(ctx && a_nodes && tx && (!a2_same || ty), "uqg_assemble_fv2d_faces: NULL argument");
+  UQG_REQUIRE(n_cells >= 2 && G >= 1 && S >= 1, "uqg_assemble_fv2d_faces: bad sizes");
+  const long long m = n_cells - 1;
+  const long long total = (long long)G * (m * m + m) * S;
+  cudaStream_t s = as_stream(stream);
+  UQG_LAUNCH(UQG_K_ASSEMBLE, s,
+             assemble_fv2d_faces_kernel<<<grid_for(total, 256), 256, 0, s>>>(
+                 n_cells, G, S, a_nodes, a2_same, a_y, tx, a2_same ? ty : nullptr, dinv));
+  return UQG_OK;
+}
+
+int uqg_spmv_fv2d(uqg_ctx* ctx, int n_cells, int S, int G, const double* tx, const double* ty,
+                  double a_y, const double* x, double* y, void* stream) {
+  UQG_REQUIRE(ctx && tx && x && y, "uqg_spmv_fv2d: NULL argument");
+  UQG_REQUIRE(n_cells >= 2 && S >= 1 && S <= kMaxLanes && G >= 1, "uqg_spmv_fv2d: bad sizes");
+  const long long m = n_cells - 1, N = m * m;
+  UQG_REQUIRE((N + m) * S <= 0x7fffffffLL, "uqg_spmv_fv2d: (N + m) * S must be < 2^31");
+  Geo geo = make_geo(N, S, 5);
+  cudaStream_t s = as_stream(stream);
+  Fv2dOp op{(int)m, tx, ty, a_y};
+  UQG_LAUNCH(UQG_K_SPMV, s, launch_spmv_fv2d(geo, G, s, N, op, x, y));
+  return UQG_OK;
+}
+
+int uqg_pcg_fv2d(uqg_ctx* ctx, int n_cells, int S, int G, const double* tx, const double* ty,
+                 double a_y, const double* rhs, double rhs_const, const double* dinv, double tol,
+                 int maxit, double* x, int* iters, unsigned char* converged,
+                 unsigned char* frozen, int* ens_iters, double* hist_host, int hist_cap,
+                 int* hist_rows_host, void* stream) {
+  UQG_REQUIRE(ctx && tx && x && iters && converged && frozen && ens_iters,
+              "uqg_pcg_fv2d: NULL argument");
+  UQG_REQUIRE(n_cells >= 2 && S >= 1 && S <= kMaxLanes && G >= 1, "uqg_pcg_fv2d: bad sizes");
+  const long long m = n_cells - 1;
+  UQG_REQUIRE((m * m + m) * S <= 0x7fffffffLL, "uqg_pcg_fv2d: (N + m) * S must be < 2^31");
+  SpOp op{nullptr, nullptr, nullptr, Fv2dOp{(int)m, tx, ty, a_y}};
+  return pcg_impl(ctx, (int)(m * m), 0, 5, S, G, op, rhs, rhs_const, dinv, tol, maxit, x, iters,
+                  converged, frozen, ens_iters, hist_host, hist_cap, hist_rows_host, stream);
+}
+
+}  // extern "C"
+
+namespace {
+
+int pcg_impl(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const SpOp& op,
+             const double* rhs, double rhs_const, const double* dinv, double tol, int maxit,
+             double* x, int* iters, unsigned char* converged, unsigned char* frozen,
+             int* ens_iters, double* hist_host, int hist_cap, int* hist_rows_host, void* stream) {
   UQG_REQUIRE(tol > 0.0 && tol <= 1.7976931348623157e308, "tol must be positive and finite");
   UQG_REQUIRE(maxit >= 0, "maxit must be >= 0");
   UQG_REQUIRE(!hist_host || (hist_cap >= 0 && hist_rows_host), "uqg_pcg: bad history buffer");
@@ -484,7 +561,8 @@ int uqg_pcg(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const i
   // 0 = launch loop; auto = cluster kernel for small batches (< 512 MB per
   // iteration), launch loop otherwise.
   const int pmode = persistent_mode();
-  const double iter_bytes = 8.0 * S * ((double)nnz + 12.0 * N) * G;
+  const double op_elems = op.fv.tx ? (double)(N + op.fv.m) * (op.fv.ty ? 2 : 1) : (double)nnz;
+  const double iter_bytes = 8.0 * S * (op_elems + 12.0 * N) * G;
   const bool small = iter_bytes < 512e6;
   bool use_cluster = false;
   int pblocks = 0;
@@ -501,9 +579,8 @@ int uqg_pcg(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const i
     UQG_TRY_CUDA(cudaMemsetAsync(pb.bar, 0, (2 * (size_t)G + 1) * sizeof(unsigned), s));
     cudaError_t le = cudaSuccess;
     UQG_LAUNCH(UQG_K_PCG_SPMV, s, {
-      le = launch_pcg_persistent(geo, G, pblocks, use_cluster, s, N, nnz, st, row_offsets,
-                                 col_indices, vals,
-                                 rhs, rhs_const, dinv, tol, maxit, x, r, p, ap, pb.partA, st.part,
+      le = launch_pcg_persistent(geo, G, pblocks, use_cluster, s, N, nnz, st, op.ro, op.ci,
+                                 op.vals, op.fv, rhs, rhs_const, dinv, tol, maxit, x, r, p, ap, pb.partA, st.part,
                                  pb.bar, pb.bar + G, reinterpret_cast<int*>(pb.bar + 2 * G));
     });
     if (le != cudaSuccess) {
@@ -541,9 +618,12 @@ int uqg_pcg(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const i
     // depend on this.
     const Geo gact = with_groups(geo, std::max(1, G - ctx->pinned[0]));
     for (int k = 0; k < chunk; ++k) {
-      UQG_LAUNCH(UQG_K_PCG_SPMV, s,
-                 launch_pcg_spmv(gact, G, s, N, nnz, st, row_offsets, col_indices, vals, p, ap,
-                                 ctx->bands.nb ? &ctx->bands : nullptr));
+      if (op.fv.tx)
+        UQG_LAUNCH(UQG_K_PCG_SPMV, s, launch_pcg_spmv_fv2d(gact, G, s, N, st, op.fv, p, ap));
+      else
+        UQG_LAUNCH(UQG_K_PCG_SPMV, s,
+                   launch_pcg_spmv(gact, G, s, N, nnz, st, op.ro, op.ci, op.vals, p, ap,
+                                   ctx->bands.nb ? &ctx->bands : nullptr));
       UQG_LAUNCH(UQG_K_PCG_UPDATE, s, launch_pcg_update(gact, G, s, N, st, dinv, maxit, r, ap));
       UQG_LAUNCH(UQG_K_PCG_DIR, s, launch_pcg_dir(gact, G, s, N, st, dinv, r, x, p));
     }
@@ -587,6 +667,10 @@ int uqg_pcg(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const i
   }
   return UQG_OK;
 }
+
+}  // namespace
+
+extern "C" {
 
 int uqg_surrogate_eval(uqg_ctx* ctx, const double* points, int n, int dim, const double* centers,
                        const double* widths, const double* surplus, int n_nodes, double* out,

@@ -141,6 +141,18 @@ __device__ __forceinline__ void ldgv(const double* p, double (&o)[V]) {
   }
 }
 
+// L2-only path (vectors written by other SMs inside the same launch)
+template <int V>
+__device__ __forceinline__ void ldcgv(const double* p, double (&o)[V]) {
+  if constexpr (V == 2) {
+    const double2 t = __ldcg(reinterpret_cast<const double2*>(p));
+    o[0] = t.x;
+    o[1] = t.y;
+  } else {
+    o[0] = __ldcg(p);
+  }
+}
+
 template <int V>
 __device__ __forceinline__ void stv(double* p, const double (&o)[V]) {
   if constexpr (V == 2) {
@@ -221,6 +233,62 @@ __device__ bool reduce_lanes(const double (&val)[NV][V], double* red, double* pa
   __syncthreads();
   tree_rows<NS>(red, T, Lp, R, t);
   if (t == 0) ticket[g] = 0u;  // ready for the next reduction on this counter
+  return true;
+}
+
+// reduce_lanes for NV = 1 over a batch of nk chunks chunk0 + k*stride
+// (k < nk) whose per-thread values the caller has stored in
+// red[(k*V + j)*T + t]: one in-block tree for the whole batch (instead of one
+// per chunk), one ticket add of nk, then the final stage of reduce_lanes.
+// Every partial and the final sum are computed exactly as reduce_lanes<1, V>
+// computes them, so results are bit-identical.  red must hold
+// max(nk, 1) * V * T doubles.
+template <int V>
+__device__ bool reduce_lanes_batch(double* red, double* part, unsigned int* ticket, int g,
+                                   int chunk0, int stride, int nk, const Geo& geo) {
+  const int t = threadIdx.x;
+  const int T = geo.T, Lp = geo.Lp, R = geo.R, L = geo.L, S = geo.S, C = geo.chunks;
+  const int ns = nk * V;
+  __syncthreads();
+  for (int st = R >> 1; st > 0; st >>= 1) {
+    if ((t / Lp) < st) {
+      for (int v = 0; v < ns; ++v) red[v * T + t] += red[v * T + t + st * Lp];
+    }
+    __syncthreads();
+  }
+  if (t < L) {
+    for (int k = 0; k < nk; ++k)
+#pragma unroll
+      for (int j = 0; j < V; ++j)
+        part[((size_t)g * C + chunk0 + k * stride) * S + V * t + j] = red[(k * V + j) * T + t];
+  }
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (t == 0) {
+    unsigned int tk = atomicAdd(&ticket[g], (unsigned)nk);
+    s_last = (tk + (unsigned)nk == (unsigned)C);
+  }
+  __syncthreads();
+  if (!s_last) return false;
+  __threadfence();
+  const int sl = t % Lp, jr = t / Lp;
+  double acc[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) acc[v] = 0.0;
+  if (sl < L) {
+#pragma unroll 4
+    for (int cc = jr; cc < C; cc += R) {
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc[j] += __ldcg(&part[((size_t)g * C + cc) * S + V * sl + j]);
+    }
+  }
+  __syncthreads();  // the batch's tree values in red[] have been consumed
+#pragma unroll
+  for (int v = 0; v < V; ++v) red[v * T + t] = acc[v];
+  __syncthreads();
+  tree_rows<V>(red, T, Lp, R, t);
+  if (t == 0) ticket[g] = 0u;
   return true;
 }
 

@@ -132,6 +132,50 @@ __global__ void assemble_fv2d_kernel(int n, int G, int S, const double* __restri
   }
 }
 
+// Face form of the same operator (Fv2dOp in uqg_kernels.cuh): one thread per
+// (group, face slot, lane).  Face slot q in [0, (m+1)*m) writes the x-face
+// tx[q] (rows f = q / m and f + 1, column j = q % m + 1), the y-face ty[q]
+// (row i = q / (m+1) + 1, columns k = q % (m+1) and k + 1) when the y
+// coefficient is random, and - for q < N, cell q - the Jacobi inverse
+// diagonal.  Same harmonic means and diagonal sum as assemble_fv2d_kernel.
+__global__ void assemble_fv2d_faces_kernel(int n, int G, int S, const double* __restrict__ a_nodes,
+                                           int a2_same, double a_y, double* __restrict__ tx,
+                                           double* __restrict__ ty, double* __restrict__ dinv) {
+  const int m = n - 1, n1 = n + 1;
+  const long long N = (long long)m * m, F = N + m, P = (long long)n1 * n1;
+  const long long total = (long long)G * F * S;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(idx % S);
+    const long long gq = idx / S;
+    const long long q = gq % F;
+    const int g = (int)(gq / F);
+    const double* a = a_nodes + (size_t)g * P * S + s;
+    {
+      const int f = (int)(q / m), j = (int)(q % m) + 1;
+      tx[idx] = harm(a[((long long)f * n1 + j) * S], a[((long long)(f + 1) * n1 + j) * S]);
+    }
+    if (a2_same) {
+      const int i = (int)(q / (m + 1)) + 1, k = (int)(q % (m + 1));
+      ty[idx] = harm(a[((long long)i * n1 + k) * S], a[((long long)i * n1 + k + 1) * S]);
+    }
+    if (dinv && q < N) {
+      const int i = (int)(q / m) + 1, j = (int)(q % m) + 1;
+      const long long c = (long long)i * n1 + j;
+      const double ac = a[c * S];
+      const double tw = harm(a[(c - n1) * S], ac);
+      const double te = harm(ac, a[(c + n1) * S]);
+      double ts = a_y, tn = a_y;
+      if (a2_same) {
+        ts = harm(a[(c - 1) * S], ac);
+        tn = harm(ac, a[(c + 1) * S]);
+      }
+      const double diag = __dadd_rn(__dadd_rn(__dadd_rn(tw, te), ts), tn);
+      dinv[((size_t)g * N + q) * S + s] = __ddiv_rn(1.0, diag);
+    }
+  }
+}
+
 // ===========================================================================
 // Jacobi inverse diagonal (ensemble.py:130-137,179-183).  The last diagonal
 // entry of a row wins (numpy fancy assignment), an absent one reads 0.

@@ -25,6 +25,70 @@ struct BandHint {
   int padded;
 };
 
+// Face storage of the 2D 5-point FV operator (fv2d.py contract; assembly in
+// assemble_fv2d_kernel).  Every CSR value of a row is a face transmissibility
+// (off-diagonals -T, diagonal ((Tw + Te) + Ts) + Tn), and each interior face
+// is shared by two rows, so the operator is stored once per face and the
+// SpMV re-derives the row in registers: 1 stream (2 with a random y
+// coefficient) instead of the 5 value streams of CSR, same products in the
+// same CSR column order - bit-identical to the CSR SpMV of the same matrix.
+//   tx [G][(m+1)*m][S]  face f*m + (j-1) between cell rows f and f+1 (f = 0..m)
+//                       at column j: row (i, j) has Tw = tx[row], Te = tx[row+m]
+//   ty [G][m*(m+1)][S]  face (i-1)*(m+1) + k between columns k and k+1 of row i:
+//                       Ts = ty[row + i - 1], Tn = ty[row + i]; nullptr = a_y
+// (row = (i-1)*m + (j-1), cells 1-based; both arrays hold (m+1)*m faces.)
+struct Fv2dOp {
+  int m;
+  const double* tx;
+  const double* ty;
+  double a_y;
+};
+
+// Ap of one row for lanes [lo, lo+V) of group g; p_g = p + g*N*S + lo.
+// P_CG: load p through L2 only (persistent kernel).  Also returns p[row].
+// In-group offsets are 32-bit: the ABI requires (N + m) * S < 2^31.
+template <int V, bool P_CG>
+__device__ __forceinline__ void fv2d_row(const Fv2dOp& op, long long N, int S, int g, int lo,
+                                         long long row_ll, const double* __restrict__ p_g,
+                                         double (&y)[V], double (&pc)[V]) {
+  const int m = op.m, row = (int)row_ll;
+  const int i0 = row / m, j0 = row - i0 * m;  // 0-based cell
+  const size_t fo = (size_t)g * (N + m) * S + lo;
+  const double* txg = op.tx + fo;
+  double tw[V], te[V], ts[V], tn[V], pw[V], ps[V], pn[V], pe[V];
+  ldgv<V>(txg + row * S, tw);
+  ldgv<V>(txg + (row + m) * S, te);
+  if (op.ty) {
+    const double* tyg = op.ty + fo;
+    ldgv<V>(tyg + (row + i0) * S, ts);
+    ldgv<V>(tyg + (row + i0 + 1) * S, tn);
+  } else {
+#pragma unroll
+    for (int j = 0; j < V; ++j) ts[j] = tn[j] = op.a_y;
+  }
+  auto ldp = [&](int r, double (&o)[V]) {
+    if constexpr (P_CG) ldcgv<V>(p_g + r * S, o);
+    else ldgv<V>(p_g + r * S, o);
+  };
+  const bool w = i0 > 0, s = j0 > 0, n = j0 < m - 1, e = i0 < m - 1;
+  if (w) ldp(row - m, pw);
+  if (s) ldp(row - 1, ps);
+  ldp(row, pc);
+  if (n) ldp(row + 1, pn);
+  if (e) ldp(row + m, pe);
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    const double d = __dadd_rn(__dadd_rn(__dadd_rn(tw[j], te[j]), ts[j]), tn[j]);
+    double acc = 0.0;
+    if (w) acc = __dadd_rn(acc, __dmul_rn(-tw[j], pw[j]));
+    if (s) acc = __dadd_rn(acc, __dmul_rn(-ts[j], ps[j]));
+    acc = __dadd_rn(acc, __dmul_rn(d, pc[j]));
+    if (n) acc = __dadd_rn(acc, __dmul_rn(-tn[j], pn[j]));
+    if (e) acc = __dadd_rn(acc, __dmul_rn(-te[j], pe[j]));
+    y[j] = acc;
+  }
+}
+
 // Per-lane / per-group solver state living in device memory (ctx scratch), so
 // the whole PCG loop - alpha, beta, freezing, convergence, termination - is
 // decided on the device.  Lane index l = g*S + s.
@@ -60,6 +124,9 @@ __global__ void kl_table_kernel(const double* modes, int P, int M, const double*
 __global__ void assemble_fv2d_kernel(int n, int G, int S, const double* a_nodes, double a_y,
                                      int a2_same, const int* row_offsets, double* vals,
                                      double* dinv);
+__global__ void assemble_fv2d_faces_kernel(int n, int G, int S, const double* a_nodes,
+                                           int a2_same, double a_y, double* tx, double* ty,
+                                           double* dinv);
 __global__ void jacobi_dinv_kernel(long long N, int S, int G, long long nnz, const int* ro,
                                    const int* ci, const double* vals, double* dinv, int* status,
                                    int raw);
@@ -85,6 +152,10 @@ void launch_pcg_init(const Geo& geo, int G, cudaStream_t s, long long N, const P
 void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long long nnz,
                      const PcgState& st, const int* ro, const int* ci, const double* vals,
                      const double* p, double* ap, const BandHint* bands);
+void launch_spmv_fv2d(const Geo& geo, int G, cudaStream_t s, long long N, const Fv2dOp& op,
+                      const double* x, double* y);
+void launch_pcg_spmv_fv2d(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,
+                          const Fv2dOp& op, const double* p, double* ap);
 void launch_pcg_update(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,
                        const double* dinv, int maxit, double* r, const double* ap);
 void launch_pcg_dir(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,
@@ -105,7 +176,8 @@ int persistent_blocks(const Geo& geo, int G);
 int persistent_cluster_size(const Geo& geo);
 cudaError_t launch_pcg_persistent(const Geo& geo, int G, int blocks, bool cluster, cudaStream_t s,
                                   long long N, long long nnz, const PcgState& st, const int* ro,
-                                  const int* ci, const double* vals, const double* rhs,
+                                  const int* ci, const double* vals, const Fv2dOp& fv,
+                                  const double* rhs,
                                   double rhs_const, const double* dinv, double tol, int maxit,
                                   double* x, double* r, double* p, double* ap, double* partA,
                                   double* partB, unsigned* bar_count, unsigned* bar_gen,

@@ -269,6 +269,117 @@ __global__ void __launch_bounds__(256) pcg_spmv_kernel(long long N, long long nn
   }
 }
 
+// Face-form FV2D operator (Fv2dOp): same reduction chunks and state updates
+// as pcg_spmv_kernel, the row's Ap re-derived from the faces (fv2d_row).
+// Chunks are reduced in batches of up to kFaceBatch (reduce_lanes_batch: one
+// tree and one ticket per batch, same bits as per-chunk reduce_lanes).
+constexpr int kFaceBatch = 4;
+
+template <int V>
+__global__ void __launch_bounds__(256, 4) pcg_spmv_fv2d_kernel(long long N, Geo geo, PcgState st,
+                                                            Fv2dOp op,
+                                                            const double* __restrict__ p,
+                                                            double* __restrict__ ap) {
+  extern __shared__ double red[];
+  const int g = blockIdx.y, t = threadIdx.x;
+  if (st.done[g] != kRunning) return;
+  const int sl = t % geo.Lp, rr = t / geo.Lp, S = geo.S, R = geo.R, m = op.m;
+  const int n = (int)N, B = gridDim.x, T = geo.T;
+  const size_t base = (size_t)g * N * S + V * sl;
+  const double* pg = p + base;
+  double* apg = ap + base;
+  const size_t fo = (size_t)g * (N + m) * S + V * sl;
+  const double* txg = op.tx + fo;
+  const double* tyg = op.ty ? op.ty + fo : nullptr;
+  const int ct = (int)geo.chunk_tiles;
+  for (int c0 = blockIdx.x; c0 < geo.chunks; c0 += kFaceBatch * B) {
+    int nk = (geo.chunks - 1 - c0) / B + 1;
+    if (nk > kFaceBatch) nk = kFaceBatch;
+    for (int k = 0; k < nk; ++k) {
+      const int chunk = c0 + k * B;
+      double acc[V] = {};
+      if (sl < geo.L) {
+        int row = chunk * ct * R + rr;  // first row of this thread in the chunk
+        int rend = (chunk + 1) * ct * R;
+        if (rend > n) rend = n;
+        int i0 = row / m, j0 = row - i0 * m;
+        for (; row < rend; row += R) {
+          double tw[V], te[V], ts[V], tn[V], pw[V], ps[V], pc[V], pn[V], pe[V];
+          ldgv<V>(txg + row * S, tw);
+          ldgv<V>(txg + (row + m) * S, te);
+          if (tyg) {
+            ldgv<V>(tyg + (row + i0) * S, ts);
+            ldgv<V>(tyg + (row + i0 + 1) * S, tn);
+          } else {
+#pragma unroll
+            for (int j = 0; j < V; ++j) ts[j] = tn[j] = op.a_y;
+          }
+          const bool w = i0 > 0, s = j0 > 0, nn = j0 < m - 1, e = i0 < m - 1;
+          if (w) ldgv<V>(pg + (row - m) * S, pw);
+          if (s) ldgv<V>(pg + (row - 1) * S, ps);
+          ldgv<V>(pg + row * S, pc);
+          if (nn) ldgv<V>(pg + (row + 1) * S, pn);
+          if (e) ldgv<V>(pg + (row + m) * S, pe);
+          double y[V];
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            const double d = __dadd_rn(__dadd_rn(__dadd_rn(tw[j], te[j]), ts[j]), tn[j]);
+            double a = 0.0;
+            if (w) a = __dadd_rn(a, __dmul_rn(-tw[j], pw[j]));
+            if (s) a = __dadd_rn(a, __dmul_rn(-ts[j], ps[j]));
+            a = __dadd_rn(a, __dmul_rn(d, pc[j]));
+            if (nn) a = __dadd_rn(a, __dmul_rn(-tn[j], pn[j]));
+            if (e) a = __dadd_rn(a, __dmul_rn(-te[j], pe[j]));
+            y[j] = a;
+            acc[j] = __fma_rn(pc[j], a, acc[j]);
+          }
+          stv<V>(apg + row * S, y);
+          j0 += R;
+          while (j0 >= m) {
+            j0 -= m;
+            ++i0;
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < V; ++j) red[(k * V + j) * T + t] = acc[j];
+    }
+    if (!reduce_lanes_batch<V>(red, st.part, st.ticket, g, c0, B, nk, geo)) continue;
+    if (t < geo.L) {
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const size_t l = (size_t)g * S + V * t + j;
+        const double pap = red[j * geo.T + t];
+        const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
+        st.frozen[l] = fr;
+        st.alpha[l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
+      }
+    }
+    if (t == 0) st.it[g] += 1;
+  }
+}
+
+template <int V>
+__global__ void __launch_bounds__(256) spmv_fv2d_kernel(long long N, Geo geo, Fv2dOp op,
+                                                        const double* __restrict__ x,
+                                                        double* __restrict__ y) {
+  const int g = blockIdx.y, t = threadIdx.x;
+  const int sl = t % geo.Lp, rr = t / geo.Lp, S = geo.S;
+  if (sl >= geo.L) return;
+  const size_t base = (size_t)g * N * S + V * sl;
+  for (int chunk = blockIdx.x; chunk < geo.chunks; chunk += gridDim.x) {
+    const ChunkRows cr = chunk_tiles(geo, chunk);
+    for (long long tile = cr.t0; tile < cr.t1; ++tile) {
+      const long long row = tile * geo.R + rr;
+      if (row < N) {
+        double acc[V], xc[V];
+        fv2d_row<V, false>(op, N, S, g, V * sl, row, x + base, acc, xc);
+        stv<V>(y + base + row * S, acc);
+      }
+    }
+  }
+}
+
 template <int V>
 __global__ void __launch_bounds__(256, 3) pcg_update_kernel(long long N, Geo geo, PcgState st,
                                                          const double* __restrict__ dinv,
@@ -498,8 +609,8 @@ __device__ __forceinline__ int block_tile_count(const Geo& geo) {
   return (int)((nb - 1) * geo.chunk_tiles + last_tiles);
 }
 
-template <int ML>
-__global__ void __launch_bounds__(256, 3) pcg_spmv_tma_kernel(long long N, long long nnz, Geo geo,
+template <int ML, int NST = kStages, int MINB = 3>
+__global__ void __launch_bounds__(256, MINB) pcg_spmv_tma_kernel(long long N, long long nnz, Geo geo,
                                                            PcgState st,
                                                            const int* __restrict__ ro,
                                                            const int* __restrict__ ci,
@@ -515,12 +626,12 @@ __global__ void __launch_bounds__(256, 3) pcg_spmv_tma_kernel(long long N, long 
   const double* pg_all = p + (size_t)g * N * S;
   const size_t stage_doubles = (size_t)R * ML * S;
   double* stage = red + (size_t)V * geo.T;  // after the reduction scratch
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stage + kStages * stage_doubles);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage + NST * stage_doubles);
   const double* vg = vals + (size_t)g * nnz * S;
   const int n_tiles = block_tile_count(geo);
 
   if (t == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < NST; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -532,10 +643,10 @@ __global__ void __launch_bounds__(256, 3) pcg_spmv_tma_kernel(long long N, long 
     const long long r1 = r0 + R < N ? r0 + R : N;
     const int k0 = __ldg(&ro[r0]), k1 = __ldg(&ro[r1]);
     const uint32_t bytes = (uint32_t)(k1 - k0) * (uint32_t)S * 8u;
-    uint64_t* bar = &bars[i % kStages];
+    uint64_t* bar = &bars[i % NST];
     fence_proxy_async();
     mbar_expect_tx(bar, bytes);
-    if (bytes) bulk_g2s(stage + (size_t)(i % kStages) * stage_doubles, vg + (size_t)k0 * S, bytes, bar);
+    if (bytes) bulk_g2s(stage + (size_t)(i % NST) * stage_doubles, vg + (size_t)k0 * S, bytes, bar);
     // banded graph: pull the p rows this tile will gather into L2 ahead of use
     // (the +m band is read here for the first time - a DRAM miss otherwise)
 #pragma unroll
@@ -549,7 +660,7 @@ __global__ void __launch_bounds__(256, 3) pcg_spmv_tma_kernel(long long N, long 
     }
   };
   if (t == 0) {
-    for (int i = 0; i < kStages && i < n_tiles; ++i) issue(i);
+    for (int i = 0; i < NST && i < n_tiles; ++i) issue(i);
   }
 
   const int sl = t % geo.Lp, rr = t / geo.Lp;
@@ -559,13 +670,13 @@ __global__ void __launch_bounds__(256, 3) pcg_spmv_tma_kernel(long long N, long 
   for (int i = 0; i < n_tiles; ++i) {
     int chunk;
     const long long tile = block_tile(geo, i, chunk);
-    mbar_wait(&bars[i % kStages], (uint32_t)((i / kStages) & 1));
+    mbar_wait(&bars[i % NST], (uint32_t)((i / NST) & 1));
     if (sl < geo.L) {
       const long long row = tile * R + rr;
       if (row < N) {
         const int kt0 = __ldg(&ro[tile * R]);
         const int k0 = __ldg(&ro[row]), k1 = __ldg(&ro[row + 1]);
-        const double* sv = stage + (size_t)(i % kStages) * stage_doubles +
+        const double* sv = stage + (size_t)(i % NST) * stage_doubles +
                            (size_t)(k0 - kt0) * S + V * sl;
         const int len = k1 - k0;
         int c[ML];
@@ -591,8 +702,8 @@ __global__ void __launch_bounds__(256, 3) pcg_spmv_tma_kernel(long long N, long 
         for (int j = 0; j < V; ++j) acc[0][j] = __fma_rn(pv[j], y[j], acc[0][j]);
       }
     }
-    __syncthreads();  // stage (i % kStages) fully consumed
-    if (t == 0 && i + kStages < n_tiles) issue(i + kStages);
+    __syncthreads();  // stage (i % NST) fully consumed
+    if (t == 0 && i + NST < n_tiles) issue(i + NST);
     const bool chunk_end = ((i + 1) % geo.chunk_tiles == 0) || (tile == geo.tiles - 1);
     if (chunk_end) {
       if (reduce_lanes<1, V>(acc, red, st.part, st.ticket, g, chunk, geo)) {
@@ -1345,22 +1456,22 @@ void launch_pcg_init(const Geo& geo, int G, cudaStream_t s, long long N, const P
                  rhs_const, dinv, tol, maxit, x, r, p);
 }
 
-template <int ML>
+template <int ML, int NST = kStages, int MINB = 3>
 static void launch_spmv_tma(const Geo& gl, int G, cudaStream_t s, long long N, long long nnz,
                             const PcgState& st, const int* ro, const int* ci, const double* vals,
                             const double* p, double* ap, const BandHint* bands) {
   const size_t smem = (size_t)2 * gl.T * sizeof(double) +
-                      (size_t)kStages * gl.R * ML * gl.S * sizeof(double) + kStages * 8;
+                      (size_t)NST * gl.R * ML * gl.S * sizeof(double) + NST * 8;
   static size_t configured = 0;
   if (smem > configured) {
-    cudaFuncSetAttribute(pcg_spmv_tma_kernel<ML>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    cudaFuncSetAttribute(pcg_spmv_tma_kernel<ML, NST, MINB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = smem;
   }
   BandHint bh{};  // L2 prefetch of the p bands (p must be 16-byte aligned)
   if (bands && (reinterpret_cast<uintptr_t>(p) & 15) == 0 && gl.S % 2 == 0) bh = *bands;
-  pcg_spmv_tma_kernel<ML><<<dim3(gl.B, G), gl.T, smem, s>>>(N, nnz, gl, st, ro, ci, vals, p, ap,
-                                                            bh);
+  pcg_spmv_tma_kernel<ML, NST, MINB><<<dim3(gl.B, G), gl.T, smem, s>>>(N, nnz, gl, st, ro, ci,
+                                                                       vals, p, ap, bh);
 }
 
 template <int ML>
@@ -1448,6 +1559,18 @@ static void launch_spmv_band(const Geo& gl, int G, cudaStream_t s, long long N, 
                                                              bh);
 }
 
+void launch_spmv_fv2d(const Geo& geo, int G, cudaStream_t s, long long N, const Fv2dOp& op,
+                      const double* x, double* y) {
+  const Geo gl = with_groups(geo, G);
+  UQG_DISPATCH_V(gl, spmv_fv2d_kernel, dim3(gl.B, G), 0, s, N, gl, op, x, y);
+}
+
+void launch_pcg_spmv_fv2d(const Geo& gl, int G, cudaStream_t s, long long N, const PcgState& st,
+                          const Fv2dOp& op, const double* p, double* ap) {
+  UQG_DISPATCH_V(gl, pcg_spmv_fv2d_kernel, dim3(gl.B, G), red_bytes(gl, kFaceBatch), s, N, gl, st,
+                 op, p, ap);
+}
+
 void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long long nnz,
                      const PcgState& st, const int* ro, const int* ci, const double* vals,
                      const double* p, double* ap, const BandHint* bands) {
@@ -1483,6 +1606,16 @@ void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long lo
         launch_spmv_tma_meta<5>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap);
       else
         launch_spmv_tma_meta<8>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap);
+    } else if (mode == 6) {  // 2 stages, 4 CTAs per SM
+      if (gl.maxrow <= 5)
+        launch_spmv_tma<5, 2, 4>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
+      else
+        launch_spmv_tma<8, 2, 4>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
+    } else if (mode == 7) {  // 4 stages, 2 CTAs per SM
+      if (gl.maxrow <= 5)
+        launch_spmv_tma<5, 4, 2>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
+      else
+        launch_spmv_tma<8, 4, 2>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
     } else if (gl.maxrow <= 5) {
       launch_spmv_tma<5>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
     } else {

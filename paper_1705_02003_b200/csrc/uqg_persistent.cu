@@ -29,17 +29,6 @@ namespace {
 
 constexpr long long kBarrierTimeout = 1LL << 35;  // ~17 s at 1.9 GHz: abort, never hang
 
-template <int V>
-__device__ __forceinline__ void ldcgv(const double* p, double (&o)[V]) {
-  if constexpr (V == 2) {
-    const double2 t = __ldcg(reinterpret_cast<const double2*>(p));
-    o[0] = t.x;
-    o[1] = t.y;
-  } else {
-    o[0] = __ldcg(p);
-  }
-}
-
 // Group-local barrier over the nb blocks of group g.
 __device__ bool group_sync(unsigned* count, unsigned* gen, unsigned nb, int* abort_flag) {
   __shared__ int s_abort;
@@ -152,7 +141,8 @@ struct LaneSmem {
 template <int V, bool CL>
 __global__ void __launch_bounds__(256) pcg_persistent_kernel(
     long long N, long long nnz, Geo geo, PcgState st, const int* __restrict__ ro,
-    const int* __restrict__ ci, const double* __restrict__ vals, const double* __restrict__ rhs,
+    const int* __restrict__ ci, const double* __restrict__ vals, Fv2dOp fv,
+    const double* __restrict__ rhs,
     double rhs_const, const double* __restrict__ dinv, double tol, int maxit,
     double* __restrict__ x, double* __restrict__ r, double* __restrict__ p,
     double* __restrict__ ap, double* partA, double* partB, unsigned* bar_count, unsigned* bar_gen,
@@ -174,7 +164,7 @@ __global__ void __launch_bounds__(256) pcg_persistent_kernel(
   unsigned* cnt = bar_count + g;
   unsigned* gen = bar_gen + g;
   const size_t base = (size_t)g * N * S + V * sl;
-  const double* vg = vals + (size_t)g * nnz * S + V * sl;
+  const double* vg = vals ? vals + (size_t)g * nnz * S + V * sl : nullptr;
 
   // ---- init: x = 0, r = b, p = z, partials b.b and r.z
   for (int chunk = blockIdx.x; chunk < C; chunk += nb) {
@@ -250,20 +240,23 @@ __global__ void __launch_bounds__(256) pcg_persistent_kernel(
         for (long long tile = t0; tile < t1; ++tile) {
           const long long row = tile * geo.R + rr;
           if (row >= N) continue;
-          const int k0 = __ldg(&ro[row]), k1 = __ldg(&ro[row + 1]);
-          double y[V];
+          double y[V], pv[V];
+          if (fv.tx) {
+            fv2d_row<V, true>(fv, N, S, g, V * sl, row, p + base, y, pv);
+          } else {
+            const int k0 = __ldg(&ro[row]), k1 = __ldg(&ro[row + 1]);
 #pragma unroll
-          for (int j = 0; j < V; ++j) y[j] = 0.0;
-          for (int k = k0; k < k1; ++k) {
-            double a[V], b[V];
-            ldgv<V>(vg + (size_t)k * S, a);
-            ldcgv<V>(p + base + (size_t)__ldg(&ci[k]) * S, b);
+            for (int j = 0; j < V; ++j) y[j] = 0.0;
+            for (int k = k0; k < k1; ++k) {
+              double a[V], b[V];
+              ldgv<V>(vg + (size_t)k * S, a);
+              ldcgv<V>(p + base + (size_t)__ldg(&ci[k]) * S, b);
 #pragma unroll
-            for (int j = 0; j < V; ++j) y[j] = __dadd_rn(y[j], __dmul_rn(a[j], b[j]));
+              for (int j = 0; j < V; ++j) y[j] = __dadd_rn(y[j], __dmul_rn(a[j], b[j]));
+            }
+            ldcgv<V>(p + base + row * S, pv);
           }
           stv<V>(ap + base + row * S, y);
-          double pv[V];
-          ldcgv<V>(p + base + row * S, pv);
 #pragma unroll
           for (int j = 0; j < V; ++j) acc[0][j] = __fma_rn(pv[j], y[j], acc[0][j]);
         }
@@ -470,14 +463,16 @@ int persistent_blocks(const Geo& geo, int G) {
 
 cudaError_t launch_pcg_persistent(const Geo& geo, int G, int blocks, bool cluster, cudaStream_t s,
                                   long long N, long long nnz, const PcgState& st, const int* ro,
-                                  const int* ci, const double* vals, const double* rhs,
+                                  const int* ci, const double* vals, const Fv2dOp& fv,
+                                  const double* rhs,
                                   double rhs_const, const double* dinv, double tol, int maxit,
                                   double* x, double* r, double* p, double* ap, double* partA,
                                   double* partB, unsigned* bar_count, unsigned* bar_gen,
                                   int* abort_flag) {
   Geo gl = geo;
   gl.B = blocks;
-  void* args[] = {&N,   &nnz,       &gl,   (void*)&st, &ro,    &ci,    &vals,
+  Fv2dOp op = fv;
+  void* args[] = {&N,   &nnz,       &gl,   (void*)&st, &ro,    &ci,    &vals,  &op,
                   &rhs, &rhs_const, &dinv, &tol,       &maxit, &x,     &r,
                   &p,   &ap,        &partA, &partB,    &bar_count, &bar_gen, &abort_flag};
   const size_t smem = persistent_smem(gl);

@@ -262,6 +262,26 @@ def _as_matrix(mat) -> EnsembleCsrMatrix:
 def run_pcg(N, nnz, S, G, d_rowptr, d_col, d_vals, d_rhs, rhs_const, d_dinv, tol, maxit,
             record_history=False, max_row_len=0):
     """Batched device PCG over G groups; returns device/host result pieces."""
+    def call(*tail):
+        return _lib.load().uqg_pcg(
+            _lib.ctx(), N, nnz, int(max_row_len), S, G, _lib.ptr(d_rowptr), _lib.ptr(d_col),
+            _lib.ptr(d_vals), _lib.ptr(d_rhs), float(rhs_const), _lib.ptr(d_dinv), float(tol),
+            int(maxit), *tail)
+    return _pcg_loop(call, N, S, G, maxit, record_history)
+
+
+def run_pcg_fv2d(n_cells, S, G, d_tx, d_ty, a_y, d_rhs, rhs_const, d_dinv, tol, maxit,
+                 record_history=False):
+    """``run_pcg`` on the face form of the 2D FV operator (``uqg_pcg_fv2d``):
+    same results bit for bit, a third of the SpMV traffic."""
+    def call(*tail):
+        return _lib.load().uqg_pcg_fv2d(
+            _lib.ctx(), n_cells, S, G, _lib.ptr(d_tx), _lib.ptr(d_ty), float(a_y), _lib.ptr(d_rhs),
+            float(rhs_const), _lib.ptr(d_dinv), float(tol), int(maxit), *tail)
+    return _pcg_loop(call, (n_cells - 1) ** 2, S, G, maxit, record_history)
+
+
+def _pcg_loop(call, N, S, G, maxit, record_history):
     torch = _lib._torch()
     dev = _lib.device()
     x = torch.empty((G * N * S,), dtype=torch.float64, device=dev)
@@ -273,11 +293,9 @@ def run_pcg(N, nnz, S, G, d_rowptr, d_col, d_vals, d_rhs, rhs_const, d_dinv, tol
     while True:
         hist = np.empty(((cap + 1) * G * S,)) if record_history else None
         rows = ctypes.c_int(0)
-        rc = _lib.load().uqg_pcg(
-            _lib.ctx(), N, nnz, int(max_row_len), S, G, _lib.ptr(d_rowptr), _lib.ptr(d_col), _lib.ptr(d_vals),
-            _lib.ptr(d_rhs), float(rhs_const), _lib.ptr(d_dinv), float(tol), int(maxit),
-            _lib.ptr(x), _lib.ptr(iters), _lib.ptr(conv), _lib.ptr(frz), _lib.ptr(ens),
-            hist.ctypes.data if hist is not None else None, cap, ctypes.byref(rows), _lib.stream())
+        rc = call(_lib.ptr(x), _lib.ptr(iters), _lib.ptr(conv), _lib.ptr(frz), _lib.ptr(ens),
+                  hist.ctypes.data if hist is not None else None, cap, ctypes.byref(rows),
+                  _lib.stream())
         if rc == _lib.UQG_ECAPACITY and cap < maxit:
             cap = int(maxit)
             continue

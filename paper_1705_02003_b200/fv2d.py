@@ -133,6 +133,33 @@ def assemble_values(mesh: StructuredMesh2D, a_nodes, G: int, S: int, a_y: float,
     return vals, dinv
 
 
+def n_faces(mesh: StructuredMesh2D) -> int:
+    """Face slots per group of the face form: (m+1)*m (x-faces; y-faces alike)."""
+    m = mesh.cells - 1
+    return (m + 1) * m
+
+
+def assemble_faces(mesh: StructuredMesh2D, a_nodes, G: int, S: int, a_y: float,
+                   a2: str = "const", tx=None, ty=None, dinv=None):
+    """Face form of the same operator (``uqg_assemble_fv2d_faces``): device
+    tx [G][(m+1)m][S], ty (None unless a2 == "same"), dinv [G][N][S]."""
+    if a2 not in ("const", "same"):
+        raise FemError(f"unknown second-direction mode {a2!r}")
+    F = n_faces(mesh)
+    if tx is None:
+        tx = a_nodes.new_empty((G * F * S,))
+    if a2 == "same" and ty is None:
+        ty = a_nodes.new_empty((G * F * S,))
+    if a2 != "same":
+        ty = None
+    if dinv is None:
+        dinv = a_nodes.new_empty((G * mesh.n_dofs * S,))
+    _lib.call("uqg_assemble_fv2d_faces", _lib.ctx(), mesh.cells, G, S, _lib.ptr(a_nodes),
+              float(a_y), int(a2 == "same"), _lib.ptr(tx), _lib.ptr(ty), _lib.ptr(dinv),
+              _lib.stream(), invalid=FemError)
+    return tx, ty, dinv
+
+
 def assemble(mesh: StructuredMesh2D, field, samples, mode_vals=None, a2: str = "const"
              ) -> AssembledEnsembleSystem:
     """Width-S ensemble system for the sample rows, assembled on the GPU.

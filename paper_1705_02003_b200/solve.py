@@ -25,10 +25,11 @@ from dataclasses import dataclass, field as dc_field
 import numpy as np
 
 from . import _lib
-from .ensemble import run_pcg
+from .ensemble import run_pcg, run_pcg_fv2d
 from .errors import FemError
 from .fem3d import StructuredMesh3D
-from .fv2d import FieldTables, StructuredMesh2D, assemble_values, kl_nodes
+from .fv2d import (FieldTables, StructuredMesh2D, assemble_faces, assemble_values, kl_nodes,
+                   n_faces)
 
 __all__ = ["LevelSolveResult", "EnsembleSolver", "EnsembleSolver2D", "EnsembleSolver3D",
            "FV2DOperator", "FEM3DOperator"]
@@ -50,11 +51,17 @@ class LevelSolveResult:
 # operators: how a group's coefficient and matrix are built on the device
 
 class FV2DOperator:
-    """BASELINE.json's 2D 5-point FV operator (``fv2d.py``)."""
+    """BASELINE.json's 2D 5-point FV operator (``fv2d.py``).
+
+    ``faces`` (default; ``UQG_FV2D_FACES=0`` selects CSR): the solve stores
+    the operator once per face (``uqg_assemble_fv2d_faces``) and runs
+    ``uqg_pcg_fv2d`` - the same matrix and the same bits as the CSR path, with
+    the SpMV streaming 1-2 face arrays instead of 5 value arrays.
+    """
 
     max_row_len = 5
 
-    def __init__(self, field, cells: int, a2: str = "const"):
+    def __init__(self, field, cells: int, a2: str = "const", faces: bool | None = None):
         if field.dim != 2:
             raise FemError("the 2D operator needs a 2D field")
         self.field, self.a2 = field, a2
@@ -62,6 +69,21 @@ class FV2DOperator:
         self.tables = FieldTables(field, self.mesh)
         self.n_dofs, self.nnz, self.n_coef = self.mesh.n_dofs, self.mesh.nnz, self.mesh.n_nodes
         self.rhs_const = self.mesh.h * self.mesh.h
+        if faces is None:
+            faces = os.environ.get("UQG_FV2D_FACES", "1") != "0"
+        self.faces = bool(faces)
+        self.n_faces = n_faces(self.mesh)
+
+    @property
+    def n_op(self) -> int:
+        """Operator doubles per group and lane (CSR values or faces)."""
+        if self.faces:
+            return self.n_faces * (2 if self.a2 == "same" else 1)
+        return self.nnz
+
+    def assemble_faces(self, a, G, S, tx, ty, dinv):
+        return assemble_faces(self.mesh, a, G, S, self.field.a_y, self.a2, tx=tx, ty=ty,
+                              dinv=dinv)
 
     def graph(self):
         return self.mesh.device()
@@ -130,7 +152,8 @@ class EnsembleSolver:
     # -- memory planning ----------------------------------------------------
     def bytes_per_group(self, S: int) -> int:
         o = self.op
-        per = 8 * S * (o.nnz + 2 * o.n_dofs + o.n_coef)      # vals, dinv, x, coefficient
+        n_op = getattr(o, "n_op", o.nnz)
+        per = 8 * S * (n_op + 2 * o.n_dofs + o.n_coef)       # operator, dinv, x, coefficient
         per += _lib.load().uqg_pcg_workspace_bytes(o.n_dofs, o.nnz, S, 1)  # r, p, Ap, ...
         return int(per)
 
@@ -180,9 +203,19 @@ class EnsembleSolver:
         torch = _lib._torch()
         o = self.op
         a = self._buf("a", G * o.n_coef * S, torch.float64)
-        vals = self._buf("vals", G * o.nnz * S, torch.float64)
         dinv = self._buf("dinv", G * o.n_dofs * S, torch.float64)
         o.coefficients(d_samples, lane_ids, G, S, a)
+        if getattr(o, "faces", False):
+            F = o.n_faces
+            tx = self._buf("vals", G * F * S, torch.float64)
+            ty = self._buf("ty", G * F * S, torch.float64) if o.a2 == "same" else None
+            o.assemble_faces(a, G, S, tx, ty, dinv)
+            self._workspace(G, S)
+            x, iters, conv, frz, ens, hist = run_pcg_fv2d(
+                o.mesh.cells, S, G, tx, ty, o.field.a_y, None, o.rhs_const, dinv, self.tol,
+                self.maxit, record_history)
+            return self._finish(x, iters, conv, frz, ens, hist, G, S)
+        vals = self._buf("vals", G * o.nnz * S, torch.float64)
         o.assemble(a, G, S, vals, dinv)
         rowptr, col = o.graph()
         self._workspace(G, S)
@@ -203,6 +236,11 @@ class EnsembleSolver:
         finally:
             if hint:
                 _lib.call("uqg_ctx_set_band_hint", _lib.ctx(), 0, None, None, 0)
+        return self._finish(x, iters, conv, frz, ens, hist, G, S)
+
+    def _finish(self, x, iters, conv, frz, ens, hist, G, S):
+        torch = _lib._torch()
+        o = self.op
         q = torch.empty((G * S,), dtype=torch.float64, device=_lib.device())
         _lib.call("uqg_lane_dot", _lib.ctx(), o.n_dofs, S, G, _lib.ptr(x), _lib.ptr(x), _lib.ptr(q),
                   _lib.stream())
@@ -333,8 +371,8 @@ class EnsembleSolver2D(EnsembleSolver):
 
     def __init__(self, field, cells: int, tol: float = 1e-8, maxit: int = 30000,
                  a2: str = "const", mem_fraction: float = 0.8,
-                 max_groups_per_wave: int | None = None):
-        super().__init__(FV2DOperator(field, cells, a2), tol, maxit, mem_fraction,
+                 max_groups_per_wave: int | None = None, faces: bool | None = None):
+        super().__init__(FV2DOperator(field, cells, a2, faces), tol, maxit, mem_fraction,
                          max_groups_per_wave)
         self.tables, self.a2 = self.op.tables, a2
 

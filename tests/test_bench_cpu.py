@@ -31,3 +31,19 @@ def test_byte_model_matches_survey():
     assert bm["spmv"] == 59688364  # B_spmv at C2 = 59.7 MB
     assert abs(bm["pcg_iter"] - 151.2e6) < 0.1e6  # 151.2 MB
     assert bm["spmv"] + bm["update"] + bm["dir"] == bm["pcg_iter_moved"] < bm["pcg_iter"]
+    assert bm["operator"] == "csr"
+
+
+def test_byte_model_faces():
+    sys.path.insert(0, str(ROOT))
+    import bench
+    from paper_1705_02003_b200.configs import get
+
+    class Op:  # the face-form FV2D operator's byte-relevant attributes
+        faces, n_op = True, 256 * 255
+    cfg = get("C2")
+    bm = bench.bytes_model(cfg, Op())
+    S, N = cfg.ensemble_size, cfg.n_dofs
+    assert bm["operator"] == "fv2d faces"
+    assert bm["spmv"] == 8 * S * (256 * 255) + 16 * S * N
+    assert bm["pcg_iter"] == 8 * S * (256 * 255 + 13 * N)

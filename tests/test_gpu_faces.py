@@ -1,0 +1,96 @@
+"""Face form of the 2D FV operator (uqg_assemble_fv2d_faces / uqg_spmv_fv2d /
+uqg_pcg_fv2d) against the CSR form of the same matrix.
+
+The face form re-derives each CSR row from the face transmissibilities with
+the same products in the same column order, so the bar is bit-identity with
+the CSR path - which the rest of the suite pins to the oracle and to the
+reference's golden outputs (test_gpu_parity.py).
+"""
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_1705_02003_b200 as uq
+from paper_1705_02003_b200 import _lib
+from paper_1705_02003_b200.fv2d import StructuredMesh2D, assemble_faces, assemble_values
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _nodes(rng, cells, G, S):
+    a = np.exp(rng.standard_normal((G, (cells + 1) ** 2, S)))  # positive, lognormal
+    return _lib.to_dev(np.ascontiguousarray(a).ravel())
+
+
+@pytest.mark.parametrize("cells,S,G", [(2, 1, 1), (5, 3, 2), (17, 8, 3), (64, 16, 2),
+                                       (33, 32, 1), (9, 2, 5)])
+@pytest.mark.parametrize("a2", ["const", "same"])
+def test_face_spmv_and_dinv_bitwise_equal_csr(cells, S, G, a2):
+    rng = np.random.default_rng(cells * 100 + S)
+    mesh = StructuredMesh2D(cells)
+    a = _nodes(rng, cells, G, S)
+    a_y = 0.7
+    vals, dinv_csr = assemble_values(mesh, a, G, S, a_y, a2)
+    tx, ty, dinv = assemble_faces(mesh, a, G, S, a_y, a2)
+    assert (ty is None) == (a2 == "const")
+    assert np.array_equal(dinv.cpu().numpy(), dinv_csr.cpu().numpy())
+    N = mesh.n_dofs
+    x = _lib.to_dev(rng.standard_normal(G * N * S))
+    y_csr = x.new_empty(G * N * S)
+    y_fac = x.new_empty(G * N * S)
+    rowptr, col = mesh.device()
+    _lib.call("uqg_spmv", _lib.ctx(), N, mesh.nnz, 5, S, G, _lib.ptr(rowptr), _lib.ptr(col),
+              _lib.ptr(vals), _lib.ptr(x), _lib.ptr(y_csr), _lib.stream())
+    _lib.call("uqg_spmv_fv2d", _lib.ctx(), cells, S, G, _lib.ptr(tx), _lib.ptr(ty), a_y,
+              _lib.ptr(x), _lib.ptr(y_fac), _lib.stream())
+    assert np.array_equal(y_fac.cpu().numpy(), y_csr.cpu().numpy())
+
+
+def test_face_entry_points_validate_arguments():
+    with pytest.raises(uq.EnsembleError):
+        _lib.call("uqg_spmv_fv2d", _lib.ctx(), 1, 1, 1, None, None, 1.0, None, None, None)
+    mesh = StructuredMesh2D(4)
+    a = _nodes(np.random.default_rng(0), 4, 1, 2)
+    tx = a.new_empty(mesh.n_dofs * 4)
+    with pytest.raises(uq.EnsembleError):  # a2_same needs ty
+        _lib.call("uqg_assemble_fv2d_faces", _lib.ctx(), 4, 1, 2, _lib.ptr(a), 1.0, 1,
+                  _lib.ptr(tx), None, None, _lib.stream())
+
+
+_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1705_02003_b200 as uq
+cfg = uq.CONFIGS["C1"]
+f = uq.build_field(**cfg.field_kwargs())
+out = []
+for a2 in ("const", "same"):
+    for faces in (False, True):
+        s = uq.EnsembleSolver2D(f, cfg.cells, cfg.tol, cfg.maxit, a2=a2, faces=faces)
+        ys = np.random.default_rng(5).uniform(-1, 1, (6, cfg.ensemble_size, cfg.n_modes))
+        r = s.solve_groups(ys, record_history=True)
+        h = np.concatenate([np.concatenate(g) for g in r.histories])
+        out.append(np.concatenate([r.iterations.ravel().astype(float), r.qoi.ravel(),
+                                   r.converged.ravel().astype(float), h]))
+np.save(sys.argv[2], np.array(out, dtype=object), allow_pickle=True)
+"""
+
+
+@pytest.mark.parametrize("persistent", ["0", "1", "2"])
+def test_face_pcg_bitwise_equal_csr_pcg(tmp_path, persistent):
+    """Whole batched solves (iterations, QoIs, residual histories) through the
+    launch loop (0), the cooperative (1) and the cluster (2) persistent kernel."""
+    env = dict(os.environ, UQG_PCG_PERSISTENT=persistent)
+    dst = tmp_path / "r.npy"
+    subprocess.run([sys.executable, "-c", _SCRIPT, str(ROOT), str(dst)], env=env, check=True)
+    out = np.load(dst, allow_pickle=True)
+    csr_c, fac_c, csr_s, fac_s = out
+    assert np.array_equal(csr_c, fac_c)
+    assert np.array_equal(csr_s, fac_s)
+    assert not np.array_equal(csr_c, csr_s)  # the random y coefficient does change the solve
