@@ -236,19 +236,20 @@ __device__ bool reduce_lanes(const double (&val)[NV][V], double* red, double* pa
   return true;
 }
 
-// reduce_lanes for NV = 1 over a batch of nk chunks chunk0 + k*stride
-// (k < nk) whose per-thread values the caller has stored in
-// red[(k*V + j)*T + t]: one in-block tree for the whole batch (instead of one
-// per chunk), one ticket add of nk, then the final stage of reduce_lanes.
-// Every partial and the final sum are computed exactly as reduce_lanes<1, V>
-// computes them, so results are bit-identical.  red must hold
-// max(nk, 1) * V * T doubles.
-template <int V>
+// reduce_lanes over a batch of nk chunks chunk0 + k*stride (k < nk) whose
+// per-thread values the caller has stored in red[((k*NV + v)*V + j)*T + t]:
+// one in-block tree for the whole batch (instead of one per chunk), one
+// ticket add of nk, then the final stage of reduce_lanes.  Every partial and
+// the final sums are computed exactly as reduce_lanes<NV, V> computes them,
+// so results are bit-identical (same result layout in red).  red must hold
+// max(nk, 1) * NV * V * T doubles.
+template <int NV, int V>
 __device__ bool reduce_lanes_batch(double* red, double* part, unsigned int* ticket, int g,
                                    int chunk0, int stride, int nk, const Geo& geo) {
+  constexpr int NS = NV * V;
   const int t = threadIdx.x;
   const int T = geo.T, Lp = geo.Lp, R = geo.R, L = geo.L, S = geo.S, C = geo.chunks;
-  const int ns = nk * V;
+  const int ns = nk * NS;
   __syncthreads();
   for (int st = R >> 1; st > 0; st >>= 1) {
     if ((t / Lp) < st) {
@@ -259,8 +260,11 @@ __device__ bool reduce_lanes_batch(double* red, double* part, unsigned int* tick
   if (t < L) {
     for (int k = 0; k < nk; ++k)
 #pragma unroll
-      for (int j = 0; j < V; ++j)
-        part[((size_t)g * C + chunk0 + k * stride) * S + V * t + j] = red[(k * V + j) * T + t];
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+          part[(((size_t)g * C + chunk0 + k * stride) * NV + v) * S + V * t + j] =
+              red[((k * NV + v) * V + j) * T + t];
   }
   __shared__ int s_last;
   __threadfence();
@@ -273,21 +277,24 @@ __device__ bool reduce_lanes_batch(double* red, double* part, unsigned int* tick
   if (!s_last) return false;
   __threadfence();
   const int sl = t % Lp, jr = t / Lp;
-  double acc[V];
+  double acc[NS];
 #pragma unroll
-  for (int v = 0; v < V; ++v) acc[v] = 0.0;
+  for (int v = 0; v < NS; ++v) acc[v] = 0.0;
   if (sl < L) {
 #pragma unroll 4
     for (int cc = jr; cc < C; cc += R) {
 #pragma unroll
-      for (int j = 0; j < V; ++j) acc[j] += __ldcg(&part[((size_t)g * C + cc) * S + V * sl + j]);
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+          acc[v * V + j] += __ldcg(&part[(((size_t)g * C + cc) * NV + v) * S + V * sl + j]);
     }
   }
   __syncthreads();  // the batch's tree values in red[] have been consumed
 #pragma unroll
-  for (int v = 0; v < V; ++v) red[v * T + t] = acc[v];
+  for (int v = 0; v < NS; ++v) red[v * T + t] = acc[v];
   __syncthreads();
-  tree_rows<V>(red, T, Lp, R, t);
+  tree_rows<NS>(red, T, Lp, R, t);
   if (t == 0) ticket[g] = 0u;
   return true;
 }

@@ -271,12 +271,68 @@ __global__ void __launch_bounds__(256) pcg_spmv_kernel(long long N, long long nn
 
 // Face-form FV2D operator (Fv2dOp): same reduction chunks and state updates
 // as pcg_spmv_kernel, the row's Ap re-derived from the faces (fv2d_row).
+// L2 prefetch of the rows [r0, r1) of a [rows][S] array (bulk, async, no
+// completion tracking).  Used for the first-touch +m bands of the face SpMV.
+__device__ __forceinline__ void prefetch_rows_l2(const double* base, int r0, int r1, int S) {
+  if (r1 <= r0) return;
+  const uint32_t bytes = (uint32_t)(r1 - r0) * (uint32_t)S * 8u;
+  if ((reinterpret_cast<uintptr_t>(base + (size_t)r0 * S) & 15) || (bytes & 15)) return;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + (size_t)r0 * S),
+               "r"(bytes)
+               : "memory");
+}
+
+// One row of the face-form operator: loads, then the CSR-order sum.
+template <int V>
+struct FaceRow {
+  double tw[V], te[V], ts[V], tn[V], pw[V], ps[V], pc[V], pn[V], pe[V];
+  bool w, s, n, e;
+  __device__ __forceinline__ void load(const double* __restrict__ txg,
+                                       const double* __restrict__ tyg,
+                                       const double* __restrict__ pg, double a_y, int m, int S,
+                                       int row, int i0, int j0) {
+    ldgv<V>(txg + row * S, tw);
+    ldgv<V>(txg + (row + m) * S, te);
+    if (tyg) {
+      ldgv<V>(tyg + (row + i0) * S, ts);
+      ldgv<V>(tyg + (row + i0 + 1) * S, tn);
+    } else {
+#pragma unroll
+      for (int j = 0; j < V; ++j) ts[j] = tn[j] = a_y;
+    }
+    w = i0 > 0;
+    s = j0 > 0;
+    n = j0 < m - 1;
+    e = i0 < m - 1;
+    if (w) ldgv<V>(pg + (row - m) * S, pw);
+    if (s) ldgv<V>(pg + (row - 1) * S, ps);
+    ldgv<V>(pg + row * S, pc);
+    if (n) ldgv<V>(pg + (row + 1) * S, pn);
+    if (e) ldgv<V>(pg + (row + m) * S, pe);
+  }
+  // y = row of A p (fv2d_row's arithmetic); acc += p[row] * y (fused)
+  __device__ __forceinline__ void apply(double (&y)[V], double (&acc)[V]) const {
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const double d = __dadd_rn(__dadd_rn(__dadd_rn(tw[j], te[j]), ts[j]), tn[j]);
+      double a = 0.0;
+      if (w) a = __dadd_rn(a, __dmul_rn(-tw[j], pw[j]));
+      if (s) a = __dadd_rn(a, __dmul_rn(-ts[j], ps[j]));
+      a = __dadd_rn(a, __dmul_rn(d, pc[j]));
+      if (n) a = __dadd_rn(a, __dmul_rn(-tn[j], pn[j]));
+      if (e) a = __dadd_rn(a, __dmul_rn(-te[j], pe[j]));
+      y[j] = a;
+      acc[j] = __fma_rn(pc[j], a, acc[j]);
+    }
+  }
+};
+
 // Chunks are reduced in batches of up to kFaceBatch (reduce_lanes_batch: one
 // tree and one ticket per batch, same bits as per-chunk reduce_lanes).
 constexpr int kFaceBatch = 4;
 
-template <int V>
-__global__ void __launch_bounds__(256, 4) pcg_spmv_fv2d_kernel(long long N, Geo geo, PcgState st,
+template <int V, int U, bool PF>
+__global__ void __launch_bounds__(256, U == 1 ? 4 : 3) pcg_spmv_fv2d_kernel(long long N, Geo geo, PcgState st,
                                                             Fv2dOp op,
                                                             const double* __restrict__ p,
                                                             double* __restrict__ ap) {
@@ -297,54 +353,48 @@ __global__ void __launch_bounds__(256, 4) pcg_spmv_fv2d_kernel(long long N, Geo 
     if (nk > kFaceBatch) nk = kFaceBatch;
     for (int k = 0; k < nk; ++k) {
       const int chunk = c0 + k * B;
+      if (t == 0 && PF) {  // first-touch (+m) bands of this block's next chunk
+        const int nc = chunk + B;
+        if (nc < geo.chunks) {
+          const int a = nc * ct * R + m, bnd = (int)(N + m);
+          int e = a + ct * R;
+          e = e < bnd ? e : bnd;
+          prefetch_rows_l2(op.tx + (size_t)g * (N + m) * S, a, e, S);
+          if (a < n) prefetch_rows_l2(p + (size_t)g * N * S, a, e < n ? e : n, S);
+        }
+      }
       double acc[V] = {};
       if (sl < geo.L) {
         int row = chunk * ct * R + rr;  // first row of this thread in the chunk
         int rend = (chunk + 1) * ct * R;
         if (rend > n) rend = n;
         int i0 = row / m, j0 = row - i0 * m;
-        for (; row < rend; row += R) {
-          double tw[V], te[V], ts[V], tn[V], pw[V], ps[V], pc[V], pn[V], pe[V];
-          ldgv<V>(txg + row * S, tw);
-          ldgv<V>(txg + (row + m) * S, te);
-          if (tyg) {
-            ldgv<V>(tyg + (row + i0) * S, ts);
-            ldgv<V>(tyg + (row + i0 + 1) * S, tn);
-          } else {
+        for (; row < rend; row += U * R) {
+          FaceRow<V> f[U];
+          bool ok[U];
 #pragma unroll
-            for (int j = 0; j < V; ++j) ts[j] = tn[j] = op.a_y;
+          for (int u = 0; u < U; ++u) {  // all loads of the U rows first
+            ok[u] = row + u * R < rend;
+            if (ok[u]) f[u].load(txg, tyg, pg, op.a_y, m, S, row + u * R, i0, j0);
+            j0 += R;
+            while (j0 >= m) {
+              j0 -= m;
+              ++i0;
+            }
           }
-          const bool w = i0 > 0, s = j0 > 0, nn = j0 < m - 1, e = i0 < m - 1;
-          if (w) ldgv<V>(pg + (row - m) * S, pw);
-          if (s) ldgv<V>(pg + (row - 1) * S, ps);
-          ldgv<V>(pg + row * S, pc);
-          if (nn) ldgv<V>(pg + (row + 1) * S, pn);
-          if (e) ldgv<V>(pg + (row + m) * S, pe);
-          double y[V];
 #pragma unroll
-          for (int j = 0; j < V; ++j) {
-            const double d = __dadd_rn(__dadd_rn(__dadd_rn(tw[j], te[j]), ts[j]), tn[j]);
-            double a = 0.0;
-            if (w) a = __dadd_rn(a, __dmul_rn(-tw[j], pw[j]));
-            if (s) a = __dadd_rn(a, __dmul_rn(-ts[j], ps[j]));
-            a = __dadd_rn(a, __dmul_rn(d, pc[j]));
-            if (nn) a = __dadd_rn(a, __dmul_rn(-tn[j], pn[j]));
-            if (e) a = __dadd_rn(a, __dmul_rn(-te[j], pe[j]));
-            y[j] = a;
-            acc[j] = __fma_rn(pc[j], a, acc[j]);
-          }
-          stv<V>(apg + row * S, y);
-          j0 += R;
-          while (j0 >= m) {
-            j0 -= m;
-            ++i0;
+          for (int u = 0; u < U; ++u) {
+            if (!ok[u]) continue;
+            double y[V];
+            f[u].apply(y, acc);
+            stv<V>(apg + (row + u * R) * S, y);
           }
         }
       }
 #pragma unroll
       for (int j = 0; j < V; ++j) red[(k * V + j) * T + t] = acc[j];
     }
-    if (!reduce_lanes_batch<V>(red, st.part, st.ticket, g, c0, B, nk, geo)) continue;
+    if (!reduce_lanes_batch<1, V>(red, st.part, st.ticket, g, c0, B, nk, geo)) continue;
     if (t < geo.L) {
 #pragma unroll
       for (int j = 0; j < V; ++j) {
@@ -380,6 +430,9 @@ __global__ void __launch_bounds__(256) spmv_fv2d_kernel(long long N, Geo geo, Fv
   }
 }
 
+// chunks per batched reduction in pcg_update (reduce_lanes_batch)
+constexpr int kUpdateBatch = 4;
+
 template <int V>
 __global__ void __launch_bounds__(256, 3) pcg_update_kernel(long long N, Geo geo, PcgState st,
                                                          const double* __restrict__ dinv,
@@ -393,42 +446,52 @@ __global__ void __launch_bounds__(256, 3) pcg_update_kernel(long long N, Geo geo
   double alpha[V];
 #pragma unroll
   for (int j = 0; j < V; ++j) alpha[j] = sl < geo.L ? st.alpha[(size_t)g * S + V * sl + j] : 0.0;
-  for (int chunk = blockIdx.x; chunk < geo.chunks; chunk += gridDim.x) {
-    double acc[2][V] = {};
-    if (sl < geo.L) {
-      const ChunkRows cr = chunk_tiles(geo, chunk);
-      // two tiles per step: all loads of both are issued before any store
-      for (long long tile = cr.t0; tile < cr.t1; tile += 2) {
-        double rv[2][V], av[2][V], dv[2][V];
-        bool ok[2];
-        size_t o[2];
+  const int B = gridDim.x, T = geo.T;
+  for (int c0 = blockIdx.x; c0 < geo.chunks; c0 += kUpdateBatch * B) {
+    int nk = (geo.chunks - 1 - c0) / B + 1;
+    if (nk > kUpdateBatch) nk = kUpdateBatch;
+    for (int k = 0; k < nk; ++k) {
+      const int chunk = c0 + k * B;
+      double acc[2][V] = {};
+      if (sl < geo.L) {
+        const ChunkRows cr = chunk_tiles(geo, chunk);
+        // two tiles per step: all loads of both are issued before any store
+        for (long long tile = cr.t0; tile < cr.t1; tile += 2) {
+          double rv[2][V], av[2][V], dv[2][V];
+          bool ok[2];
+          size_t o[2];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const long long row = (tile + u) * geo.R + rr;
-          ok[u] = tile + u < cr.t1 && row < N;
-          o[u] = base + (ok[u] ? row : 0) * S;
-          if (ok[u]) {
-            ldv<V>(r + o[u], rv[u]);
-            ldv<V>(ap + o[u], av[u]);
-            if (dinv) ldgv<V>(dinv + o[u], dv[u]);
+          for (int u = 0; u < 2; ++u) {
+            const long long row = (tile + u) * geo.R + rr;
+            ok[u] = tile + u < cr.t1 && row < N;
+            o[u] = base + (ok[u] ? row : 0) * S;
+            if (ok[u]) {
+              ldv<V>(r + o[u], rv[u]);
+              ldv<V>(ap + o[u], av[u]);
+              if (dinv) ldgv<V>(dinv + o[u], dv[u]);
+            }
           }
-        }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          if (!ok[u]) continue;
-          double zv[V];
+          for (int u = 0; u < 2; ++u) {
+            if (!ok[u]) continue;
+            double zv[V];
 #pragma unroll
-          for (int j = 0; j < V; ++j) {
-            rv[u][j] = __dsub_rn(rv[u][j], __dmul_rn(alpha[j], av[u][j]));
-            zv[j] = dinv ? __dmul_rn(rv[u][j], dv[u][j]) : rv[u][j];
-            acc[0][j] = __fma_rn(rv[u][j], rv[u][j], acc[0][j]);
-            acc[1][j] = __fma_rn(rv[u][j], zv[j], acc[1][j]);
+            for (int j = 0; j < V; ++j) {
+              rv[u][j] = __dsub_rn(rv[u][j], __dmul_rn(alpha[j], av[u][j]));
+              zv[j] = dinv ? __dmul_rn(rv[u][j], dv[u][j]) : rv[u][j];
+              acc[0][j] = __fma_rn(rv[u][j], rv[u][j], acc[0][j]);
+              acc[1][j] = __fma_rn(rv[u][j], zv[j], acc[1][j]);
+            }
+            stv<V>(r + o[u], rv[u]);
           }
-          stv<V>(r + o[u], rv[u]);
         }
       }
+#pragma unroll
+      for (int v = 0; v < 2; ++v)
+#pragma unroll
+        for (int j = 0; j < V; ++j) red[((k * 2 + v) * V + j) * T + t] = acc[v][j];
     }
-    if (!reduce_lanes<2, V>(acc, red, st.part, st.ticket, g, chunk, geo)) continue;
+    if (!reduce_lanes_batch<2, V>(red, st.part, st.ticket, g, c0, B, nk, geo)) continue;
     __shared__ int s_all, s_bad;
     if (t == 0) {
       s_all = 1;
@@ -607,6 +670,171 @@ __device__ __forceinline__ int block_tile_count(const Geo& geo) {
   long long last_tiles = geo.tiles - (long long)last * geo.chunk_tiles;
   if (last_tiles > geo.chunk_tiles) last_tiles = geo.chunk_tiles;
   return (int)((nb - 1) * geo.chunk_tiles + last_tiles);
+}
+
+// ---------------------------------------------------------------------------
+// Face-form SpMV with per-thread cp.async pipelining.  Each thread gathers the
+// 7 (9 with random y-faces) 16-byte operands of its next NSTG-1 rows straight
+// into its own shared-memory slots (cp.async: no registers held while the
+// loads are in flight), so the loads of several rows overlap without the
+// register cost of the register kernel.  Threads only read their own slots:
+// no block barrier in the pipeline.  Same arithmetic, chunks and batched
+// reduction as pcg_spmv_fv2d_kernel: identical bits.
+
+__device__ __forceinline__ void cp_async_ca(void* dst, const void* src, int bytes) {
+  if (bytes == 16)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int NW>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(NW) : "memory");
+}
+
+template <int V>
+__device__ __forceinline__ void lds_v(const double* p, double (&o)[V]) {
+  if constexpr (V == 2) {
+    const double2 t = *reinterpret_cast<const double2*>(p);
+    o[0] = t.x;
+    o[1] = t.y;
+  } else {
+    o[0] = *p;
+  }
+}
+
+// 0-based cell (i0, j0) of a row: float quotient, corrected (row < m*m).
+__device__ __forceinline__ void cell_of(int row, int m, float inv_m, int& i0, int& j0) {
+  i0 = (int)((float)row * inv_m);
+  j0 = row - i0 * m;
+  if (j0 < 0) {
+    --i0;
+    j0 += m;
+  } else if (j0 >= m) {
+    ++i0;
+    j0 -= m;
+  }
+}
+
+template <int V, int NSTG, bool TY>
+__global__ void __launch_bounds__(256) pcg_spmv_fv2d_async_kernel(long long N, Geo geo,
+                                                                  PcgState st, Fv2dOp op,
+                                                                  const double* __restrict__ p,
+                                                                  double* __restrict__ ap) {
+  constexpr int NSL = TY ? 9 : 7;  // tw te [ts tn] pw ps pc pn pe
+  extern __shared__ __align__(16) double red[];
+  const int g = blockIdx.y, t = threadIdx.x;
+  if (st.done[g] != kRunning) return;
+  const int sl = t % geo.Lp, rr = t / geo.Lp, S = geo.S, R = geo.R, m = op.m;
+  const int n = (int)N, B = gridDim.x, T = geo.T;
+  const bool lane_ok = sl < geo.L;
+  const size_t base = (size_t)g * N * S + V * sl;
+  const double* pg = p + base;
+  double* apg = ap + base;
+  const size_t fo = (size_t)g * (N + m) * S + V * sl;
+  const double* txg = op.tx + fo;
+  const double* tyg = TY ? op.ty + fo : nullptr;
+  double* stg = red + (size_t)kFaceBatch * V * T;
+  const float inv_m = 1.0f / (float)m;
+  const int ct = (int)geo.chunk_tiles;
+  constexpr int BY = 8 * V;
+  auto slot = [&](int s, int k) { return stg + ((size_t)(s * NSL + k) * T + t) * V; };
+  for (int c0 = blockIdx.x; c0 < geo.chunks; c0 += kFaceBatch * B) {
+    int nk = (geo.chunks - 1 - c0) / B + 1;
+    if (nk > kFaceBatch) nk = kFaceBatch;
+    const int items = nk * ct;
+    auto item_row = [&](int q) {
+      const int k = q / ct;
+      const int row = ((c0 + k * B) * ct + (q - k * ct)) * R + rr;
+      return row < n ? row : -1;
+    };
+    auto issue = [&](int q) {
+      if (q < items && lane_ok) {
+        const int row = item_row(q);
+        if (row >= 0) {
+          int i0, j0;
+          cell_of(row, m, inv_m, i0, j0);
+          const int s = q % NSTG;
+          cp_async_ca(slot(s, 0), txg + row * S, BY);
+          cp_async_ca(slot(s, 1), txg + (row + m) * S, BY);
+          if constexpr (TY) {
+            cp_async_ca(slot(s, 2), tyg + (row + i0) * S, BY);
+            cp_async_ca(slot(s, 3), tyg + (row + i0 + 1) * S, BY);
+          }
+          constexpr int P0 = TY ? 4 : 2;
+          if (i0 > 0) cp_async_ca(slot(s, P0), pg + (row - m) * S, BY);
+          if (j0 > 0) cp_async_ca(slot(s, P0 + 1), pg + (row - 1) * S, BY);
+          cp_async_ca(slot(s, P0 + 2), pg + row * S, BY);
+          if (j0 < m - 1) cp_async_ca(slot(s, P0 + 3), pg + (row + 1) * S, BY);
+          if (i0 < m - 1) cp_async_ca(slot(s, P0 + 4), pg + (row + m) * S, BY);
+        }
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int q = 0; q < NSTG - 1; ++q) issue(q);
+    double acc[V] = {};
+    for (int q = 0; q < items; ++q) {
+      issue(q + NSTG - 1);
+      cp_async_wait<NSTG - 1>();
+      const int k = q / ct;
+      if (lane_ok) {
+        const int row = item_row(q);
+        if (row >= 0) {
+          int i0, j0;
+          cell_of(row, m, inv_m, i0, j0);
+          const int s = q % NSTG;
+          constexpr int P0 = TY ? 4 : 2;
+          FaceRow<V> f;
+          lds_v<V>(slot(s, 0), f.tw);
+          lds_v<V>(slot(s, 1), f.te);
+          if constexpr (TY) {
+            lds_v<V>(slot(s, 2), f.ts);
+            lds_v<V>(slot(s, 3), f.tn);
+          } else {
+#pragma unroll
+            for (int j = 0; j < V; ++j) f.ts[j] = f.tn[j] = op.a_y;
+          }
+          f.w = i0 > 0;
+          f.s = j0 > 0;
+          f.n = j0 < m - 1;
+          f.e = i0 < m - 1;
+          if (f.w) lds_v<V>(slot(s, P0), f.pw);
+          if (f.s) lds_v<V>(slot(s, P0 + 1), f.ps);
+          lds_v<V>(slot(s, P0 + 2), f.pc);
+          if (f.n) lds_v<V>(slot(s, P0 + 3), f.pn);
+          if (f.e) lds_v<V>(slot(s, P0 + 4), f.pe);
+          double y[V];
+          f.apply(y, acc);
+          stv<V>(apg + row * S, y);
+        }
+      }
+      if (q - k * ct == ct - 1) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          red[(k * V + j) * T + t] = acc[j];
+          acc[j] = 0.0;
+        }
+      }
+    }
+    if (!reduce_lanes_batch<1, V>(red, st.part, st.ticket, g, c0, B, nk, geo)) continue;
+    if (t < geo.L) {
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const size_t l = (size_t)g * S + V * t + j;
+        const double pap = red[j * geo.T + t];
+        const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
+        st.frozen[l] = fr;
+        st.alpha[l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
+      }
+    }
+    if (t == 0) st.it[g] += 1;
+  }
 }
 
 template <int ML, int NST = kStages, int MINB = 3>
@@ -1567,8 +1795,69 @@ void launch_spmv_fv2d(const Geo& geo, int G, cudaStream_t s, long long N, const 
 
 void launch_pcg_spmv_fv2d(const Geo& gl, int G, cudaStream_t s, long long N, const PcgState& st,
                           const Fv2dOp& op, const double* p, double* ap) {
-  UQG_DISPATCH_V(gl, pcg_spmv_fv2d_kernel, dim3(gl.B, G), red_bytes(gl, kFaceBatch), s, N, gl, st,
-                 op, p, ap);
+  // UQG_FACE_ROWS: rows per thread in flight (1 or 2); identical results
+  static const int rows = [] {
+    const char* e = getenv("UQG_FACE_ROWS");
+    return e ? atoi(e) : 1;
+  }();
+  const size_t smem = red_bytes(gl, kFaceBatch);
+  // UQG_FACE_ASYNC: cp.async pipeline depth (stages) of the async kernel, 0 =
+  // register kernel; identical results
+  static const int stages = [] {
+    const char* e = getenv("UQG_FACE_ASYNC");
+    return e ? atoi(e) : 0;
+  }();
+  if (stages == 2 || stages == 3 || stages == 4) {
+    const bool ty = op.ty != nullptr;
+    const size_t sm = smem + (size_t)stages * (ty ? 9 : 7) * gl.T * gl.V * sizeof(double);
+#define UQG_FACE_ASYNC_LAUNCH(VV, NS, TYB)                                                    \
+  do {                                                                                      \
+    static size_t configured = 0;                                                           \
+    if (sm > configured) {                                                                  \
+      cudaFuncSetAttribute(pcg_spmv_fv2d_async_kernel<VV, NS, TYB>,                          \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);           \
+      configured = sm;                                                                      \
+    }                                                                                       \
+    pcg_spmv_fv2d_async_kernel<VV, NS, TYB><<<dim3(gl.B, G), gl.T, sm, s>>>(N, gl, st, op,  \
+                                                                          p, ap);           \
+  } while (0)
+#define UQG_FACE_ASYNC_NS(VV, TYB)                       \
+  do {                                                   \
+    if (stages == 2) UQG_FACE_ASYNC_LAUNCH(VV, 2, TYB);  \
+    else if (stages == 3) UQG_FACE_ASYNC_LAUNCH(VV, 3, TYB); \
+    else UQG_FACE_ASYNC_LAUNCH(VV, 4, TYB);              \
+  } while (0)
+    if (gl.V == 2) {
+      if (ty) UQG_FACE_ASYNC_NS(2, true);
+      else UQG_FACE_ASYNC_NS(2, false);
+    } else {
+      if (ty) UQG_FACE_ASYNC_NS(1, true);
+      else UQG_FACE_ASYNC_NS(1, false);
+    }
+#undef UQG_FACE_ASYNC_NS
+#undef UQG_FACE_ASYNC_LAUNCH
+    return;
+  }
+  // UQG_FACE_PREFETCH=1: bulk-prefetch each next chunk's +m bands into L2
+  static const bool pf = [] {
+    const char* e = getenv("UQG_FACE_PREFETCH");
+    return e && atoi(e) != 0;
+  }();
+#define UQG_FACE_REG(VV, UU)                                                                 \
+  do {                                                                                       \
+    if (pf) pcg_spmv_fv2d_kernel<VV, UU, true><<<dim3(gl.B, G), gl.T, smem, s>>>(N, gl, st, op, \
+                                                                               p, ap);       \
+    else pcg_spmv_fv2d_kernel<VV, UU, false><<<dim3(gl.B, G), gl.T, smem, s>>>(N, gl, st, op, \
+                                                                                p, ap);      \
+  } while (0)
+  if (gl.V == 2) {
+    if (rows == 1) UQG_FACE_REG(2, 1);
+    else UQG_FACE_REG(2, 2);
+  } else {
+    if (rows == 1) UQG_FACE_REG(1, 1);
+    else UQG_FACE_REG(1, 2);
+  }
+#undef UQG_FACE_REG
 }
 
 void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long long nnz,
@@ -1630,7 +1919,8 @@ void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long lo
 void launch_pcg_update(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,
                        const double* dinv, int maxit, double* r, const double* ap) {
   const Geo& gl = geo;  // B preset by the caller (blocks per ACTIVE group)
-  UQG_DISPATCH_V(gl, pcg_update_kernel, dim3(gl.B, G), red_bytes(gl, 2), s, N, gl, st, dinv,
+  UQG_DISPATCH_V(gl, pcg_update_kernel, dim3(gl.B, G), red_bytes(gl, 2 * kUpdateBatch), s, N, gl,
+                 st, dinv,
                  maxit, r, ap);
 }
 

@@ -82,11 +82,15 @@ np.save(sys.argv[2], np.array(out, dtype=object), allow_pickle=True)
 """
 
 
-@pytest.mark.parametrize("persistent", ["0", "1", "2"])
-def test_face_pcg_bitwise_equal_csr_pcg(tmp_path, persistent):
+@pytest.mark.parametrize("persistent,stages,rows", [
+    ("0", "3", "2"), ("1", "3", "2"), ("2", "3", "2"),   # default face kernels
+    ("0", "2", "2"), ("0", "4", "2"), ("0", "0", "1"), ("0", "0", "2")])
+def test_face_pcg_bitwise_equal_csr_pcg(tmp_path, persistent, stages, rows):
     """Whole batched solves (iterations, QoIs, residual histories) through the
-    launch loop (0), the cooperative (1) and the cluster (2) persistent kernel."""
-    env = dict(os.environ, UQG_PCG_PERSISTENT=persistent)
+    launch loop (0), the cooperative (1) and the cluster (2) persistent kernel,
+    with the cp.async face SpMV at 2/3/4 stages or the register face SpMV."""
+    env = dict(os.environ, UQG_PCG_PERSISTENT=persistent, UQG_FACE_ASYNC=stages,
+               UQG_FACE_ROWS=rows)
     dst = tmp_path / "r.npy"
     subprocess.run([sys.executable, "-c", _SCRIPT, str(ROOT), str(dst)], env=env, check=True)
     out = np.load(dst, allow_pickle=True)
