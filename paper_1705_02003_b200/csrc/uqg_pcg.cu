@@ -329,7 +329,7 @@ struct FaceRow {
 
 // Chunks are reduced in batches of up to kFaceBatch (reduce_lanes_batch: one
 // tree and one ticket per batch, same bits as per-chunk reduce_lanes).
-constexpr int kFaceBatch = 4;
+constexpr int kFaceBatch = 8;
 
 template <int V, int U, bool PF>
 __global__ void __launch_bounds__(256, U == 1 ? 4 : 3) pcg_spmv_fv2d_kernel(long long N, Geo geo, PcgState st,
@@ -389,6 +389,113 @@ __global__ void __launch_bounds__(256, U == 1 ? 4 : 3) pcg_spmv_fv2d_kernel(long
             f[u].apply(y, acc);
             stv<V>(apg + (row + u * R) * S, y);
           }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < V; ++j) red[(k * V + j) * T + t] = acc[j];
+    }
+    if (!reduce_lanes_batch<1, V>(red, st.part, st.ticket, g, c0, B, nk, geo)) continue;
+    if (t < geo.L) {
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const size_t l = (size_t)g * S + V * t + j;
+        const double pap = red[j * geo.T + t];
+        const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
+        st.frozen[l] = fr;
+        st.alpha[l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
+      }
+    }
+    if (t == 0) st.it[g] += 1;
+  }
+}
+
+// Register face SpMV with the +-1 neighbours shared through warp shuffles: a
+// warp covers RW = 32 / Lp consecutive rows, so p[row - 1] / p[row + 1] are
+// the centre values of the neighbouring lanes except at the warp's first /
+// last row, which load them.  Cuts the L1/L2 requests for p by 2 of 5 per row
+// (the kernel is bound by L2 request throughput, not DRAM).  Needs Lp <= 32.
+// Identical arithmetic, chunks and reduction: identical bits.
+template <int V>
+__device__ __forceinline__ void shfl_v(double (&o)[V], const double (&v)[V], int delta, bool up) {
+#pragma unroll
+  for (int j = 0; j < V; ++j)
+    o[j] = up ? __shfl_up_sync(0xffffffffu, v[j], delta) : __shfl_down_sync(0xffffffffu, v[j], delta);
+}
+
+template <int V>
+__global__ void __launch_bounds__(256, 4) pcg_spmv_fv2d_shfl_kernel(long long N, Geo geo,
+                                                                    PcgState st, Fv2dOp op,
+                                                                    const double* __restrict__ p,
+                                                                    double* __restrict__ ap) {
+  extern __shared__ double red[];
+  const int g = blockIdx.y, t = threadIdx.x;
+  if (st.done[g] != kRunning) return;
+  const int Lp = geo.Lp, sl = t % Lp, rr = t / Lp, S = geo.S, R = geo.R, m = op.m;
+  const int n = (int)N, B = gridDim.x, T = geo.T;
+  const int RW = 32 / Lp, wr = rr % RW;  // rows per warp, this row's place in the warp
+  const bool lane_ok = sl < geo.L;
+  const size_t base = (size_t)g * N * S + V * sl;
+  const double* pg = p + base;
+  double* apg = ap + base;
+  const size_t fo = (size_t)g * (N + m) * S + V * sl;
+  const double* txg = op.tx + fo;
+  const double* tyg = op.ty ? op.ty + fo : nullptr;
+  const int ct = (int)geo.chunk_tiles, tiles = (int)geo.tiles;
+  for (int c0 = blockIdx.x; c0 < geo.chunks; c0 += kFaceBatch * B) {
+    int nk = (geo.chunks - 1 - c0) / B + 1;
+    if (nk > kFaceBatch) nk = kFaceBatch;
+    for (int k = 0; k < nk; ++k) {
+      const int chunk = c0 + k * B;
+      double acc[V] = {};
+      int tile = chunk * ct, tend = tile + ct;
+      if (tend > tiles) tend = tiles;
+      int row = tile * R + rr;
+      int i0 = row / m, j0 = row - i0 * m;
+      for (; tile < tend; ++tile, row += R) {  // warp-uniform trip count
+        const bool ok = lane_ok && row < n;
+        FaceRow<V> f;
+        f.w = i0 > 0;
+        f.s = j0 > 0;
+        f.n = j0 < m - 1;
+        f.e = i0 < m - 1;
+#pragma unroll
+        for (int j = 0; j < V; ++j) f.pc[j] = 0.0;
+        if (ok) {
+          ldgv<V>(txg + row * S, f.tw);
+          ldgv<V>(txg + (row + m) * S, f.te);
+          if (tyg) {
+            ldgv<V>(tyg + (row + i0) * S, f.ts);
+            ldgv<V>(tyg + (row + i0 + 1) * S, f.tn);
+          } else {
+#pragma unroll
+            for (int j = 0; j < V; ++j) f.ts[j] = f.tn[j] = op.a_y;
+          }
+          if (f.w) ldgv<V>(pg + (row - m) * S, f.pw);
+          ldgv<V>(pg + row * S, f.pc);
+          if (f.e) ldgv<V>(pg + (row + m) * S, f.pe);
+          if (f.s && wr == 0) ldgv<V>(pg + (row - 1) * S, f.ps);
+          if (f.n && (wr == RW - 1 || row + 1 >= n)) ldgv<V>(pg + (row + 1) * S, f.pn);
+        }
+        double up[V], dn[V];
+        shfl_v<V>(up, f.pc, Lp, true);    // p[row - 1] from the lane one row up
+        shfl_v<V>(dn, f.pc, Lp, false);   // p[row + 1] from the lane one row down
+        if (ok) {
+          if (wr != 0) {
+#pragma unroll
+            for (int j = 0; j < V; ++j) f.ps[j] = up[j];
+          }
+          if (wr != RW - 1 && row + 1 < n) {
+#pragma unroll
+            for (int j = 0; j < V; ++j) f.pn[j] = dn[j];
+          }
+          double y[V];
+          f.apply(y, acc);
+          stv<V>(apg + row * S, y);
+        }
+        j0 += R;
+        while (j0 >= m) {
+          j0 -= m;
+          ++i0;
         }
       }
 #pragma unroll
@@ -828,6 +935,128 @@ __global__ void __launch_bounds__(256) pcg_spmv_fv2d_async_kernel(long long N, G
       for (int j = 0; j < V; ++j) {
         const size_t l = (size_t)g * S + V * t + j;
         const double pap = red[j * geo.T + t];
+        const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
+        st.frozen[l] = fr;
+        st.alpha[l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
+      }
+    }
+    if (t == 0) st.it[g] += 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Face-form SpMV with TMA-staged first-touch bands.  Of a tile's loads, only
+// the east faces Te = tx[row + m] and the east neighbours p[row + m] are
+// first touches (DRAM); every other operand was streamed in by an earlier tile
+// (L1/L2 hits).  One elected thread bulk-copies those two R-row bands of the
+// next NST tiles into shared memory (cp.async.bulk + mbarrier), which keeps
+// NST x 2 x R x S x 8 bytes of DRAM reads in flight per CTA without holding
+// registers; the L2-resident operands are plain loads.  Same arithmetic,
+// chunks and batched reduction as pcg_spmv_fv2d_kernel: identical bits.
+// Needs S even (16-byte rows) and 16-byte aligned tx / p.
+template <int NST>
+__global__ void __launch_bounds__(256, 4) pcg_spmv_fv2d_tma_kernel(long long N, Geo geo,
+                                                                   PcgState st, Fv2dOp op,
+                                                                   const double* __restrict__ p,
+                                                                   double* __restrict__ ap) {
+  constexpr int V = 2;
+  extern __shared__ __align__(128) double red[];
+  const int g = blockIdx.y, t = threadIdx.x;
+  if (st.done[g] != kRunning) return;
+  const int S = geo.S, R = geo.R, T = geo.T, m = op.m, n = (int)N, B = gridDim.x;
+  const int sl = t % geo.Lp, rr = t / geo.Lp;
+  const bool lane_ok = sl < geo.L;
+  const double* pg_all = p + (size_t)g * N * S;
+  const double* txg_all = op.tx + (size_t)g * (N + m) * S;
+  const double* pg = pg_all + V * sl;
+  const double* txg = txg_all + V * sl;
+  const double* tyg = op.ty ? op.ty + (size_t)g * (N + m) * S + V * sl : nullptr;
+  double* apg = ap + (size_t)g * N * S + V * sl;
+  const int band = R * S;  // doubles per staged band
+  double* stage = red + (size_t)kFaceBatch * V * T;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage + (size_t)NST * 2 * band);
+  const int n_tiles = block_tile_count(geo);
+  const float inv_m = 1.0f / (float)m;
+
+  if (t == 0) {
+    for (int s = 0; s < NST; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int i) {
+    int chunk;
+    const int r0 = (int)block_tile(geo, i, chunk) * R + m;  // first row of the +m bands
+    int tx1 = r0 + R, p1 = r0 + R;
+    if (tx1 > n + m) tx1 = n + m;
+    if (p1 > n) p1 = n;
+    const uint32_t tb = (uint32_t)(tx1 > r0 ? tx1 - r0 : 0) * (uint32_t)S * 8u;
+    const uint32_t pb = (uint32_t)(p1 > r0 ? p1 - r0 : 0) * (uint32_t)S * 8u;
+    uint64_t* bar = &bars[i % NST];
+    double* st0 = stage + (size_t)(i % NST) * 2 * band;
+    fence_proxy_async();
+    mbar_expect_tx(bar, tb + pb);
+    if (tb) bulk_g2s(st0, txg_all + (size_t)r0 * S, tb, bar);
+    if (pb) bulk_g2s(st0 + band, pg_all + (size_t)r0 * S, pb, bar);
+  };
+  if (t == 0) {
+    for (int i = 0; i < NST && i < n_tiles; ++i) issue(i);
+  }
+
+  const int ct = (int)geo.chunk_tiles;
+  double acc[V] = {};
+  int k = 0, c0 = blockIdx.x;  // chunk slot in the current batch, its first chunk
+  for (int i = 0; i < n_tiles; ++i) {
+    int chunk;
+    const long long tile = block_tile(geo, i, chunk);
+    mbar_wait(&bars[i % NST], (uint32_t)((i / NST) & 1));
+    const int row = (int)tile * R + rr;
+    if (lane_ok && row < n) {
+      int i0, j0;
+      cell_of(row, m, inv_m, i0, j0);
+      const double* st0 = stage + (size_t)(i % NST) * 2 * band + rr * S + V * sl;
+      FaceRow<V> f;
+      f.w = i0 > 0;
+      f.s = j0 > 0;
+      f.n = j0 < m - 1;
+      f.e = i0 < m - 1;
+      ldgv<V>(txg + row * S, f.tw);
+      lds_v<V>(st0, f.te);
+      if (tyg) {
+        ldgv<V>(tyg + (row + i0) * S, f.ts);
+        ldgv<V>(tyg + (row + i0 + 1) * S, f.tn);
+      } else {
+#pragma unroll
+        for (int j = 0; j < V; ++j) f.ts[j] = f.tn[j] = op.a_y;
+      }
+      if (f.w) ldgv<V>(pg + (row - m) * S, f.pw);
+      if (f.s) ldgv<V>(pg + (row - 1) * S, f.ps);
+      ldgv<V>(pg + row * S, f.pc);
+      if (f.n) ldgv<V>(pg + (row + 1) * S, f.pn);
+      if (f.e) lds_v<V>(st0 + band, f.pe);
+      double y[V];
+      f.apply(y, acc);
+      stv<V>(apg + row * S, y);
+    }
+    __syncthreads();  // stage (i % NST) consumed by every thread
+    if (t == 0 && i + NST < n_tiles) issue(i + NST);
+    const bool chunk_end = ((i + 1) % ct == 0) || (tile == geo.tiles - 1);
+    if (!chunk_end) continue;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      red[(k * V + j) * T + t] = acc[j];
+      acc[j] = 0.0;
+    }
+    ++k;
+    if (k < kFaceBatch && i + 1 < n_tiles) continue;
+    const bool last = reduce_lanes_batch<1, V>(red, st.part, st.ticket, g, c0, B, k, geo);
+    c0 += k * B;
+    k = 0;
+    if (!last) continue;
+    if (t < geo.L) {
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const size_t l = (size_t)g * S + V * t + j;
+        const double pap = red[j * T + t];
         const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
         st.frozen[l] = fr;
         st.alpha[l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
@@ -1807,6 +2036,47 @@ void launch_pcg_spmv_fv2d(const Geo& gl, int G, cudaStream_t s, long long N, con
     const char* e = getenv("UQG_FACE_ASYNC");
     return e ? atoi(e) : 0;
   }();
+  // UQG_FACE_SHFL=1: warp-shuffle register kernel (off by default: slower)
+  static const bool shfl = [] {
+    const char* e = getenv("UQG_FACE_SHFL");
+    return e && atoi(e) != 0;
+  }();
+  if (shfl && gl.Lp <= 32) {
+    if (gl.V == 2)
+      pcg_spmv_fv2d_shfl_kernel<2><<<dim3(gl.B, G), gl.T, smem, s>>>(N, gl, st, op, p, ap);
+    else
+      pcg_spmv_fv2d_shfl_kernel<1><<<dim3(gl.B, G), gl.T, smem, s>>>(N, gl, st, op, p, ap);
+    return;
+  }
+  // UQG_FACE_TMA: stages of the TMA-banded kernel (0 = off, default)
+  static const int tma = [] {
+    const char* e = getenv("UQG_FACE_TMA");
+    return e ? atoi(e) : 0;
+  }();
+  const bool aligned = ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(op.tx)) &
+                        15) == 0;
+  if (tma >= 2 && tma <= 6 && gl.V == 2 && aligned) {
+    const size_t sm = smem + (size_t)tma * 2 * gl.R * gl.S * sizeof(double) + tma * 8;
+#define UQG_FACE_TMA_LAUNCH(NS)                                                               \
+  do {                                                                                        \
+    static size_t configured = 0;                                                             \
+    if (sm > configured) {                                                                    \
+      cudaFuncSetAttribute(pcg_spmv_fv2d_tma_kernel<NS>,                                      \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);             \
+      configured = sm;                                                                        \
+    }                                                                                         \
+    pcg_spmv_fv2d_tma_kernel<NS><<<dim3(gl.B, G), gl.T, sm, s>>>(N, gl, st, op, p, ap);       \
+  } while (0)
+    switch (tma) {
+      case 2: UQG_FACE_TMA_LAUNCH(2); break;
+      case 3: UQG_FACE_TMA_LAUNCH(3); break;
+      case 4: UQG_FACE_TMA_LAUNCH(4); break;
+      case 5: UQG_FACE_TMA_LAUNCH(5); break;
+      default: UQG_FACE_TMA_LAUNCH(6); break;
+    }
+#undef UQG_FACE_TMA_LAUNCH
+    return;
+  }
   if (stages == 2 || stages == 3 || stages == 4) {
     const bool ty = op.ty != nullptr;
     const size_t sm = smem + (size_t)stages * (ty ? 9 : 7) * gl.T * gl.V * sizeof(double);

@@ -82,15 +82,18 @@ np.save(sys.argv[2], np.array(out, dtype=object), allow_pickle=True)
 """
 
 
-@pytest.mark.parametrize("persistent,stages,rows", [
-    ("0", "3", "2"), ("1", "3", "2"), ("2", "3", "2"),   # default face kernels
-    ("0", "2", "2"), ("0", "4", "2"), ("0", "0", "1"), ("0", "0", "2")])
-def test_face_pcg_bitwise_equal_csr_pcg(tmp_path, persistent, stages, rows):
+@pytest.mark.parametrize("persistent,shfl,tma,stages,rows", [
+    ("0", "0", "0", "0", "1"), ("1", "0", "0", "0", "1"), ("2", "0", "0", "0", "1"),  # defaults
+    ("0", "1", "0", "0", "1"),                              # warp-shuffle
+    ("0", "0", "2", "0", "1"), ("0", "0", "4", "0", "1"),  # TMA-banded
+    ("0", "0", "0", "0", "2"),                              # 2 rows per thread
+    ("0", "0", "0", "2", "1"), ("0", "0", "0", "4", "1")])  # cp.async kernel
+def test_face_pcg_bitwise_equal_csr_pcg(tmp_path, persistent, shfl, tma, stages, rows):
     """Whole batched solves (iterations, QoIs, residual histories) through the
     launch loop (0), the cooperative (1) and the cluster (2) persistent kernel,
-    with the cp.async face SpMV at 2/3/4 stages or the register face SpMV."""
-    env = dict(os.environ, UQG_PCG_PERSISTENT=persistent, UQG_FACE_ASYNC=stages,
-               UQG_FACE_ROWS=rows)
+    with every face SpMV variant (warp-shuffle, TMA-banded, register, cp.async)."""
+    env = dict(os.environ, UQG_PCG_PERSISTENT=persistent, UQG_FACE_SHFL=shfl, UQG_FACE_TMA=tma,
+               UQG_FACE_ASYNC=stages, UQG_FACE_ROWS=rows)
     dst = tmp_path / "r.npy"
     subprocess.run([sys.executable, "-c", _SCRIPT, str(ROOT), str(dst)], env=env, check=True)
     out = np.load(dst, allow_pickle=True)
