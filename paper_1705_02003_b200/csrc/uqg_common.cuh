@@ -72,6 +72,7 @@ struct Geo {
   long long chunk_tiles;  // tiles per reduction chunk
   int chunks;     // reduction chunks per group (<= kMaxChunks)
   int B;          // blocks per group in the launch (set by with_groups)
+  int gact;       // groups still running (with_groups), for occupancy-aware sizing
   int maxrow;     // longest graph row if known (0 = unknown): picks the unrolled SpMV
 };
 
@@ -104,6 +105,7 @@ inline Geo make_geo(long long N, int S, int maxrow = 0) {
   g.chunk_tiles = ct;
   g.chunks = (int)((g.tiles + ct - 1) / ct);
   g.B = g.chunks;
+  g.gact = 1;
   return g;
 }
 
@@ -112,15 +114,66 @@ inline Geo with_groups(Geo g, int G) {
   long long b = (kTargetBlocks + G - 1) / (G < 1 ? 1 : G);
   if (b > g.chunks) b = g.chunks;
   g.B = b < 1 ? 1 : (int)b;
+  g.gact = G < 1 ? 1 : G;
   return g;
+}
+
+// Blocks per group for G running groups of `chunks` chunks when `slots` CTAs
+// of the kernel fit on the GPU at once: the grid-stride blocks all run about
+// equally long, so the launch takes ceil(G*B / slots) "waves"; pick the B with
+// the least idle tail (G*B / (waves*slots) largest; fewer waves on near-ties).
+// Results do not depend on B (reductions follow the chunks).
+inline int pick_blocks(int G, int chunks, int slots) {
+  if (G < 1) G = 1;
+  if (slots < 1) slots = 1;
+  int best = 1;
+  double best_score = -1.0;
+  for (int b = 1; b <= chunks; ++b) {
+    const long long blocks = (long long)G * b;
+    const long long waves = (blocks + slots - 1) / slots;
+    const double eff = (double)blocks / ((double)waves * slots);
+    const double score = eff - 0.004 * (double)waves;
+    if (score > best_score) {
+      best_score = score;
+      best = b;
+    }
+    if (waves > 64) break;
+  }
+  return best;
+}
+
+// Resident CTAs of `fn` on the whole GPU (cached per shared-memory size).
+struct SlotCache {
+  size_t smem = (size_t)-1;
+  int slots = 0;
+};
+template <class F>
+inline int kernel_slots(SlotCache& c, F fn, int T, size_t smem) {
+  if (c.smem != smem) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, T, smem) != cudaSuccess) {
+      cudaGetLastError();
+      per = 1;
+    }
+    c.slots = (per < 1 ? 1 : per) * (sms < 1 ? 1 : sms);
+    c.smem = smem;
+  }
+  return c.slots;
 }
 
 // ---------------------------------------------------------------------------
 // V-lane vector access (16-byte loads/stores for V = 2).
 
+// V = 4 (32-byte accesses, sm_100 LDG/STG.256) is used by the face SpMV only.
 template <int V>
 __device__ __forceinline__ void ldv(const double* p, double (&o)[V]) {
-  if constexpr (V == 2) {
+  if constexpr (V == 4) {
+    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3])
+                 : "l"(p));
+  } else if constexpr (V == 2) {
     const double2 t = *reinterpret_cast<const double2*>(p);
     o[0] = t.x;
     o[1] = t.y;
@@ -132,7 +185,11 @@ __device__ __forceinline__ void ldv(const double* p, double (&o)[V]) {
 // read-only path (matrix values, dinv): non-coherent cache
 template <int V>
 __device__ __forceinline__ void ldgv(const double* p, double (&o)[V]) {
-  if constexpr (V == 2) {
+  if constexpr (V == 4) {
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+        : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3])
+        : "l"(p));
+  } else if constexpr (V == 2) {
     const double2 t = __ldg(reinterpret_cast<const double2*>(p));
     o[0] = t.x;
     o[1] = t.y;
@@ -144,7 +201,11 @@ __device__ __forceinline__ void ldgv(const double* p, double (&o)[V]) {
 // L2-only path (vectors written by other SMs inside the same launch)
 template <int V>
 __device__ __forceinline__ void ldcgv(const double* p, double (&o)[V]) {
-  if constexpr (V == 2) {
+  if constexpr (V == 4) {
+    asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3])
+                 : "l"(p));
+  } else if constexpr (V == 2) {
     const double2 t = __ldcg(reinterpret_cast<const double2*>(p));
     o[0] = t.x;
     o[1] = t.y;
@@ -155,7 +216,11 @@ __device__ __forceinline__ void ldcgv(const double* p, double (&o)[V]) {
 
 template <int V>
 __device__ __forceinline__ void stv(double* p, const double (&o)[V]) {
-  if constexpr (V == 2) {
+  if constexpr (V == 4) {
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(o[0]), "d"(o[1]),
+                 "d"(o[2]), "d"(o[3])
+                 : "memory");
+  } else if constexpr (V == 2) {
     *reinterpret_cast<double2*>(p) = make_double2(o[0], o[1]);
   } else {
     *p = o[0];

@@ -271,17 +271,6 @@ __global__ void __launch_bounds__(256) pcg_spmv_kernel(long long N, long long nn
 
 // Face-form FV2D operator (Fv2dOp): same reduction chunks and state updates
 // as pcg_spmv_kernel, the row's Ap re-derived from the faces (fv2d_row).
-// L2 prefetch of the rows [r0, r1) of a [rows][S] array (bulk, async, no
-// completion tracking).  Used for the first-touch +m bands of the face SpMV.
-__device__ __forceinline__ void prefetch_rows_l2(const double* base, int r0, int r1, int S) {
-  if (r1 <= r0) return;
-  const uint32_t bytes = (uint32_t)(r1 - r0) * (uint32_t)S * 8u;
-  if ((reinterpret_cast<uintptr_t>(base + (size_t)r0 * S) & 15) || (bytes & 15)) return;
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + (size_t)r0 * S),
-               "r"(bytes)
-               : "memory");
-}
-
 // One row of the face-form operator: loads, then the CSR-order sum.
 template <int V>
 struct FaceRow {
@@ -332,11 +321,10 @@ struct FaceRow {
 constexpr int kFaceBatch = 8;
 
 template <int V, int U, bool PF>
-__global__ void __launch_bounds__(256, U == 1 ? 4 : 3) pcg_spmv_fv2d_kernel(long long N, Geo geo, PcgState st,
-                                                            Fv2dOp op,
-                                                            const double* __restrict__ p,
-                                                            double* __restrict__ ap) {
-  extern __shared__ double red[];
+__device__ __forceinline__ void face_spmv_body(long long N, const Geo& geo, const PcgState& st,
+                                               const Fv2dOp& op, const double* __restrict__ p,
+                                               double* __restrict__ ap) {
+  extern __shared__ __align__(16) double red[];
   const int g = blockIdx.y, t = threadIdx.x;
   if (st.done[g] != kRunning) return;
   const int sl = t % geo.Lp, rr = t / geo.Lp, S = geo.S, R = geo.R, m = op.m;
@@ -353,14 +341,13 @@ __global__ void __launch_bounds__(256, U == 1 ? 4 : 3) pcg_spmv_fv2d_kernel(long
     if (nk > kFaceBatch) nk = kFaceBatch;
     for (int k = 0; k < nk; ++k) {
       const int chunk = c0 + k * B;
-      if (t == 0 && PF) {  // first-touch (+m) bands of this block's next chunk
-        const int nc = chunk + B;
-        if (nc < geo.chunks) {
-          const int a = nc * ct * R + m, bnd = (int)(N + m);
-          int e = a + ct * R;
-          e = e < bnd ? e : bnd;
-          prefetch_rows_l2(op.tx + (size_t)g * (N + m) * S, a, e, S);
-          if (a < n) prefetch_rows_l2(p + (size_t)g * N * S, a, e < n ? e : n, S);
+      if (PF && sl < geo.L && chunk + B < geo.chunks) {
+        // L2 prefetch of this thread's first-touch (DRAM) operands of its
+        // next chunk: the +m rows of tx and p (no registers held)
+        int r = (chunk + B) * ct * R + rr + m;
+        for (int u = 0; u < ct; ++u, r += R) {
+          if (r < n + m) asm volatile("prefetch.global.L2 [%0];" ::"l"(txg + r * S));
+          if (r < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(pg + r * S));
         }
       }
       double acc[V] = {};
@@ -407,6 +394,23 @@ __global__ void __launch_bounds__(256, U == 1 ? 4 : 3) pcg_spmv_fv2d_kernel(long
     }
     if (t == 0) st.it[g] += 1;
   }
+}
+
+template <int V, int U, bool PF>
+__global__ void __launch_bounds__(256, U == 1 ? 4 : 3) pcg_spmv_fv2d_kernel(
+    long long N, Geo geo, PcgState st, Fv2dOp op, const double* __restrict__ p,
+    double* __restrict__ ap) {
+  face_spmv_body<V, U, PF>(N, geo, st, op, p, ap);
+}
+
+// 4 lanes per thread (32-byte LDG/STG.256) at half the block size: the same
+// rows per tile (R), chunks and per-lane reduction trees as the 2-lane kernel
+// (identical bits), half the address arithmetic and more bytes in flight per
+// register.  geo: the 2-lane geometry with V = 4, L and Lp halved, T = 128.
+__global__ void __launch_bounds__(128, 5) pcg_spmv_fv2d4_kernel(
+    long long N, Geo geo, PcgState st, Fv2dOp op, const double* __restrict__ p,
+    double* __restrict__ ap) {
+  face_spmv_body<4, 1, false>(N, geo, st, op, p, ap);
 }
 
 // Register face SpMV with the +-1 neighbours shared through warp shuffles: a
@@ -1892,6 +1896,24 @@ __global__ void pcg_finalize_kernel(PcgState st, int G, int S, int* ens_iters) {
 
 static size_t red_bytes(const Geo& geo, int nv) { return (size_t)nv * geo.V * geo.T * sizeof(double); }
 
+// Blocks per group sized to the kernel's residency (pick_blocks) for the
+// geo.gact running groups; UQG_OCC_BLOCKS=0 keeps with_groups' fixed target.
+static bool occ_blocks() {
+  static const bool on = [] {
+    const char* e = getenv("UQG_OCC_BLOCKS");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+
+template <class F>
+static Geo sized(const Geo& geo, SlotCache& c, F fn, int T, size_t smem) {
+  Geo gl = geo;
+  if (occ_blocks()) gl.B = pick_blocks(geo.gact, geo.chunks, kernel_slots(c, fn, T, smem));
+  return gl;
+}
+
+
 void launch_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long long nnz, const int* ro,
                  const int* ci, const double* vals, const double* x, double* y) {
   const Geo gl = with_groups(geo, G);
@@ -2022,8 +2044,14 @@ void launch_spmv_fv2d(const Geo& geo, int G, cudaStream_t s, long long N, const 
   UQG_DISPATCH_V(gl, spmv_fv2d_kernel, dim3(gl.B, G), 0, s, N, gl, op, x, y);
 }
 
-void launch_pcg_spmv_fv2d(const Geo& gl, int G, cudaStream_t s, long long N, const PcgState& st,
+void launch_pcg_spmv_fv2d(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,
                           const Fv2dOp& op, const double* p, double* ap) {
+  static SlotCache cf2, cf1;
+  const Geo gl = geo.V == 2
+                     ? sized(geo, cf2, pcg_spmv_fv2d_kernel<2, 1, false>, geo.T,
+                             red_bytes(geo, kFaceBatch))
+                     : sized(geo, cf1, pcg_spmv_fv2d_kernel<1, 1, false>, geo.T,
+                             red_bytes(geo, kFaceBatch));
   // UQG_FACE_ROWS: rows per thread in flight (1 or 2); identical results
   static const int rows = [] {
     const char* e = getenv("UQG_FACE_ROWS");
@@ -2036,6 +2064,22 @@ void launch_pcg_spmv_fv2d(const Geo& gl, int G, cudaStream_t s, long long N, con
     const char* e = getenv("UQG_FACE_ASYNC");
     return e ? atoi(e) : 0;
   }();
+  // UQG_FACE_V4=0 disables the 4-lanes-per-thread kernel (default when S % 4 == 0)
+  static const bool v4 = [] {
+    const char* e = getenv("UQG_FACE_V4");
+    return !e || atoi(e) != 0;
+  }();
+  const bool al32 = ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(op.tx) |
+                      reinterpret_cast<uintptr_t>(ap)) & 31) == 0;
+  if (v4 && gl.V == 2 && gl.S % 4 == 0 && gl.Lp >= 2 && gl.T == 256 && al32 && !op.ty) {
+    Geo g4 = gl;
+    g4.V = 4;
+    g4.L = gl.L / 2;
+    g4.Lp = gl.Lp / 2;
+    g4.T = gl.T / 2;  // rows per tile R unchanged
+    pcg_spmv_fv2d4_kernel<<<dim3(g4.B, G), g4.T, smem, s>>>(N, g4, st, op, p, ap);
+    return;
+  }
   // UQG_FACE_SHFL=1: warp-shuffle register kernel (off by default: slower)
   static const bool shfl = [] {
     const char* e = getenv("UQG_FACE_SHFL");
@@ -2108,7 +2152,7 @@ void launch_pcg_spmv_fv2d(const Geo& gl, int G, cudaStream_t s, long long N, con
 #undef UQG_FACE_ASYNC_LAUNCH
     return;
   }
-  // UQG_FACE_PREFETCH=1: bulk-prefetch each next chunk's +m bands into L2
+  // UQG_FACE_PREFETCH=1: per-thread L2 prefetch of the next chunk's +m rows
   static const bool pf = [] {
     const char* e = getenv("UQG_FACE_PREFETCH");
     return e && atoi(e) != 0;
@@ -2188,15 +2232,18 @@ void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long lo
 
 void launch_pcg_update(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,
                        const double* dinv, int maxit, double* r, const double* ap) {
-  const Geo& gl = geo;  // B preset by the caller (blocks per ACTIVE group)
-  UQG_DISPATCH_V(gl, pcg_update_kernel, dim3(gl.B, G), red_bytes(gl, 2 * kUpdateBatch), s, N, gl,
-                 st, dinv,
-                 maxit, r, ap);
+  static SlotCache c1, c2;
+  const size_t smem = red_bytes(geo, 2 * kUpdateBatch);
+  const Geo gl = geo.V == 2 ? sized(geo, c2, pcg_update_kernel<2>, geo.T, smem)
+                            : sized(geo, c1, pcg_update_kernel<1>, geo.T, smem);
+  UQG_DISPATCH_V(gl, pcg_update_kernel, dim3(gl.B, G), smem, s, N, gl, st, dinv, maxit, r, ap);
 }
 
 void launch_pcg_dir(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,
                     const double* dinv, const double* r, double* x, double* p) {
-  const Geo& gl = geo;  // B preset by the caller (blocks per ACTIVE group)
+  // fixed with_groups target: measured faster for this pure stream than the
+  // residency-sized grid (C2: 2043 vs 2099 ms)
+  const Geo& gl = geo;
   UQG_DISPATCH_V(gl, pcg_dir_kernel, dim3(gl.B, G), 0, s, N, gl, st, dinv, r, x, p);
 }
 

@@ -82,18 +82,25 @@ np.save(sys.argv[2], np.array(out, dtype=object), allow_pickle=True)
 """
 
 
-@pytest.mark.parametrize("persistent,shfl,tma,stages,rows", [
-    ("0", "0", "0", "0", "1"), ("1", "0", "0", "0", "1"), ("2", "0", "0", "0", "1"),  # defaults
-    ("0", "1", "0", "0", "1"),                              # warp-shuffle
-    ("0", "0", "2", "0", "1"), ("0", "0", "4", "0", "1"),  # TMA-banded
-    ("0", "0", "0", "0", "2"),                              # 2 rows per thread
-    ("0", "0", "0", "2", "1"), ("0", "0", "0", "4", "1")])  # cp.async kernel
-def test_face_pcg_bitwise_equal_csr_pcg(tmp_path, persistent, shfl, tma, stages, rows):
+_VARIANTS = {  # face SpMV variants (all must give the CSR bits)
+    "v4": {},                                            # default: 4 lanes / thread
+    "reg": {"UQG_FACE_V4": "0"},                         # 2 lanes / thread
+    "reg2": {"UQG_FACE_V4": "0", "UQG_FACE_ROWS": "2"},  # 2 rows in flight
+    "shfl": {"UQG_FACE_V4": "0", "UQG_FACE_SHFL": "1"},  # warp-shuffle neighbours
+    "tma2": {"UQG_FACE_V4": "0", "UQG_FACE_TMA": "2"},   # TMA-banded
+    "tma4": {"UQG_FACE_V4": "0", "UQG_FACE_TMA": "4"},
+    "async2": {"UQG_FACE_V4": "0", "UQG_FACE_ASYNC": "2"},  # cp.async
+    "async4": {"UQG_FACE_V4": "0", "UQG_FACE_ASYNC": "4"},
+}
+
+
+@pytest.mark.parametrize("persistent,variant", [
+    ("0", "v4"), ("1", "v4"), ("2", "v4")] + [("0", v) for v in _VARIANTS if v != "v4"])
+def test_face_pcg_bitwise_equal_csr_pcg(tmp_path, persistent, variant):
     """Whole batched solves (iterations, QoIs, residual histories) through the
     launch loop (0), the cooperative (1) and the cluster (2) persistent kernel,
-    with every face SpMV variant (warp-shuffle, TMA-banded, register, cp.async)."""
-    env = dict(os.environ, UQG_PCG_PERSISTENT=persistent, UQG_FACE_SHFL=shfl, UQG_FACE_TMA=tma,
-               UQG_FACE_ASYNC=stages, UQG_FACE_ROWS=rows)
+    with every face SpMV variant."""
+    env = dict(os.environ, UQG_PCG_PERSISTENT=persistent, **_VARIANTS[variant])
     dst = tmp_path / "r.npy"
     subprocess.run([sys.executable, "-c", _SCRIPT, str(ROOT), str(dst)], env=env, check=True)
     out = np.load(dst, allow_pickle=True)
