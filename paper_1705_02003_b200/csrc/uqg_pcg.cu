@@ -2064,10 +2064,10 @@ void launch_pcg_spmv_fv2d(const Geo& geo, int G, cudaStream_t s, long long N, co
     const char* e = getenv("UQG_FACE_ASYNC");
     return e ? atoi(e) : 0;
   }();
-  // UQG_FACE_V4=0 disables the 4-lanes-per-thread kernel (default when S % 4 == 0)
+  // UQG_FACE_V4=1: 4-lanes-per-thread kernel (off by default: measured slower)
   static const bool v4 = [] {
     const char* e = getenv("UQG_FACE_V4");
-    return !e || atoi(e) != 0;
+    return e && atoi(e) != 0;
   }();
   const bool al32 = ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(op.tx) |
                       reinterpret_cast<uintptr_t>(ap)) & 31) == 0;

@@ -139,7 +139,7 @@ struct LaneSmem {
 };
 
 template <int V, bool CL>
-__global__ void __launch_bounds__(256) pcg_persistent_kernel(
+__global__ void __launch_bounds__(256, 4) pcg_persistent_kernel(
     long long N, long long nnz, Geo geo, PcgState st, const int* __restrict__ ro,
     const int* __restrict__ ci, const double* __restrict__ vals, Fv2dOp fv,
     const double* __restrict__ rhs,

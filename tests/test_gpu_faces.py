@@ -83,19 +83,21 @@ np.save(sys.argv[2], np.array(out, dtype=object), allow_pickle=True)
 
 
 _VARIANTS = {  # face SpMV variants (all must give the CSR bits)
-    "v4": {},                                            # default: 4 lanes / thread
-    "reg": {"UQG_FACE_V4": "0"},                         # 2 lanes / thread
-    "reg2": {"UQG_FACE_V4": "0", "UQG_FACE_ROWS": "2"},  # 2 rows in flight
-    "shfl": {"UQG_FACE_V4": "0", "UQG_FACE_SHFL": "1"},  # warp-shuffle neighbours
-    "tma2": {"UQG_FACE_V4": "0", "UQG_FACE_TMA": "2"},   # TMA-banded
-    "tma4": {"UQG_FACE_V4": "0", "UQG_FACE_TMA": "4"},
-    "async2": {"UQG_FACE_V4": "0", "UQG_FACE_ASYNC": "2"},  # cp.async
-    "async4": {"UQG_FACE_V4": "0", "UQG_FACE_ASYNC": "4"},
+    "reg": {},                                            # default: 2 lanes / thread
+    "v4": {"UQG_FACE_V4": "1"},                           # 4 lanes / thread (LDG.256)
+    "reg2": {"UQG_FACE_ROWS": "2"},                       # 2 rows in flight
+    "shfl": {"UQG_FACE_SHFL": "1"},                       # warp-shuffle neighbours
+    "tma2": {"UQG_FACE_TMA": "2"},                        # TMA-banded
+    "tma4": {"UQG_FACE_TMA": "4"},
+    "async2": {"UQG_FACE_ASYNC": "2"},                    # cp.async
+    "async4": {"UQG_FACE_ASYNC": "4"},
+    "pf": {"UQG_FACE_PREFETCH": "1"},                     # per-thread L2 prefetch
+    "fixed": {"UQG_OCC_BLOCKS": "0"},                     # with_groups block sizing
 }
 
 
 @pytest.mark.parametrize("persistent,variant", [
-    ("0", "v4"), ("1", "v4"), ("2", "v4")] + [("0", v) for v in _VARIANTS if v != "v4"])
+    ("0", "reg"), ("1", "reg"), ("2", "reg")] + [("0", v) for v in _VARIANTS if v != "reg"])
 def test_face_pcg_bitwise_equal_csr_pcg(tmp_path, persistent, variant):
     """Whole batched solves (iterations, QoIs, residual histories) through the
     launch loop (0), the cooperative (1) and the cluster (2) persistent kernel,
