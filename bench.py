@@ -420,13 +420,26 @@ def main():
         peaks = json.loads(pk.read_text())
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    traffic = {}
+    traffic_all = {}
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
-        key = cfg.name if bm["operator"] == "csr" else f"{cfg.name}:faces"
-        traffic = json.loads(tf.read_text()).get(key, {})
-    spmv_ms = ms[3]
-    spmv_gbs = group_iters * bm["spmv"] / (spmv_ms / 1e3) / 1e9 if spmv_ms else None
+        traffic_all = json.loads(tf.read_text())
+    # per-kernel rooflines of the three PCG kernels; the line's "roofline" is the
+    # one with the largest measured time share (the dominant kernel)
+    spmv_name = "pcg_spmv_fv2d_kernel" if bm["operator"] != "csr" else "pcg_spmv_tma_kernel"
+    per = {}
+    for key, idx, kname in (("spmv", 3, spmv_name), ("update", 4, "pcg_update_kernel"),
+                            ("dir", 5, "pcg_dir_kernel")):
+        t_ms = ms[idx]
+        gbs = group_iters * bm[key] / (t_ms / 1e3) / 1e9 if t_ms else None
+        tr = traffic_all.get(f"{cfg.name}:{kname}", {})
+        per[key] = {"kernel": kname, "ms": t_ms, "achieved": gbs,
+                    "frac": gbs / peak if gbs else None,
+                    "bytes_per_group_launch": bm[key],
+                    "traffic": tr.get("dram_bytes_per_launch"),
+                    "traffic_algorithmic_same_launch": tr.get("algorithmic_bytes_per_launch"),
+                    "traffic_source": tr.get("source")}
+    dom = max(per, key=lambda k: per[k]["ms"] or 0.0)
     loop_ms = ms[3] + ms[4] + ms[5]
     loop_gbs = group_iters * bm["pcg_iter"] / (loop_ms / 1e3) / 1e9 if loop_ms else None
     step_gbs = group_iters * bm["pcg_iter"] / (total_ms / 1e3) / 1e9
@@ -458,18 +471,17 @@ def main():
         "e2e": {"value": world * n * len(e2e_t) / sum(e2e_t) * (args.max_iters or 1),
                 "unit": unit,
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
-        "roofline": {"bound": "hbm",
-                     "kernel": ("pcg_spmv_fv2d_kernel" if bm["operator"] != "csr"
-                                else "pcg_spmv_tma_kernel"),
-                     "operator": bm["operator"],
-                     "achieved": spmv_gbs, "peak": peak, "unit": "GB/s",
-                     "frac": (spmv_gbs / peak) if spmv_gbs else None,
-                     "traffic": traffic.get("dram_bytes_per_launch"),
-                     "traffic_algorithmic_same_launch": traffic.get("algorithmic_bytes_per_launch"),
-                     "traffic_source": traffic.get("source"),
+        "roofline": {"bound": "hbm", "kernel": per[dom]["kernel"], "operator": bm["operator"],
+                     "achieved": per[dom]["achieved"], "peak": peak, "unit": "GB/s",
+                     "frac": per[dom]["frac"], "traffic": per[dom]["traffic"],
+                     "traffic_algorithmic_same_launch": per[dom]["traffic_algorithmic_same_launch"],
+                     "traffic_source": per[dom]["traffic_source"],
                      "peak_source": peak_src,
-                     "bytes_per_group_launch": bm["spmv"],
-                     "group_launches": group_iters},
+                     "bytes_per_group_launch": per[dom]["bytes_per_group_launch"],
+                     "group_launches": group_iters,
+                     "time_share": (per[dom]["ms"] / sum(ms[k] for k in range(NK))
+                                    if sum(ms[k] for k in range(NK)) else None),
+                     "pcg_kernels": per},
         "pcg_loop": {"achieved_gbs": loop_gbs, "frac": loop_gbs / peak if loop_gbs else None,
                      "bytes_per_group_iter": bm["pcg_iter"],
                      "moved_gbs": (loop_gbs * bm["pcg_iter_moved"] / bm["pcg_iter"])
