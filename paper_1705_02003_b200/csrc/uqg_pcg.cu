@@ -320,7 +320,7 @@ struct FaceRow {
 // tree and one ticket per batch, same bits as per-chunk reduce_lanes).
 constexpr int kFaceBatch = 8;
 
-template <int V, int U, bool PF>
+template <int V>
 __device__ __forceinline__ void face_spmv_body(long long N, const Geo& geo, const PcgState& st,
                                                const Fv2dOp& op, const double* __restrict__ p,
                                                double* __restrict__ ap) {
@@ -341,40 +341,22 @@ __device__ __forceinline__ void face_spmv_body(long long N, const Geo& geo, cons
     if (nk > kFaceBatch) nk = kFaceBatch;
     for (int k = 0; k < nk; ++k) {
       const int chunk = c0 + k * B;
-      if (PF && sl < geo.L && chunk + B < geo.chunks) {
-        // L2 prefetch of this thread's first-touch (DRAM) operands of its
-        // next chunk: the +m rows of tx and p (no registers held)
-        int r = (chunk + B) * ct * R + rr + m;
-        for (int u = 0; u < ct; ++u, r += R) {
-          if (r < n + m) asm volatile("prefetch.global.L2 [%0];" ::"l"(txg + r * S));
-          if (r < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(pg + r * S));
-        }
-      }
       double acc[V] = {};
       if (sl < geo.L) {
         int row = chunk * ct * R + rr;  // first row of this thread in the chunk
         int rend = (chunk + 1) * ct * R;
         if (rend > n) rend = n;
         int i0 = row / m, j0 = row - i0 * m;
-        for (; row < rend; row += U * R) {
-          FaceRow<V> f[U];
-          bool ok[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {  // all loads of the U rows first
-            ok[u] = row + u * R < rend;
-            if (ok[u]) f[u].load(txg, tyg, pg, op.a_y, m, S, row + u * R, i0, j0);
-            j0 += R;
-            while (j0 >= m) {
-              j0 -= m;
-              ++i0;
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            if (!ok[u]) continue;
-            double y[V];
-            f[u].apply(y, acc);
-            stv<V>(apg + (row + u * R) * S, y);
+        for (; row < rend; row += R) {
+          FaceRow<V> f;
+          f.load(txg, tyg, pg, op.a_y, m, S, row, i0, j0);
+          double y[V];
+          f.apply(y, acc);
+          stv<V>(apg + row * S, y);
+          j0 += R;
+          while (j0 >= m) {
+            j0 -= m;
+            ++i0;
           }
         }
       }
@@ -396,11 +378,11 @@ __device__ __forceinline__ void face_spmv_body(long long N, const Geo& geo, cons
   }
 }
 
-template <int V, int U, bool PF>
-__global__ void __launch_bounds__(256, U == 1 ? 4 : 3) pcg_spmv_fv2d_kernel(
+template <int V>
+__global__ void __launch_bounds__(256, 4) pcg_spmv_fv2d_kernel(
     long long N, Geo geo, PcgState st, Fv2dOp op, const double* __restrict__ p,
     double* __restrict__ ap) {
-  face_spmv_body<V, U, PF>(N, geo, st, op, p, ap);
+  face_spmv_body<V>(N, geo, st, op, p, ap);
 }
 
 // 4 lanes per thread (32-byte LDG/STG.256) at half the block size: the same
@@ -410,7 +392,7 @@ __global__ void __launch_bounds__(256, U == 1 ? 4 : 3) pcg_spmv_fv2d_kernel(
 __global__ void __launch_bounds__(128, 5) pcg_spmv_fv2d4_kernel(
     long long N, Geo geo, PcgState st, Fv2dOp op, const double* __restrict__ p,
     double* __restrict__ ap) {
-  face_spmv_body<4, 1, false>(N, geo, st, op, p, ap);
+  face_spmv_body<4>(N, geo, st, op, p, ap);
 }
 
 // Register face SpMV with the +-1 neighbours shared through warp shuffles: a
@@ -784,29 +766,7 @@ __device__ __forceinline__ int block_tile_count(const Geo& geo) {
 }
 
 // ---------------------------------------------------------------------------
-// Face-form SpMV with per-thread cp.async pipelining.  Each thread gathers the
-// 7 (9 with random y-faces) 16-byte operands of its next NSTG-1 rows straight
-// into its own shared-memory slots (cp.async: no registers held while the
-// loads are in flight), so the loads of several rows overlap without the
-// register cost of the register kernel.  Threads only read their own slots:
-// no block barrier in the pipeline.  Same arithmetic, chunks and batched
-// reduction as pcg_spmv_fv2d_kernel: identical bits.
-
-__device__ __forceinline__ void cp_async_ca(void* dst, const void* src, int bytes) {
-  if (bytes == 16)
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
-                 : "memory");
-  else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int NW>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(NW) : "memory");
-}
+// Shared helpers of the staged face SpMV.
 
 template <int V>
 __device__ __forceinline__ void lds_v(const double* p, double (&o)[V]) {
@@ -829,122 +789,6 @@ __device__ __forceinline__ void cell_of(int row, int m, float inv_m, int& i0, in
   } else if (j0 >= m) {
     ++i0;
     j0 -= m;
-  }
-}
-
-template <int V, int NSTG, bool TY>
-__global__ void __launch_bounds__(256) pcg_spmv_fv2d_async_kernel(long long N, Geo geo,
-                                                                  PcgState st, Fv2dOp op,
-                                                                  const double* __restrict__ p,
-                                                                  double* __restrict__ ap) {
-  constexpr int NSL = TY ? 9 : 7;  // tw te [ts tn] pw ps pc pn pe
-  extern __shared__ __align__(16) double red[];
-  const int g = blockIdx.y, t = threadIdx.x;
-  if (st.done[g] != kRunning) return;
-  const int sl = t % geo.Lp, rr = t / geo.Lp, S = geo.S, R = geo.R, m = op.m;
-  const int n = (int)N, B = gridDim.x, T = geo.T;
-  const bool lane_ok = sl < geo.L;
-  const size_t base = (size_t)g * N * S + V * sl;
-  const double* pg = p + base;
-  double* apg = ap + base;
-  const size_t fo = (size_t)g * (N + m) * S + V * sl;
-  const double* txg = op.tx + fo;
-  const double* tyg = TY ? op.ty + fo : nullptr;
-  double* stg = red + (size_t)kFaceBatch * V * T;
-  const float inv_m = 1.0f / (float)m;
-  const int ct = (int)geo.chunk_tiles;
-  constexpr int BY = 8 * V;
-  auto slot = [&](int s, int k) { return stg + ((size_t)(s * NSL + k) * T + t) * V; };
-  for (int c0 = blockIdx.x; c0 < geo.chunks; c0 += kFaceBatch * B) {
-    int nk = (geo.chunks - 1 - c0) / B + 1;
-    if (nk > kFaceBatch) nk = kFaceBatch;
-    const int items = nk * ct;
-    auto item_row = [&](int q) {
-      const int k = q / ct;
-      const int row = ((c0 + k * B) * ct + (q - k * ct)) * R + rr;
-      return row < n ? row : -1;
-    };
-    auto issue = [&](int q) {
-      if (q < items && lane_ok) {
-        const int row = item_row(q);
-        if (row >= 0) {
-          int i0, j0;
-          cell_of(row, m, inv_m, i0, j0);
-          const int s = q % NSTG;
-          cp_async_ca(slot(s, 0), txg + row * S, BY);
-          cp_async_ca(slot(s, 1), txg + (row + m) * S, BY);
-          if constexpr (TY) {
-            cp_async_ca(slot(s, 2), tyg + (row + i0) * S, BY);
-            cp_async_ca(slot(s, 3), tyg + (row + i0 + 1) * S, BY);
-          }
-          constexpr int P0 = TY ? 4 : 2;
-          if (i0 > 0) cp_async_ca(slot(s, P0), pg + (row - m) * S, BY);
-          if (j0 > 0) cp_async_ca(slot(s, P0 + 1), pg + (row - 1) * S, BY);
-          cp_async_ca(slot(s, P0 + 2), pg + row * S, BY);
-          if (j0 < m - 1) cp_async_ca(slot(s, P0 + 3), pg + (row + 1) * S, BY);
-          if (i0 < m - 1) cp_async_ca(slot(s, P0 + 4), pg + (row + m) * S, BY);
-        }
-      }
-      cp_async_commit();
-    };
-#pragma unroll
-    for (int q = 0; q < NSTG - 1; ++q) issue(q);
-    double acc[V] = {};
-    for (int q = 0; q < items; ++q) {
-      issue(q + NSTG - 1);
-      cp_async_wait<NSTG - 1>();
-      const int k = q / ct;
-      if (lane_ok) {
-        const int row = item_row(q);
-        if (row >= 0) {
-          int i0, j0;
-          cell_of(row, m, inv_m, i0, j0);
-          const int s = q % NSTG;
-          constexpr int P0 = TY ? 4 : 2;
-          FaceRow<V> f;
-          lds_v<V>(slot(s, 0), f.tw);
-          lds_v<V>(slot(s, 1), f.te);
-          if constexpr (TY) {
-            lds_v<V>(slot(s, 2), f.ts);
-            lds_v<V>(slot(s, 3), f.tn);
-          } else {
-#pragma unroll
-            for (int j = 0; j < V; ++j) f.ts[j] = f.tn[j] = op.a_y;
-          }
-          f.w = i0 > 0;
-          f.s = j0 > 0;
-          f.n = j0 < m - 1;
-          f.e = i0 < m - 1;
-          if (f.w) lds_v<V>(slot(s, P0), f.pw);
-          if (f.s) lds_v<V>(slot(s, P0 + 1), f.ps);
-          lds_v<V>(slot(s, P0 + 2), f.pc);
-          if (f.n) lds_v<V>(slot(s, P0 + 3), f.pn);
-          if (f.e) lds_v<V>(slot(s, P0 + 4), f.pe);
-          double y[V];
-          f.apply(y, acc);
-          stv<V>(apg + row * S, y);
-        }
-      }
-      if (q - k * ct == ct - 1) {
-#pragma unroll
-        for (int j = 0; j < V; ++j) {
-          red[(k * V + j) * T + t] = acc[j];
-          acc[j] = 0.0;
-        }
-      }
-    }
-    if (!reduce_lanes_batch<1, V>(red, st.part, st.ticket, g, c0, B, nk, geo)) continue;
-    if (t < geo.L) {
-#pragma unroll
-      for (int j = 0; j < V; ++j) {
-        const size_t l = (size_t)g * S + V * t + j;
-        const double pap = red[j * geo.T + t];
-        const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
-        st.frozen[l] = fr;
-        st.alpha[l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
-      }
-    }
-    if (t == 0) st.it[g] += 1;
   }
 }
 
@@ -2048,22 +1892,11 @@ void launch_pcg_spmv_fv2d(const Geo& geo, int G, cudaStream_t s, long long N, co
                           const Fv2dOp& op, const double* p, double* ap) {
   static SlotCache cf2, cf1;
   const Geo gl = geo.V == 2
-                     ? sized(geo, cf2, pcg_spmv_fv2d_kernel<2, 1, false>, geo.T,
+                     ? sized(geo, cf2, pcg_spmv_fv2d_kernel<2>, geo.T,
                              red_bytes(geo, kFaceBatch))
-                     : sized(geo, cf1, pcg_spmv_fv2d_kernel<1, 1, false>, geo.T,
+                     : sized(geo, cf1, pcg_spmv_fv2d_kernel<1>, geo.T,
                              red_bytes(geo, kFaceBatch));
-  // UQG_FACE_ROWS: rows per thread in flight (1 or 2); identical results
-  static const int rows = [] {
-    const char* e = getenv("UQG_FACE_ROWS");
-    return e ? atoi(e) : 1;
-  }();
   const size_t smem = red_bytes(gl, kFaceBatch);
-  // UQG_FACE_ASYNC: cp.async pipeline depth (stages) of the async kernel, 0 =
-  // register kernel; identical results
-  static const int stages = [] {
-    const char* e = getenv("UQG_FACE_ASYNC");
-    return e ? atoi(e) : 0;
-  }();
   // UQG_FACE_V4=1: 4-lanes-per-thread kernel (off by default: measured slower)
   static const bool v4 = [] {
     const char* e = getenv("UQG_FACE_V4");
@@ -2121,57 +1954,10 @@ void launch_pcg_spmv_fv2d(const Geo& geo, int G, cudaStream_t s, long long N, co
 #undef UQG_FACE_TMA_LAUNCH
     return;
   }
-  if (stages == 2 || stages == 3 || stages == 4) {
-    const bool ty = op.ty != nullptr;
-    const size_t sm = smem + (size_t)stages * (ty ? 9 : 7) * gl.T * gl.V * sizeof(double);
-#define UQG_FACE_ASYNC_LAUNCH(VV, NS, TYB)                                                    \
-  do {                                                                                      \
-    static size_t configured = 0;                                                           \
-    if (sm > configured) {                                                                  \
-      cudaFuncSetAttribute(pcg_spmv_fv2d_async_kernel<VV, NS, TYB>,                          \
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);           \
-      configured = sm;                                                                      \
-    }                                                                                       \
-    pcg_spmv_fv2d_async_kernel<VV, NS, TYB><<<dim3(gl.B, G), gl.T, sm, s>>>(N, gl, st, op,  \
-                                                                          p, ap);           \
-  } while (0)
-#define UQG_FACE_ASYNC_NS(VV, TYB)                       \
-  do {                                                   \
-    if (stages == 2) UQG_FACE_ASYNC_LAUNCH(VV, 2, TYB);  \
-    else if (stages == 3) UQG_FACE_ASYNC_LAUNCH(VV, 3, TYB); \
-    else UQG_FACE_ASYNC_LAUNCH(VV, 4, TYB);              \
-  } while (0)
-    if (gl.V == 2) {
-      if (ty) UQG_FACE_ASYNC_NS(2, true);
-      else UQG_FACE_ASYNC_NS(2, false);
-    } else {
-      if (ty) UQG_FACE_ASYNC_NS(1, true);
-      else UQG_FACE_ASYNC_NS(1, false);
-    }
-#undef UQG_FACE_ASYNC_NS
-#undef UQG_FACE_ASYNC_LAUNCH
-    return;
-  }
-  // UQG_FACE_PREFETCH=1: per-thread L2 prefetch of the next chunk's +m rows
-  static const bool pf = [] {
-    const char* e = getenv("UQG_FACE_PREFETCH");
-    return e && atoi(e) != 0;
-  }();
-#define UQG_FACE_REG(VV, UU)                                                                 \
-  do {                                                                                       \
-    if (pf) pcg_spmv_fv2d_kernel<VV, UU, true><<<dim3(gl.B, G), gl.T, smem, s>>>(N, gl, st, op, \
-                                                                               p, ap);       \
-    else pcg_spmv_fv2d_kernel<VV, UU, false><<<dim3(gl.B, G), gl.T, smem, s>>>(N, gl, st, op, \
-                                                                                p, ap);      \
-  } while (0)
-  if (gl.V == 2) {
-    if (rows == 1) UQG_FACE_REG(2, 1);
-    else UQG_FACE_REG(2, 2);
-  } else {
-    if (rows == 1) UQG_FACE_REG(1, 1);
-    else UQG_FACE_REG(1, 2);
-  }
-#undef UQG_FACE_REG
+  if (gl.V == 2)
+    pcg_spmv_fv2d_kernel<2><<<dim3(gl.B, G), gl.T, smem, s>>>(N, gl, st, op, p, ap);
+  else
+    pcg_spmv_fv2d_kernel<1><<<dim3(gl.B, G), gl.T, smem, s>>>(N, gl, st, op, p, ap);
 }
 
 void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long long nnz,

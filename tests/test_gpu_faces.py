@@ -85,13 +85,9 @@ np.save(sys.argv[2], np.array(out, dtype=object), allow_pickle=True)
 _VARIANTS = {  # face SpMV variants (all must give the CSR bits)
     "reg": {},                                            # default: 2 lanes / thread
     "v4": {"UQG_FACE_V4": "1"},                           # 4 lanes / thread (LDG.256)
-    "reg2": {"UQG_FACE_ROWS": "2"},                       # 2 rows in flight
     "shfl": {"UQG_FACE_SHFL": "1"},                       # warp-shuffle neighbours
     "tma2": {"UQG_FACE_TMA": "2"},                        # TMA-banded
     "tma4": {"UQG_FACE_TMA": "4"},
-    "async2": {"UQG_FACE_ASYNC": "2"},                    # cp.async
-    "async4": {"UQG_FACE_ASYNC": "4"},
-    "pf": {"UQG_FACE_PREFETCH": "1"},                     # per-thread L2 prefetch
     "fixed": {"UQG_OCC_BLOCKS": "0"},                     # with_groups block sizing
 }
 
