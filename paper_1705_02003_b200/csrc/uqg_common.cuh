@@ -74,10 +74,6 @@ struct Geo {
   int B;          // blocks per group in the launch (set by with_groups)
   int gact;       // groups still running (with_groups), for occupancy-aware sizing
   int maxrow;     // longest graph row if known (0 = unknown): picks the unrolled SpMV
-  int sc;         // chunks per super-chunk (1 = no super level: chunks <= kMaxChunks)
-  int nsc;        // super-chunks (sc > 1)
-  int pstride;    // partial rows per group: chunks (+ nsc super-partials when sc > 1)
-  int tstride;    // tickets per group: 1 (+ nsc super-chunk tickets when sc > 1)
 };
 
 // UQG_LANES_PER_THREAD=1 forces V = 1 (tuning experiments only; V changes the
@@ -102,28 +98,12 @@ inline Geo make_geo(long long N, int S, int maxrow = 0) {
   g.R = g.T / g.Lp;
   g.tiles = (N + g.R - 1) / g.R;
   if (g.tiles < 1) g.tiles = 1;
-  // aim for >= 64 chunks of <= 8 tiles.  A block sweeps its chunks' tiles in
-  // order, so short chunks keep the rows all blocks of a group work on in one
-  // band (the +-m stencil neighbours are reused from L2 before eviction).
-  // Large N (> kMaxChunks chunks): consecutive chunks form super-chunks whose
-  // partials are summed (in chunk order) by the block completing the
-  // super-chunk, and the final stage sums the <= kMaxChunks super-partials -
-  // so the last block's serial work stays bounded.
+  // aim for >= 64 chunks of <= 8 tiles (small N), at most kMaxChunks (large N)
   long long ct = g.tiles / 64;
   ct = ct < 1 ? 1 : (ct > 8 ? 8 : ct);
+  if ((g.tiles + ct - 1) / ct > kMaxChunks) ct = (g.tiles + kMaxChunks - 1) / kMaxChunks;
   g.chunk_tiles = ct;
   g.chunks = (int)((g.tiles + ct - 1) / ct);
-  if (g.chunks > kMaxChunks) {
-    g.sc = (g.chunks + kMaxChunks - 1) / kMaxChunks;
-    g.nsc = (g.chunks + g.sc - 1) / g.sc;
-    g.pstride = g.chunks + g.nsc;
-    g.tstride = 1 + g.nsc;
-  } else {
-    g.sc = 1;
-    g.nsc = g.chunks;
-    g.pstride = g.chunks;
-    g.tstride = 1;
-  }
   g.B = g.chunks;
   g.gact = 1;
   return g;
@@ -255,15 +235,8 @@ __device__ __forceinline__ void stv(double* p, const double (&o)[V]) {
 // chunk, value, lane), and takes a ticket.  The block that completes the last
 // chunk of the group sums the chunk partials of each lane in a fixed order
 // (strided sequential sums, then the same binary tree) and returns true with
-// the total of value v, lane V*sl+j in red[(v*V + j)*T + sl].  With
-// super-chunks (geo.sc > 1) the block completing a super-chunk first sums its
-// chunk partials sequentially in chunk order into a super-partial, and the
-// final stage runs over the super-partials.  No floating-point atomics: the
-// result is a pure function of the inputs.
-//
-// Layout per group g: part rows [g*pstride + r][NV][S] (r < chunks: chunk
-// partials, then super-partials); tickets [g*tstride]: group ticket, then one
-// per super-chunk.
+// the total of value v, lane V*sl+j in red[(v*V + j)*T + sl].  No
+// floating-point atomics: the result is a pure function of the inputs.
 
 template <int NS>
 __device__ __forceinline__ void tree_rows(double* red, int T, int Lp, int R, int t) {
@@ -276,95 +249,12 @@ __device__ __forceinline__ void tree_rows(double* red, int T, int Lp, int R, int
   }
 }
 
-// Tickets of nk chunks (chunk0 + k*stride) whose partials are written and
-// fenced (all threads call after a __syncthreads).  Returns true in the one
-// block that completes the group, with the totals in red[].
-template <int NV, int V>
-__device__ bool finish_chunks(double* red, double* part, unsigned int* ticket, int g, int chunk0,
-                              int stride, int nk, const Geo& geo) {
-  constexpr int NS = NV * V;
-  const int t = threadIdx.x;
-  const int T = geo.T, Lp = geo.Lp, R = geo.R, L = geo.L, S = geo.S, C = geo.chunks;
-  unsigned int* gt = ticket + (size_t)g * geo.tstride;
-  double* gp = part + (size_t)g * geo.pstride * NV * S;
-  __shared__ int s_flag;
-  int rows = C, row0 = 0;
-  if (geo.sc == 1) {
-    if (t == 0) {
-      const unsigned int tk = atomicAdd(gt, (unsigned)nk);
-      s_flag = (tk + (unsigned)nk == (unsigned)C);
-    }
-    __syncthreads();
-    if (!s_flag) return false;
-  } else {
-    bool last = false;
-    for (int k = 0; k < nk; ++k) {
-      const int c = chunk0 + k * stride, si = c / geo.sc;
-      const int c_lo = si * geo.sc, c_hi = c_lo + geo.sc < C ? c_lo + geo.sc : C;
-      if (t == 0) {
-        const unsigned int tk = atomicAdd(gt + 1 + si, 1u);
-        s_flag = (tk + 1u == (unsigned)(c_hi - c_lo));
-      }
-      __syncthreads();
-      const int done_super = s_flag;
-      __syncthreads();
-      if (!done_super) continue;
-      __threadfence();
-      if (t < L) {  // super-partial: the super-chunk's partials in chunk order
-#pragma unroll
-        for (int v = 0; v < NV; ++v)
-#pragma unroll
-          for (int j = 0; j < V; ++j) {
-            double a = 0.0;
-            for (int cc = c_lo; cc < c_hi; ++cc) a += __ldcg(&gp[((size_t)cc * NV + v) * S + V * t + j]);
-            gp[((size_t)(C + si) * NV + v) * S + V * t + j] = a;
-          }
-      }
-      __threadfence();
-      __syncthreads();
-      if (t == 0) {
-        gt[1 + si] = 0u;
-        const unsigned int tk = atomicAdd(gt, 1u);
-        s_flag = (tk + 1u == (unsigned)geo.nsc);
-      }
-      __syncthreads();
-      if (s_flag) last = true;
-      __syncthreads();
-    }
-    if (!last) return false;
-    rows = geo.nsc;
-    row0 = C;
-  }
-  __threadfence();
-  const int sl = t % Lp, jr = t / Lp;
-  double acc[NS];
-#pragma unroll
-  for (int v = 0; v < NS; ++v) acc[v] = 0.0;
-  if (sl < L) {
-#pragma unroll 4
-    for (int cc = jr; cc < rows; cc += R) {
-#pragma unroll
-      for (int v = 0; v < NV; ++v)
-#pragma unroll
-        for (int j = 0; j < V; ++j)
-          acc[v * V + j] += __ldcg(&gp[((size_t)(row0 + cc) * NV + v) * S + V * sl + j]);
-    }
-  }
-  __syncthreads();  // red[] may still hold the caller's tree values
-#pragma unroll
-  for (int v = 0; v < NS; ++v) red[v * T + t] = acc[v];
-  __syncthreads();
-  tree_rows<NS>(red, T, Lp, R, t);
-  if (t == 0) gt[0] = 0u;  // ready for the next reduction on this counter
-  return true;
-}
-
 template <int NV, int V>
 __device__ bool reduce_lanes(const double (&val)[NV][V], double* red, double* part,
                              unsigned int* ticket, int g, int chunk, const Geo& geo) {
   constexpr int NS = NV * V;
   const int t = threadIdx.x;
-  const int T = geo.T, Lp = geo.Lp, R = geo.R, L = geo.L, S = geo.S;
+  const int T = geo.T, Lp = geo.Lp, R = geo.R, L = geo.L, S = geo.S, C = geo.chunks;
   __syncthreads();  // red[] may still be read by the previous chunk's tree
 #pragma unroll
   for (int v = 0; v < NV; ++v)
@@ -377,26 +267,53 @@ __device__ bool reduce_lanes(const double (&val)[NV][V], double* red, double* pa
     for (int v = 0; v < NV; ++v)
 #pragma unroll
       for (int j = 0; j < V; ++j)
-        part[(((size_t)g * geo.pstride + chunk) * NV + v) * S + V * t + j] =
-            red[(v * V + j) * T + t];
+        part[(((size_t)g * C + chunk) * NV + v) * S + V * t + j] = red[(v * V + j) * T + t];
   }
+  __shared__ int s_last;
   __threadfence();
   __syncthreads();
-  return finish_chunks<NV, V>(red, part, ticket, g, chunk, 1, 1, geo);
+  if (t == 0) {
+    unsigned int tk = atomicAdd(&ticket[g], 1u);
+    s_last = (tk == (unsigned)(C - 1));
+  }
+  __syncthreads();
+  if (!s_last) return false;
+  __threadfence();
+  const int sl = t % Lp, jr = t / Lp;
+  double acc[NS];
+#pragma unroll
+  for (int v = 0; v < NS; ++v) acc[v] = 0.0;
+  if (sl < L) {
+#pragma unroll 4
+    for (int cc = jr; cc < C; cc += R) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+          acc[v * V + j] += __ldcg(&part[(((size_t)g * C + cc) * NV + v) * S + V * sl + j]);
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < NS; ++v) red[v * T + t] = acc[v];
+  __syncthreads();
+  tree_rows<NS>(red, T, Lp, R, t);
+  if (t == 0) ticket[g] = 0u;  // ready for the next reduction on this counter
+  return true;
 }
 
 // reduce_lanes over a batch of nk chunks chunk0 + k*stride (k < nk) whose
 // per-thread values the caller has stored in red[((k*NV + v)*V + j)*T + t]:
-// one in-block tree for the whole batch (instead of one per chunk), then the
-// chunks' tickets.  Every partial and the final sums are computed exactly as
-// reduce_lanes<NV, V> computes them, so results are bit-identical (same result
-// layout in red).  red must hold max(nk, 1) * NV * V * T doubles.
+// one in-block tree for the whole batch (instead of one per chunk), one
+// ticket add of nk, then the final stage of reduce_lanes.  Every partial and
+// the final sums are computed exactly as reduce_lanes<NV, V> computes them,
+// so results are bit-identical (same result layout in red).  red must hold
+// max(nk, 1) * NV * V * T doubles.
 template <int NV, int V>
 __device__ bool reduce_lanes_batch(double* red, double* part, unsigned int* ticket, int g,
                                    int chunk0, int stride, int nk, const Geo& geo) {
   constexpr int NS = NV * V;
   const int t = threadIdx.x;
-  const int T = geo.T, Lp = geo.Lp, R = geo.R, L = geo.L, S = geo.S;
+  const int T = geo.T, Lp = geo.Lp, R = geo.R, L = geo.L, S = geo.S, C = geo.chunks;
   const int ns = nk * NS;
   __syncthreads();
   for (int st = R >> 1; st > 0; st >>= 1) {
@@ -411,25 +328,51 @@ __device__ bool reduce_lanes_batch(double* red, double* part, unsigned int* tick
       for (int v = 0; v < NV; ++v)
 #pragma unroll
         for (int j = 0; j < V; ++j)
-          part[(((size_t)g * geo.pstride + chunk0 + k * stride) * NV + v) * S + V * t + j] =
+          part[(((size_t)g * C + chunk0 + k * stride) * NV + v) * S + V * t + j] =
               red[((k * NV + v) * V + j) * T + t];
   }
+  __shared__ int s_last;
   __threadfence();
   __syncthreads();
-  return finish_chunks<NV, V>(red, part, ticket, g, chunk0, stride, nk, geo);
+  if (t == 0) {
+    unsigned int tk = atomicAdd(&ticket[g], (unsigned)nk);
+    s_last = (tk + (unsigned)nk == (unsigned)C);
+  }
+  __syncthreads();
+  if (!s_last) return false;
+  __threadfence();
+  const int sl = t % Lp, jr = t / Lp;
+  double acc[NS];
+#pragma unroll
+  for (int v = 0; v < NS; ++v) acc[v] = 0.0;
+  if (sl < L) {
+#pragma unroll 4
+    for (int cc = jr; cc < C; cc += R) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+          acc[v * V + j] += __ldcg(&part[(((size_t)g * C + cc) * NV + v) * S + V * sl + j]);
+    }
+  }
+  __syncthreads();  // the batch's tree values in red[] have been consumed
+#pragma unroll
+  for (int v = 0; v < NS; ++v) red[v * T + t] = acc[v];
+  __syncthreads();
+  tree_rows<NS>(red, T, Lp, R, t);
+  if (t == 0) ticket[g] = 0u;
+  return true;
 }
 
-// "last block of the group" without values (for state transitions); uses the
-// group ticket (slot 0 of the group's tickets).
-__device__ __forceinline__ bool last_block(unsigned int* ticket, int g, int B, int tstride) {
+// "last block of the group" without values (for state transitions).
+__device__ __forceinline__ bool last_block(unsigned int* ticket, int g, int B) {
   __shared__ int s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    unsigned int* gt = ticket + (size_t)g * tstride;
-    unsigned int tk = atomicAdd(gt, 1u);
+    unsigned int tk = atomicAdd(&ticket[g], 1u);
     s_last = (tk == (unsigned)(B - 1));
-    if (s_last) *gt = 0u;
+    if (s_last) ticket[g] = 0u;
   }
   __syncthreads();
   return s_last;

@@ -690,7 +690,7 @@ __global__ void __launch_bounds__(256, 3) pcg_dir_kernel(long long N, Geo geo, P
       }
     }
   }
-  if (state == kFinishing && last_block(st.ticket, g, gridDim.x, geo.tstride) && t == 0) {
+  if (state == kFinishing && last_block(st.ticket, g, gridDim.x) && t == 0) {
     st.done[g] = kDone;
     atomicAdd(st.ndone, 1);
   }
@@ -1374,13 +1374,12 @@ __device__ bool reduce_lanes_c(const double (&val)[NV][V], double* red, double* 
     for (int v = 0; v < NV; ++v)
 #pragma unroll
       for (int j = 0; j < V; ++j)
-        part[(((size_t)g * geo.pstride + chunk) * NV + v) * S + V * t + j] =
-            red[(v * V + j) * T + t];
+        part[(((size_t)g * C + chunk) * NV + v) * S + V * t + j] = red[(v * V + j) * T + t];
   }
   __threadfence();
   consumer_sync();
-  if (t == 0) {  // (no super-chunks: the host selects this kernel only when geo.sc == 1)
-    unsigned int tk = atomicAdd(&ticket[(size_t)g * geo.tstride], 1u);
+  if (t == 0) {
+    unsigned int tk = atomicAdd(&ticket[g], 1u);
     *s_last = (tk == (unsigned)(C - 1));
   }
   consumer_sync();
@@ -1397,15 +1396,14 @@ __device__ bool reduce_lanes_c(const double (&val)[NV][V], double* red, double* 
       for (int v = 0; v < NV; ++v)
 #pragma unroll
         for (int j = 0; j < V; ++j)
-          acc[v * V + j] +=
-              __ldcg(&part[(((size_t)g * geo.pstride + cc) * NV + v) * S + V * sl + j]);
+          acc[v * V + j] += __ldcg(&part[(((size_t)g * C + cc) * NV + v) * S + V * sl + j]);
     }
   }
 #pragma unroll
   for (int v = 0; v < NS; ++v) red[v * T + t] = acc[v];
   consumer_sync();
   tree_rows_c<NS>(red, T, Lp, R, t);
-  if (t == 0) ticket[(size_t)g * geo.tstride] = 0u;
+  if (t == 0) ticket[g] = 0u;
   return true;
 }
 
@@ -1982,7 +1980,7 @@ void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long lo
   }
   if (mode && gl.V == 2 && aligned && gl.maxrow >= 1 && gl.maxrow <= 8) {
     // the metadata variant needs R + 1 <= T and R * ML <= 2T (S >= 8)
-    if (mode == 4 && gl.T == 256 && gl.sc == 1) {
+    if (mode == 4 && gl.T == 256) {
       if (gl.maxrow <= 5)
         launch_spmv_ws<5>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
       else
