@@ -100,7 +100,11 @@ inline Geo make_geo(long long N, int S, int maxrow = 0) {
   if (g.tiles < 1) g.tiles = 1;
   // aim for >= 64 chunks of <= 8 tiles (small N), at most kMaxChunks (large N)
   long long ct = g.tiles / 64;
-  ct = ct < 1 ? 1 : (ct > 8 ? 8 : ct);
+  static const int ct_max = [] {  // UQG_CHUNK_TILES (tuning only: changes the trees)
+    const char* e = getenv("UQG_CHUNK_TILES");
+    return e ? atoi(e) : 8;
+  }();
+  ct = ct < 1 ? 1 : (ct > ct_max ? ct_max : ct);
   if ((g.tiles + ct - 1) / ct > kMaxChunks) ct = (g.tiles + kMaxChunks - 1) / kMaxChunks;
   g.chunk_tiles = ct;
   g.chunks = (int)((g.tiles + ct - 1) / ct);
