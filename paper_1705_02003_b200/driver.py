@@ -42,17 +42,26 @@ def sample_set(cfg: StudyConfig) -> np.ndarray:
 
 
 def adaptive_run(cfg: StudyConfig, solver: EnsembleSolver | None = None, shard=None,
-                 max_levels: int | None = None, device_keys: bool = False):
+                 max_levels: int | None = None, device_keys: bool = False,
+                 residual_sink=None):
     """Run the grouped adaptive loop; returns (records, stop_reason, grid).
 
     ``shard``: optional callable(plan, coords_by_id) -> (iters, qois, notes)
     replacing ``solver.solve_plan`` (multi-GPU sharded solve + allgather).
     ``device_keys``: evaluate the iteration surrogate on the GPU
     (``SparseGrid.evaluate_device``; bit-identical keys on this channel).
+    ``residual_sink(level, ensemble, history)``: per-ensemble lane residual
+    histories, as the reference's ``adaptive_run(residual_sink=...)``
+    (``report.residual_sink`` writes the reference's CSVs).
     """
     if solver is None and shard is None:
         solver = cfg.make_solver()
-    solve = shard or solver.solve_plan
+    if residual_sink is not None:
+        if shard is not None:
+            raise ValueError("residual histories are recorded by the single-device solve only")
+        solve = lambda plan, coords: solver.solve_plan(plan, coords, residual_sink)  # noqa: E731
+    else:
+        solve = shard or solver.solve_plan
     S = cfg.ensemble_size
     grid = SparseGrid(cfg.n_modes)
     batch = grid.add_initial_levels(cfg.initial_level)

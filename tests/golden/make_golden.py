@@ -322,6 +322,36 @@ def fv2d_small():
                         row_offsets=mesh.row_offsets, col_indices=mesh.col_indices)
 
 
+def refrun_outputs():
+    """The reference CLI's own output files for a small pde_test1 study
+    (``cli.py:116-131`` residual dump + ``harness.py:762-797`` emission):
+    S=4, n_max=60, 6^3 cells, surrogate grouping.  Pins report.py's formats and,
+    through the device study, the per-sample iteration table byte for byte."""
+    import shutil
+    import tempfile
+
+    from uqgroup import cli
+
+    dst = HERE / "refrun_pde_test1"
+    if dst.exists():
+        shutil.rmtree(dst)
+    dst.mkdir()
+    with tempfile.TemporaryDirectory() as tmp:
+        rc = cli.main(["run", "--problem", "pde_test1", "--strategies", "sur", "--S", "4",
+                       "--n-max", "60", "--mesh-cells", "6", "--dump-residuals",
+                       "--out-dir", tmp])
+        assert rc in (0, 2)  # 2: stopped on the budget, outputs complete
+        for name in ("iterations_by_level.csv", "residuals_level1_ens0.csv",
+                     "residuals_level1_ens11.csv", "residuals_level2_ens0.csv"):
+            shutil.copy(Path(tmp) / name, dst / name)
+        n = len(list(Path(tmp).glob("residuals_level*_ens*.csv")))
+        (dst / "README").write_text(
+            "Outputs of the reference CLI (uqgroup run --problem pde_test1 --strategies sur "
+            "--S 4 --n-max 60 --mesh-cells 6 --dump-residuals), generated by "
+            f"tests/golden/make_golden.py:refrun_outputs; {n} residual files in the run, "
+            "3 kept.\n")
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["pcg", "special", "grouping", "eigen", "fv2d", "c1", "c2"]
     if "pcg" in which:
@@ -339,6 +369,8 @@ if __name__ == "__main__":
         (HERE / "c1_adaptive.json").write_text(json.dumps(doc))
     if "c2" in which:
         c2_group()
+    if "refrun" in which:
+        refrun_outputs()
     if "fem3d" in which:
         fem3d_cases()
     for preset in ("pde_test1", "pde_test2"):

@@ -1,0 +1,64 @@
+"""The device study emits the reference CLI's run files.
+
+The reference's pde_test1 preset at S=4, n_max=60, 6^3 cells is run through
+driver.adaptive_run with a report.residual_sink.  The per-sample iteration
+table must have the reference's rows (levels, sample ids, order) with counts
+inside the preset's rounding envelope (+-1: the reference's own counts move by
+that much under a different dot-product order, DESIGN.md "Rounding
+envelope"); the residual histories of lockstep lanes match its values to
+rounding; and two device runs must emit identical bytes (the reference's
+acceptance criterion 8).  Byte-exact formatting is pinned on the CPU
+(tests/test_report_cpu.py).
+"""
+
+import csv
+import dataclasses
+
+import numpy as np
+import pytest
+
+import paper_1705_02003_b200 as uq
+from paper_1705_02003_b200.driver import adaptive_run
+from paper_1705_02003_b200.report import residual_sink, write_iterations_by_level
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+REF = GOLDEN / "refrun_pde_test1"
+
+
+def _run(out):
+    cfg = dataclasses.replace(uq.PRESETS_3D["pde_test1"], cells=6, n_max=60)
+    records, stop, _ = adaptive_run(cfg, residual_sink=residual_sink(out, cfg.ensemble_size))
+    write_iterations_by_level(records, out)
+    return stop
+
+
+def test_device_study_emits_reference_files(tmp_path):
+    a, b = tmp_path / "a", tmp_path / "b"
+    assert _run(a) == "budget_exhausted"
+    mine = list(csv.reader((a / "iterations_by_level.csv").read_text().splitlines()))
+    ref = list(csv.reader((REF / "iterations_by_level.csv").read_text().splitlines()))
+    assert mine[0] == ref[0] and len(mine) == len(ref)
+    for m, r in zip(mine[1:], ref[1:]):
+        assert m[:3] == r[:3]                           # run, level, sample id
+        assert abs(int(m[3]) - int(r[3])) <= 1          # iterations (envelope)
+        assert (m[4] == "") == (r[4] == "")             # predicted on the same levels
+        if r[4]:
+            assert abs(float(m[4]) - float(r[4])) <= 2.0
+    exact = sum(m[3] == r[3] for m, r in zip(mine[1:], ref[1:]))
+    assert exact >= 0.8 * (len(ref) - 1)
+    for name in ("residuals_level1_ens0.csv", "residuals_level1_ens11.csv"):
+        m = list(csv.reader((a / name).read_text().splitlines()))
+        r = list(csv.reader((REF / name).read_text().splitlines()))
+        assert m[0] == r[0]
+        n = min(len(m), len(r))  # the final iteration may differ by one (envelope)
+        mv = np.array([[float(v) for v in row] for row in m[1:n]])
+        rv = np.array([[float(v) for v in row] for row in r[1:n]])
+        assert np.array_equal(mv[:, 0], rv[:, 0])
+        np.testing.assert_allclose(mv[:, 1:], rv[:, 1:], rtol=1e-6, atol=1e-12 * rv[0, 1:].max())
+    _run(b)
+    files = sorted(p.name for p in a.iterdir())
+    assert files == sorted(p.name for p in b.iterdir()) and len(files) > 10
+    for name in files:
+        assert (a / name).read_bytes() == (b / name).read_bytes(), name
