@@ -88,7 +88,8 @@ __global__ void __launch_bounds__(256, 4) probe(Args a) {
 // blocks take chunks b, b+B, ...; per-thread p.Ap accumulated per chunk.
 // RED = 0: the per-chunk accumulators go straight to global memory;
 // RED = 1: + the library's batched in-block tree (8 chunks per tree) and a
-// per-group atomic ticket per batch (no final stage).
+// per-group atomic ticket per batch (no final stage); RED = 2: + the library's
+// exact arithmetic (separate roundings, CSR term order, predicated terms).
 template <int RED>
 __global__ void __launch_bounds__(256, 4) probe_chunked(Args a, int CT, double* part,
                                                         unsigned* ticket) {
@@ -118,8 +119,27 @@ __global__ void __launch_bounds__(256, 4) probe_chunked(Args a, int CT, double* 
         if (j0 > 0) ps = ld2(pg + (row - 1) * S);
         if (j0 < m - 1) pn = ld2(pg + (row + 1) * S);
         double2 y;
-        y.x = (tw.x + te.x) * pc.x - tw.x * pw.x - te.x * pe.x - ps.x - pn.x;
-        y.y = (tw.y + te.y) * pc.y - tw.y * pw.y - te.y * pe.y - ps.y - pn.y;
+        if (RED < 2) {
+          y.x = (tw.x + te.x) * pc.x - tw.x * pw.x - te.x * pe.x - ps.x - pn.x;
+          y.y = (tw.y + te.y) * pc.y - tw.y * pw.y - te.y * pe.y - ps.y - pn.y;
+        } else {  // the library's exact CSR-order arithmetic (separate roundings)
+          const double ay = 1.0;
+          double d = __dadd_rn(__dadd_rn(__dadd_rn(tw.x, te.x), ay), ay), a = 0.0;
+          if (i0 > 0) a = __dadd_rn(a, __dmul_rn(-tw.x, pw.x));
+          if (j0 > 0) a = __dadd_rn(a, __dmul_rn(-ay, ps.x));
+          a = __dadd_rn(a, __dmul_rn(d, pc.x));
+          if (j0 < m - 1) a = __dadd_rn(a, __dmul_rn(-ay, pn.x));
+          if (i0 < m - 1) a = __dadd_rn(a, __dmul_rn(-te.x, pe.x));
+          y.x = a;
+          d = __dadd_rn(__dadd_rn(__dadd_rn(tw.y, te.y), ay), ay);
+          a = 0.0;
+          if (i0 > 0) a = __dadd_rn(a, __dmul_rn(-tw.y, pw.y));
+          if (j0 > 0) a = __dadd_rn(a, __dmul_rn(-ay, ps.y));
+          a = __dadd_rn(a, __dmul_rn(d, pc.y));
+          if (j0 < m - 1) a = __dadd_rn(a, __dmul_rn(-ay, pn.y));
+          if (i0 < m - 1) a = __dadd_rn(a, __dmul_rn(-te.y, pe.y));
+          y.y = a;
+        }
         *reinterpret_cast<double2*>(apg + row * S) = y;
         acc.x = fma(pc.x, y.x, acc.x);
         acc.y = fma(pc.y, y.y, acc.y);
@@ -131,7 +151,7 @@ __global__ void __launch_bounds__(256, 4) probe_chunked(Args a, int CT, double* 
         red[(2 * k + 1) * T + t] = acc.y;
       }
     }
-    if (RED == 1) {
+    if (RED >= 1) {
       __syncthreads();
       for (int st = R >> 1; st > 0; st >>= 1) {
         if (rr < st)
@@ -224,8 +244,10 @@ int main(int argc, char** argv) {
   for (int b : bpg) {
     const float t4 = run_chunked<0>(a, ct, b, 20, part, ticket);
     const float t5 = run_chunked<1>(a, ct, b, 20, part, ticket);
-    printf("blocks/group %3d (chunks of %d tiles): chunked %.0f  +batched tree %.0f GB/s\n", b,
-           ct, bytes / t4 / 1e6, bytes / t5 / 1e6);
+    const float t6 = run_chunked<2>(a, ct, b, 20, part, ticket);
+    printf("blocks/group %3d (chunks of %d tiles): chunked %.0f  +batched tree %.0f  "
+           "+exact arithmetic %.0f GB/s\n", b, ct, bytes / t4 / 1e6, bytes / t5 / 1e6,
+           bytes / t6 / 1e6);
   }
   return 0;
 }
