@@ -12,11 +12,10 @@ constexpr int kDone = 2;
 
 // Band hint for banded graphs (stencils): the columns of tile rows [r0, r0+R)
 // lie in nb row bands [r0 + start[b], r0 + start[b] + R + extra[b]).  With a
-// hint, the PCG SpMV stages those p bands (and the tile's values, columns and
-// row offsets) in shared memory by bulk async copies; a column outside every
-// band falls back to a global load, so any hint gives identical results.
-// padded != 0 promises >= 4 ints of readable slack after row_offsets[N] and
-// col_indices[nnz-1] (bulk copies move 16-byte aligned spans).
+// hint, the TMA CSR SpMV bulk-prefetches those p bands into L2 when it issues
+// the tile's values (the hint only moves data earlier: any hint gives
+// identical results).  padded != 0 promises >= 4 ints of readable slack after
+// row_offsets[N] and col_indices[nnz-1].
 constexpr int kMaxBands = 9;
 struct BandHint {
   int nb;

@@ -395,113 +395,6 @@ __global__ void __launch_bounds__(128, 5) pcg_spmv_fv2d4_kernel(
   face_spmv_body<4>(N, geo, st, op, p, ap);
 }
 
-// Register face SpMV with the +-1 neighbours shared through warp shuffles: a
-// warp covers RW = 32 / Lp consecutive rows, so p[row - 1] / p[row + 1] are
-// the centre values of the neighbouring lanes except at the warp's first /
-// last row, which load them.  Cuts the L1/L2 requests for p by 2 of 5 per row
-// (the kernel is bound by L2 request throughput, not DRAM).  Needs Lp <= 32.
-// Identical arithmetic, chunks and reduction: identical bits.
-template <int V>
-__device__ __forceinline__ void shfl_v(double (&o)[V], const double (&v)[V], int delta, bool up) {
-#pragma unroll
-  for (int j = 0; j < V; ++j)
-    o[j] = up ? __shfl_up_sync(0xffffffffu, v[j], delta) : __shfl_down_sync(0xffffffffu, v[j], delta);
-}
-
-template <int V>
-__global__ void __launch_bounds__(256, 4) pcg_spmv_fv2d_shfl_kernel(long long N, Geo geo,
-                                                                    PcgState st, Fv2dOp op,
-                                                                    const double* __restrict__ p,
-                                                                    double* __restrict__ ap) {
-  extern __shared__ double red[];
-  const int g = blockIdx.y, t = threadIdx.x;
-  if (st.done[g] != kRunning) return;
-  const int Lp = geo.Lp, sl = t % Lp, rr = t / Lp, S = geo.S, R = geo.R, m = op.m;
-  const int n = (int)N, B = gridDim.x, T = geo.T;
-  const int RW = 32 / Lp, wr = rr % RW;  // rows per warp, this row's place in the warp
-  const bool lane_ok = sl < geo.L;
-  const size_t base = (size_t)g * N * S + V * sl;
-  const double* pg = p + base;
-  double* apg = ap + base;
-  const size_t fo = (size_t)g * (N + m) * S + V * sl;
-  const double* txg = op.tx + fo;
-  const double* tyg = op.ty ? op.ty + fo : nullptr;
-  const int ct = (int)geo.chunk_tiles, tiles = (int)geo.tiles;
-  for (int c0 = blockIdx.x; c0 < geo.chunks; c0 += kFaceBatch * B) {
-    int nk = (geo.chunks - 1 - c0) / B + 1;
-    if (nk > kFaceBatch) nk = kFaceBatch;
-    for (int k = 0; k < nk; ++k) {
-      const int chunk = c0 + k * B;
-      double acc[V] = {};
-      int tile = chunk * ct, tend = tile + ct;
-      if (tend > tiles) tend = tiles;
-      int row = tile * R + rr;
-      int i0 = row / m, j0 = row - i0 * m;
-      for (; tile < tend; ++tile, row += R) {  // warp-uniform trip count
-        const bool ok = lane_ok && row < n;
-        FaceRow<V> f;
-        f.w = i0 > 0;
-        f.s = j0 > 0;
-        f.n = j0 < m - 1;
-        f.e = i0 < m - 1;
-#pragma unroll
-        for (int j = 0; j < V; ++j) f.pc[j] = 0.0;
-        if (ok) {
-          ldgv<V>(txg + row * S, f.tw);
-          ldgv<V>(txg + (row + m) * S, f.te);
-          if (tyg) {
-            ldgv<V>(tyg + (row + i0) * S, f.ts);
-            ldgv<V>(tyg + (row + i0 + 1) * S, f.tn);
-          } else {
-#pragma unroll
-            for (int j = 0; j < V; ++j) f.ts[j] = f.tn[j] = op.a_y;
-          }
-          if (f.w) ldgv<V>(pg + (row - m) * S, f.pw);
-          ldgv<V>(pg + row * S, f.pc);
-          if (f.e) ldgv<V>(pg + (row + m) * S, f.pe);
-          if (f.s && wr == 0) ldgv<V>(pg + (row - 1) * S, f.ps);
-          if (f.n && (wr == RW - 1 || row + 1 >= n)) ldgv<V>(pg + (row + 1) * S, f.pn);
-        }
-        double up[V], dn[V];
-        shfl_v<V>(up, f.pc, Lp, true);    // p[row - 1] from the lane one row up
-        shfl_v<V>(dn, f.pc, Lp, false);   // p[row + 1] from the lane one row down
-        if (ok) {
-          if (wr != 0) {
-#pragma unroll
-            for (int j = 0; j < V; ++j) f.ps[j] = up[j];
-          }
-          if (wr != RW - 1 && row + 1 < n) {
-#pragma unroll
-            for (int j = 0; j < V; ++j) f.pn[j] = dn[j];
-          }
-          double y[V];
-          f.apply(y, acc);
-          stv<V>(apg + row * S, y);
-        }
-        j0 += R;
-        while (j0 >= m) {
-          j0 -= m;
-          ++i0;
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < V; ++j) red[(k * V + j) * T + t] = acc[j];
-    }
-    if (!reduce_lanes_batch<1, V>(red, st.part, st.ticket, g, c0, B, nk, geo)) continue;
-    if (t < geo.L) {
-#pragma unroll
-      for (int j = 0; j < V; ++j) {
-        const size_t l = (size_t)g * S + V * t + j;
-        const double pap = red[j * geo.T + t];
-        const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
-        st.frozen[l] = fr;
-        st.alpha[l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
-      }
-    }
-    if (t == 0) st.it[g] += 1;
-  }
-}
-
 template <int V>
 __global__ void __launch_bounds__(256) spmv_fv2d_kernel(long long N, Geo geo, Fv2dOp op,
                                                         const double* __restrict__ x,
@@ -1029,306 +922,6 @@ __global__ void __launch_bounds__(256, MINB) pcg_spmv_tma_kernel(long long N, lo
   }
 }
 
-// Variant with the tile metadata (row offsets, column indices) also staged in
-// shared memory ahead of use by all threads, so a row's dependent chain is
-// only the p gather (row offsets of tile i+2 and columns of tile i+1 are
-// loaded before tile i is computed and stored after it).  Identical results.
-template <int ML>
-__global__ void __launch_bounds__(256, 3) pcg_spmv_tma_meta_kernel(
-    long long N, long long nnz, Geo geo, PcgState st, const int* __restrict__ ro,
-    const int* __restrict__ ci, const double* __restrict__ vals, const double* __restrict__ p,
-    double* __restrict__ ap) {
-  constexpr int V = 2;
-  extern __shared__ __align__(128) double red[];
-  const int g = blockIdx.y, t = threadIdx.x;
-  if (st.done[g] != kRunning) return;
-  const int S = geo.S, R = geo.R, T = geo.T;
-  const int stage_doubles = R * ML * S;
-  const int ro_stride = (R + 2) & ~1, col_stride = R * ML;
-  double* stage = red + V * T;
-  int* ro_s = reinterpret_cast<int*>(stage + kStages * stage_doubles);
-  int* col_s = ro_s + kStages * ro_stride;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(col_s + kStages * col_stride);
-  const double* vg = vals + (size_t)g * nnz * S;
-  const int n_tiles = block_tile_count(geo);
-  const int ct = (int)geo.chunk_tiles;
-  const long long tiles = geo.tiles;
-
-  auto tile_of = [&](int i) -> long long {
-    const int j = i / ct;
-    return ((long long)blockIdx.x + (long long)j * gridDim.x) * ct + (i - j * ct);
-  };
-  auto nrows = [&](long long tile) -> int {
-    const long long n = N - tile * R;
-    return n < R ? (int)n : R;
-  };
-  auto issue = [&](int i, int k0, int k1) {  // thread 0 only
-    const uint32_t bytes = (uint32_t)(k1 - k0) * (uint32_t)S * 8u;
-    uint64_t* bar = &bars[i % kStages];
-    fence_proxy_async();
-    mbar_expect_tx(bar, bytes);
-    if (bytes) bulk_g2s(stage + (i % kStages) * stage_doubles, vg + (size_t)k0 * S, bytes, bar);
-  };
-
-  // prologue: metadata of tiles 0, 1 and columns of tile 0; bulk copies 0..kStages-1
-  if (t == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
-    fence_mbar_init();
-  }
-  for (int i = 0; i < 2 && i < n_tiles; ++i) {
-    const long long tl = tile_of(i);
-    if (t <= nrows(tl)) ro_s[(i % kStages) * ro_stride + t] = __ldg(&ro[tl * R + t]);
-  }
-  __syncthreads();
-  if (n_tiles > 0) {
-    const int nr = nrows(tile_of(0));
-    const int k0 = ro_s[0], cnt = ro_s[nr] - k0;
-    for (int q = t; q < cnt; q += T) col_s[q] = __ldg(&ci[k0 + q]);
-  }
-  if (t == 0) {
-    for (int i = 0; i < kStages && i < n_tiles; ++i) {
-      const long long tl = tile_of(i);
-      const int nr = nrows(tl);
-      if (i < 2) {
-        issue(i, ro_s[(i % kStages) * ro_stride], ro_s[(i % kStages) * ro_stride + nr]);
-      } else {
-        issue(i, __ldg(&ro[tl * R]), __ldg(&ro[tl * R + nr]));
-      }
-    }
-  }
-  __syncthreads();
-
-  const int sl = t % geo.Lp, rr = t / geo.Lp;
-  const size_t base = (size_t)g * N * S + V * sl;
-  const double* pg = p + base;
-  double acc[1][V] = {};
-  long long tile = n_tiles > 0 ? tile_of(0) : 0;
-  long long tile1 = n_tiles > 1 ? tile_of(1) : 0;
-  for (int i = 0; i < n_tiles; ++i) {
-    const int s0 = i % kStages, s1 = (i + 1) % kStages, s2 = (i + 2) % kStages;
-    const long long tile2 = i + 2 < n_tiles ? tile_of(i + 2) : 0;
-    // prefetch: row offsets of tile i+2, columns of tile i+1, value range of i+kStages
-    int ro_next = 0, col_next[2] = {0, 0};
-    if (i + 2 < n_tiles && t <= nrows(tile2)) ro_next = __ldg(&ro[tile2 * R + t]);
-    int cnt1 = 0;
-    if (i + 1 < n_tiles) {
-      const int* rs1 = ro_s + s1 * ro_stride;
-      const int k01 = rs1[0];
-      cnt1 = rs1[nrows(tile1)] - k01;
-#pragma unroll
-      for (int u = 0; u < 2; ++u)
-        if (t + u * T < cnt1) col_next[u] = __ldg(&ci[k01 + t + u * T]);
-    }
-    int kn0 = 0, kn1 = 0;
-    if (t == 0 && i + kStages < n_tiles) {
-      const long long tl3 = tile_of(i + kStages);
-      kn0 = __ldg(&ro[tl3 * R]);
-      kn1 = __ldg(&ro[tl3 * R + nrows(tl3)]);
-    }
-    mbar_wait(&bars[s0], (uint32_t)((i / kStages) & 1));
-    if (sl < geo.L && rr < nrows(tile)) {
-      const long long row = tile * R + rr;
-      const int* rs = ro_s + s0 * ro_stride;
-      const int* cs = col_s + s0 * col_stride;
-      const int kt0 = rs[0];
-      const int k0 = rs[rr] - kt0, len = rs[rr + 1] - rs[rr];
-      const double* sv = stage + s0 * stage_doubles + (size_t)k0 * S + V * sl;
-      int c[ML];
-#pragma unroll
-      for (int e = 0; e < ML; ++e) c[e] = e < len ? cs[k0 + e] : 0;
-      double b[ML][V];
-#pragma unroll
-      for (int e = 0; e < ML; ++e)
-        if (e < len) ldgv<V>(pg + (size_t)c[e] * S, b[e]);
-      double y[V] = {0.0, 0.0};
-#pragma unroll
-      for (int e = 0; e < ML; ++e) {
-        if (e < len) {
-          const double2 a = *reinterpret_cast<const double2*>(sv + (size_t)e * S);
-          y[0] = __dadd_rn(y[0], __dmul_rn(a.x, b[e][0]));
-          y[1] = __dadd_rn(y[1], __dmul_rn(a.y, b[e][1]));
-        }
-      }
-      stv<V>(ap + base + row * S, y);
-      double pv[V];
-      ldgv<V>(pg + row * S, pv);
-#pragma unroll
-      for (int j = 0; j < V; ++j) acc[0][j] = __fma_rn(pv[j], y[j], acc[0][j]);
-    }
-    if (i + 2 < n_tiles && t <= nrows(tile2)) ro_s[s2 * ro_stride + t] = ro_next;
-#pragma unroll
-    for (int u = 0; u < 2; ++u)
-      if (t + u * T < cnt1) col_s[s1 * col_stride + t + u * T] = col_next[u];
-    __syncthreads();  // stage s0 consumed; metadata of tiles i+1, i+2 visible
-    if (t == 0 && i + kStages < n_tiles) issue(i + kStages, kn0, kn1);
-    const bool chunk_end = ((i + 1) % ct == 0) || (tile == tiles - 1);
-    if (chunk_end) {
-      const int chunk = (int)(tile / ct);
-      if (reduce_lanes<1, V>(acc, red, st.part, st.ticket, g, chunk, geo)) {
-        if (t < geo.L) {
-#pragma unroll
-          for (int j = 0; j < V; ++j) {
-            const size_t l = (size_t)g * S + V * t + j;
-            const double pap = red[j * geo.T + t];
-            const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
-            st.frozen[l] = fr;
-            st.alpha[l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
-          }
-        }
-        if (t == 0) st.it[g] += 1;
-      }
-      acc[0][0] = acc[0][1] = 0.0;
-    }
-    tile = tile1;
-    tile1 = tile2;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Paired variant: a step covers two consecutive tiles of a chunk (one bulk
-// copy of 2R rows' values, 2 stages), and every thread computes its row in
-// both tiles with all gathers of both rows issued before the ordered sums -
-// two independent dependent-load chains per thread and half the CTA barriers
-// per row.  The per-thread accumulation still runs tile by tile, so results
-// are identical.
-constexpr int kPairStages = 2;
-
-template <int ML>
-__global__ void __launch_bounds__(256, 2) pcg_spmv_pair_kernel(
-    long long N, long long nnz, Geo geo, PcgState st, const int* __restrict__ ro,
-    const int* __restrict__ ci, const double* __restrict__ vals, const double* __restrict__ p,
-    double* __restrict__ ap, BandHint bh) {
-  constexpr int V = 2;
-  extern __shared__ __align__(128) double red[];
-  const int g = blockIdx.y, t = threadIdx.x;
-  if (st.done[g] != kRunning) return;
-  const int S = geo.S, R = geo.R;
-  const int stage_doubles = 2 * R * ML * S;
-  double* stage = red + V * geo.T;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stage + kPairStages * stage_doubles);
-  const double* vg = vals + (size_t)g * nnz * S;
-  const double* pg_all = p + (size_t)g * N * S;
-  const int n_tiles = block_tile_count(geo);
-  const int ct = (int)geo.chunk_tiles;
-  const long long tiles = geo.tiles;
-  auto tile_of = [&](int i) -> long long {
-    const int j = i / ct;
-    return ((long long)blockIdx.x + (long long)j * gridDim.x) * ct + (i - j * ct);
-  };
-  // tiles in the step starting at block-tile index i: 2 if tile i+1 is in the same chunk
-  auto step_len = [&](int i) -> int {
-    return (i + 1 < n_tiles && (i % ct) + 1 < ct) ? 2 : 1;
-  };
-  auto issue = [&](int k, int i) {  // thread 0: step k starts at block-tile i
-    const int u = step_len(i);
-    const long long r0 = tile_of(i) * R;
-    long long r1 = r0 + (long long)u * R;
-    r1 = r1 < N ? r1 : N;
-    const int k0 = __ldg(&ro[r0]), k1 = __ldg(&ro[r1]);
-    const uint32_t bytes = (uint32_t)(k1 - k0) * (uint32_t)S * 8u;
-    uint64_t* bar = &bars[k % kPairStages];
-    fence_proxy_async();
-    mbar_expect_tx(bar, bytes);
-    if (bytes) bulk_g2s(stage + (k % kPairStages) * stage_doubles, vg + (size_t)k0 * S, bytes, bar);
-#pragma unroll
-    for (int b = 0; b < kMaxBands; ++b) {
-      if (b < bh.nb) {
-        long long lo = r0 + bh.start[b], hi = lo + (long long)u * R + bh.extra[b];
-        lo = lo < 0 ? 0 : lo;
-        hi = hi > N ? N : hi;
-        if (hi > lo) bulk_prefetch_l2(pg_all + lo * S, (uint32_t)(hi - lo) * S * 8u);
-      }
-    }
-    return i + u;
-  };
-  int next_issue_tile = 0, next_issue_step = 0;
-  if (t == 0) {
-    for (int s = 0; s < kPairStages; ++s) mbar_init(&bars[s], 1);
-    fence_mbar_init();
-    while (next_issue_step < kPairStages && next_issue_tile < n_tiles)
-      next_issue_tile = issue(next_issue_step++, next_issue_tile);
-  }
-  __syncthreads();
-
-  const int sl = t % geo.Lp, rr = t / geo.Lp;
-  const size_t base = (size_t)g * N * S + V * sl;
-  const double* pg = p + base;
-  double acc[1][V] = {};
-  int i = 0;
-  for (int k = 0; i < n_tiles; ++k) {
-    const int u = step_len(i);
-    const long long tile = tile_of(i);
-    const int s = k % kPairStages;
-    mbar_wait(&bars[s], (uint32_t)((k / kPairStages) & 1));
-    if (sl < geo.L) {
-      const long long r0 = tile * R;
-      const int kt0 = __ldg(&ro[r0]);
-      int c[2][ML], len[2], kr[2];
-      bool ok[2];
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const long long row = r0 + (long long)q * R + rr;
-        ok[q] = q < u && row < N;
-        kr[q] = ok[q] ? __ldg(&ro[row]) : 0;
-        len[q] = ok[q] ? __ldg(&ro[row + 1]) - kr[q] : 0;
-      }
-#pragma unroll
-      for (int q = 0; q < 2; ++q)
-#pragma unroll
-        for (int e = 0; e < ML; ++e) c[q][e] = e < len[q] ? __ldg(&ci[kr[q] + e]) : 0;
-      double b[2][ML][V];
-#pragma unroll
-      for (int q = 0; q < 2; ++q)
-#pragma unroll
-        for (int e = 0; e < ML; ++e)
-          if (e < len[q]) ldgv<V>(pg + (size_t)c[q][e] * S, b[q][e]);
-      double pv[2][V];
-#pragma unroll
-      for (int q = 0; q < 2; ++q)
-        if (ok[q]) ldgv<V>(pg + (size_t)(r0 + (long long)q * R + rr) * S, pv[q]);
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        if (!ok[q]) continue;
-        const double* sv = stage + s * stage_doubles + (size_t)(kr[q] - kt0) * S + V * sl;
-        double y[V] = {0.0, 0.0};
-#pragma unroll
-        for (int e = 0; e < ML; ++e) {
-          if (e < len[q]) {
-            const double2 a = *reinterpret_cast<const double2*>(sv + (size_t)e * S);
-            y[0] = __dadd_rn(y[0], __dmul_rn(a.x, b[q][e][0]));
-            y[1] = __dadd_rn(y[1], __dmul_rn(a.y, b[q][e][1]));
-          }
-        }
-        stv<V>(ap + base + (size_t)(r0 + (long long)q * R + rr) * S, y);
-#pragma unroll
-        for (int j = 0; j < V; ++j) acc[0][j] = __fma_rn(pv[q][j], y[j], acc[0][j]);
-      }
-    }
-    __syncthreads();  // stage s consumed
-    if (t == 0 && next_issue_tile < n_tiles) next_issue_tile = issue(next_issue_step++, next_issue_tile);
-    const long long last_tile = tile + u - 1;
-    i += u;
-    const bool chunk_end = (i % ct == 0) || (last_tile == tiles - 1);
-    if (chunk_end) {
-      const int chunk = (int)(last_tile / ct);
-      if (reduce_lanes<1, V>(acc, red, st.part, st.ticket, g, chunk, geo)) {
-        if (t < geo.L) {
-#pragma unroll
-          for (int j = 0; j < V; ++j) {
-            const size_t l = (size_t)g * S + V * t + j;
-            const double pap = red[j * geo.T + t];
-            const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
-            st.frozen[l] = fr;
-            st.alpha[l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
-          }
-        }
-        if (t == 0) st.it[g] += 1;
-      }
-      acc[0][0] = acc[0][1] = 0.0;
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
 // Warp-specialized variant: one producer warp streams the tiles' values into a
 // 4-stage ring (full/empty mbarrier pair per stage) while 8 consumer warps
@@ -1527,185 +1120,6 @@ __global__ void __launch_bounds__(288, 2) pcg_spmv_ws_kernel(
   }
 }
 
-// Fully staged variant for banded graphs (BandHint): per tile, one elected
-// thread bulk-copies the tile's values, its column indices and row offsets
-// (16-byte aligned spans of the padded graph) and the nb p bands the tile's
-// rows reference; consumers then work from shared memory only (a column that
-// misses every band is read from global memory).  Same arithmetic and order
-// as pcg_spmv_kernel: identical bits.
-struct BandLayout {
-  int vals_d, band_d, col_i, ro_i, stage_d;
-  int rows[kMaxBands];
-  int off_d[kMaxBands];
-};
-
-__host__ __device__ inline BandLayout band_layout(const Geo& geo, const BandHint& bh, int ML) {
-  BandLayout L{};
-  const int R = geo.R, S = geo.S;
-  L.vals_d = R * ML * S;
-  int acc = 0;
-#pragma unroll
-  for (int b = 0; b < kMaxBands; ++b) {
-    const bool on = b < bh.nb;
-    L.rows[b] = on ? R + bh.extra[b] : 0;
-    L.off_d[b] = L.vals_d + acc;
-    acc += L.rows[b] * S;
-  }
-  L.band_d = acc;
-  L.col_i = ((R * ML + 8) + 3) & ~3;
-  L.ro_i = ((R + 1 + 8) + 3) & ~3;
-  L.stage_d = L.vals_d + L.band_d + (L.col_i + L.ro_i) / 2;
-  L.stage_d = (L.stage_d + 1) & ~1;  // 16-byte multiple
-  return L;
-}
-
-template <int ML>
-__global__ void __launch_bounds__(256, 2) pcg_spmv_band_kernel(
-    long long N, long long nnz, Geo geo, PcgState st, const int* __restrict__ ro,
-    const int* __restrict__ ci, const double* __restrict__ vals, const double* __restrict__ p,
-    double* __restrict__ ap, BandHint bh) {
-  constexpr int V = 2;
-  extern __shared__ __align__(128) double red[];
-  const int g = blockIdx.y, t = threadIdx.x;
-  if (st.done[g] != kRunning) return;
-  const int S = geo.S, R = geo.R, T = geo.T;
-  const BandLayout L = band_layout(geo, bh, ML);
-  double* stage = red + V * T;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stage + kStages * L.stage_d);
-  const double* vg = vals + (size_t)g * nnz * S;
-  const double* pg_all = p + (size_t)g * N * S;
-  const int n_tiles = block_tile_count(geo);
-  const int ct = (int)geo.chunk_tiles;
-  const long long tiles = geo.tiles;
-
-  auto tile_of = [&](int i) -> long long {
-    const int j = i / ct;
-    return ((long long)blockIdx.x + (long long)j * gridDim.x) * ct + (i - j * ct);
-  };
-  auto col_stage = [&](int s) { return reinterpret_cast<int*>(stage + s * L.stage_d + L.vals_d + L.band_d); };
-  auto ro_stage = [&](int s) { return col_stage(s) + L.col_i; };
-
-  auto issue = [&](int i) {  // thread 0 only
-    const long long tile = tile_of(i);
-    const long long r0 = tile * R;
-    const int nr = (int)(N - r0 < R ? N - r0 : R);
-    const int k0 = __ldg(&ro[r0]), k1 = __ldg(&ro[r0 + nr]);
-    const int s = i % kStages;
-    double* sd = stage + s * L.stage_d;
-    const int ka = k0 & ~3, kb = (k1 + 3) & ~3;
-    const long long ra = r0 & ~3LL, rb = (r0 + nr + 1 + 3) & ~3LL;
-    uint32_t total = (uint32_t)(k1 - k0) * S * 8u + (uint32_t)(kb - ka) * 4u + (uint32_t)(rb - ra) * 4u;
-#pragma unroll
-    for (int b = 0; b < kMaxBands; ++b) {
-      if (b < bh.nb) {
-        const long long lo = r0 + bh.start[b], hi = lo + L.rows[b];
-        const long long lc = lo < 0 ? 0 : lo, hc = hi > N ? N : hi;
-        if (hc > lc) total += (uint32_t)(hc - lc) * S * 8u;
-      }
-    }
-    uint64_t* bar = &bars[s];
-    fence_proxy_async();
-    mbar_expect_tx(bar, total);
-    if (k1 > k0) bulk_g2s(sd, vg + (size_t)k0 * S, (uint32_t)(k1 - k0) * S * 8u, bar);
-    if (kb > ka) bulk_g2s(col_stage(s), ci + ka, (uint32_t)(kb - ka) * 4u, bar);
-    bulk_g2s(ro_stage(s), ro + ra, (uint32_t)(rb - ra) * 4u, bar);
-#pragma unroll
-    for (int b = 0; b < kMaxBands; ++b) {
-      if (b < bh.nb) {
-        const long long lo = r0 + bh.start[b], hi = lo + L.rows[b];
-        const long long lc = lo < 0 ? 0 : lo, hc = hi > N ? N : hi;
-        if (hc > lc)
-          bulk_g2s(sd + L.off_d[b] + (lc - lo) * S, pg_all + lc * S, (uint32_t)(hc - lc) * S * 8u,
-                   bar);
-      }
-    }
-  };
-
-  if (t == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
-    fence_mbar_init();
-    for (int i = 0; i < kStages && i < n_tiles; ++i) issue(i);
-  }
-  __syncthreads();
-
-  const int sl = t % geo.Lp, rr = t / geo.Lp;
-  const size_t base = (size_t)g * N * S + V * sl;
-  const double* pg = p + base;
-  double acc[1][V] = {};
-  for (int i = 0; i < n_tiles; ++i) {
-    const long long tile = tile_of(i);
-    const int s = i % kStages;
-    mbar_wait(&bars[s], (uint32_t)((i / kStages) & 1));
-    const long long r0 = tile * R;
-    if (sl < geo.L && r0 + rr < N) {
-      const long long row = r0 + rr;
-      const double* sd = stage + s * L.stage_d;
-      const int* rs = ro_stage(s) + (r0 - (r0 & ~3LL));
-      const int kt0 = rs[0];
-      const int* cs = col_stage(s) + (kt0 - (kt0 & ~3));
-      const int k0 = rs[rr] - kt0, len = rs[rr + 1] - rs[rr];
-      const double* sv = sd + (size_t)k0 * S + V * sl;
-      double y[V] = {0.0, 0.0};
-      double pv[V] = {0.0, 0.0};
-#pragma unroll
-      for (int e = 0; e < ML; ++e) {
-        if (e < len) {
-          const long long c = cs[k0 + e];
-          const double* src = nullptr;
-#pragma unroll
-          for (int b = kMaxBands - 1; b >= 0; --b) {  // first matching band wins
-            if (b < bh.nb) {
-              const long long d = c - (r0 + bh.start[b]);
-              if (d >= 0 && d < L.rows[b]) src = sd + L.off_d[b] + d * S + V * sl;
-            }
-          }
-          double2 bv;
-          if (src) bv = *reinterpret_cast<const double2*>(src);
-          else bv = __ldg(reinterpret_cast<const double2*>(pg + c * S));
-          const double2 a = *reinterpret_cast<const double2*>(sv + (size_t)e * S);
-          y[0] = __dadd_rn(y[0], __dmul_rn(a.x, bv.x));
-          y[1] = __dadd_rn(y[1], __dmul_rn(a.y, bv.y));
-          if (c == row) {
-            pv[0] = bv.x;
-            pv[1] = bv.y;
-          }
-        }
-      }
-      // p of the row itself (p.Ap); the diagonal entry normally provided it
-      bool have_diag = false;
-      for (int e = 0; e < len && e < ML; ++e) have_diag |= (cs[k0 + e] == row);
-      if (!have_diag) {
-        const double2 t2 = __ldg(reinterpret_cast<const double2*>(pg + row * S));
-        pv[0] = t2.x;
-        pv[1] = t2.y;
-      }
-      stv<V>(ap + base + row * S, y);
-#pragma unroll
-      for (int j = 0; j < V; ++j) acc[0][j] = __fma_rn(pv[j], y[j], acc[0][j]);
-    }
-    __syncthreads();  // stage s consumed
-    if (t == 0 && i + kStages < n_tiles) issue(i + kStages);
-    const bool chunk_end = ((i + 1) % ct == 0) || (tile == tiles - 1);
-    if (chunk_end) {
-      const int chunk = (int)(tile / ct);
-      if (reduce_lanes<1, V>(acc, red, st.part, st.ticket, g, chunk, geo)) {
-        if (t < geo.L) {
-#pragma unroll
-          for (int j = 0; j < V; ++j) {
-            const size_t l = (size_t)g * S + V * t + j;
-            const double pap = red[j * geo.T + t];
-            const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
-            st.frozen[l] = fr;
-            st.alpha[l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
-          }
-        }
-        if (t == 0) st.it[g] += 1;
-      }
-      acc[0][0] = acc[0][1] = 0.0;
-    }
-  }
-}
-
 // ensemble_iterations = max over lanes (ensemble.py:277)
 __global__ void pcg_finalize_kernel(PcgState st, int G, int S, int* ens_iters) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1798,25 +1212,6 @@ static void launch_spmv_tma(const Geo& gl, int G, cudaStream_t s, long long N, l
 }
 
 template <int ML>
-static void launch_spmv_pair(const Geo& gl, int G, cudaStream_t s, long long N, long long nnz,
-                             const PcgState& st, const int* ro, const int* ci, const double* vals,
-                             const double* p, double* ap, const BandHint* bands) {
-  const size_t smem = (size_t)2 * gl.T * sizeof(double) +
-                      (size_t)kPairStages * 2 * gl.R * ML * gl.S * sizeof(double) +
-                      kPairStages * 8;
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaFuncSetAttribute(pcg_spmv_pair_kernel<ML>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    configured = smem;
-  }
-  BandHint bh{};
-  if (bands && (reinterpret_cast<uintptr_t>(p) & 15) == 0) bh = *bands;
-  pcg_spmv_pair_kernel<ML><<<dim3(gl.B, G), gl.T, smem, s>>>(N, nnz, gl, st, ro, ci, vals, p, ap,
-                                                             bh);
-}
-
-template <int ML>
 static void launch_spmv_ws(const Geo& gl, int G, cudaStream_t s, long long N, long long nnz,
                            const PcgState& st, const int* ro, const int* ci, const double* vals,
                            const double* p, double* ap, const BandHint* bands) {
@@ -1833,53 +1228,18 @@ static void launch_spmv_ws(const Geo& gl, int G, cudaStream_t s, long long N, lo
   pcg_spmv_ws_kernel<ML><<<dim3(gl.B, G), 288, smem, s>>>(N, nnz, gl, st, ro, ci, vals, p, ap, bh);
 }
 
-template <int ML>
-static void launch_spmv_tma_meta(const Geo& gl, int G, cudaStream_t s, long long N, long long nnz,
-                                 const PcgState& st, const int* ro, const int* ci,
-                                 const double* vals, const double* p, double* ap) {
-  const size_t smem = (size_t)2 * gl.T * sizeof(double) +
-                      (size_t)kStages * gl.R * ML * gl.S * sizeof(double) +
-                      (size_t)kStages * (((gl.R + 2) & ~1) + gl.R * ML) * sizeof(int) +
-                      kStages * 8;
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaFuncSetAttribute(pcg_spmv_tma_meta_kernel<ML>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = smem;
-  }
-  pcg_spmv_tma_meta_kernel<ML><<<dim3(gl.B, G), gl.T, smem, s>>>(N, nnz, gl, st, ro, ci, vals, p,
-                                                                 ap);
-}
-
-// UQG_SPMV_TMA: 0 = register-gather kernel, 1 = TMA-staged values (default;
-// fastest on B200: C2 4.55 TB/s; with a band hint it also bulk-prefetches the
-// tile's p bands into L2), 2 = TMA-staged values + shared-memory tile metadata
-// (4.25 TB/s: the extra per-tile staging work outweighs the shorter
-// dependent-load chain), 3 = everything incl. the p bands staged in shared
-// memory (needs a band hint; 1.9 TB/s).  All give identical bits.
+// UQG_SPMV_TMA (CSR SpMV): 0 = register-gather kernel, 1 = TMA-staged values
+// (default; C2 4.73 TB/s with the band hint's L2 prefetch of the p bands),
+// 4 = warp-specialized producer/consumer ring (4.04 TB/s), 6 / 7 = mode 1 with
+// 2 stages x 4 CTAs/SM / 4 stages x 2 CTAs/SM (both slower).  All give
+// identical bits.  (Metadata-staged, fully band-staged and paired-tile
+// variants were measured slower still and removed.)
 int spmv_tma_mode() {
   static const int mode = [] {
     const char* e = getenv("UQG_SPMV_TMA");
     return e ? atoi(e) : 1;
   }();
   return mode;
-}
-
-template <int ML>
-static void launch_spmv_band(const Geo& gl, int G, cudaStream_t s, long long N, long long nnz,
-                             const PcgState& st, const int* ro, const int* ci, const double* vals,
-                             const double* p, double* ap, const BandHint& bh) {
-  const BandLayout L = band_layout(gl, bh, ML);
-  const size_t smem = (size_t)2 * gl.T * sizeof(double) +
-                      (size_t)kStages * L.stage_d * sizeof(double) + kStages * 8;
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaFuncSetAttribute(pcg_spmv_band_kernel<ML>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    configured = smem;
-  }
-  pcg_spmv_band_kernel<ML><<<dim3(gl.B, G), gl.T, smem, s>>>(N, nnz, gl, st, ro, ci, vals, p, ap,
-                                                             bh);
 }
 
 void launch_spmv_fv2d(const Geo& geo, int G, cudaStream_t s, long long N, const Fv2dOp& op,
@@ -1911,18 +1271,6 @@ void launch_pcg_spmv_fv2d(const Geo& geo, int G, cudaStream_t s, long long N, co
     g4.Lp = gl.Lp / 2;
     g4.T = gl.T / 2;  // rows per tile R unchanged
     pcg_spmv_fv2d4_kernel<<<dim3(g4.B, G), g4.T, smem, s>>>(N, g4, st, op, p, ap);
-    return;
-  }
-  // UQG_FACE_SHFL=1: warp-shuffle register kernel (off by default: slower)
-  static const bool shfl = [] {
-    const char* e = getenv("UQG_FACE_SHFL");
-    return e && atoi(e) != 0;
-  }();
-  if (shfl && gl.Lp <= 32) {
-    if (gl.V == 2)
-      pcg_spmv_fv2d_shfl_kernel<2><<<dim3(gl.B, G), gl.T, smem, s>>>(N, gl, st, op, p, ap);
-    else
-      pcg_spmv_fv2d_shfl_kernel<1><<<dim3(gl.B, G), gl.T, smem, s>>>(N, gl, st, op, p, ap);
     return;
   }
   // UQG_FACE_TMA: stages of the TMA-banded kernel (0 = off, default)
@@ -1966,35 +1314,12 @@ void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long lo
   const Geo& gl = geo;  // B preset by the caller (blocks per ACTIVE group)
   const bool aligned = (reinterpret_cast<uintptr_t>(vals) & 15) == 0;
   const int mode = spmv_tma_mode();
-  const bool aligned_all = aligned && (reinterpret_cast<uintptr_t>(p) & 15) == 0 &&
-                           (reinterpret_cast<uintptr_t>(ro) & 15) == 0 &&
-                           (reinterpret_cast<uintptr_t>(ci) & 15) == 0;
-  // mode 3: fully band-staged kernel (needs the band hint + padded graph)
-  if (mode == 3 && bands && bands->nb > 0 && bands->padded && gl.V == 2 && aligned_all &&
-      gl.maxrow >= 1 && gl.maxrow <= 8) {
-    if (gl.maxrow <= 5)
-      launch_spmv_band<5>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, *bands);
-    else
-      launch_spmv_band<8>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, *bands);
-    return;
-  }
   if (mode && gl.V == 2 && aligned && gl.maxrow >= 1 && gl.maxrow <= 8) {
-    // the metadata variant needs R + 1 <= T and R * ML <= 2T (S >= 8)
     if (mode == 4 && gl.T == 256) {
       if (gl.maxrow <= 5)
         launch_spmv_ws<5>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
       else
         launch_spmv_ws<8>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
-    } else if (mode == 5) {
-      if (gl.maxrow <= 5)
-        launch_spmv_pair<5>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
-      else
-        launch_spmv_pair<8>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
-    } else if (mode == 2 && gl.Lp >= 4) {
-      if (gl.maxrow <= 5)
-        launch_spmv_tma_meta<5>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap);
-      else
-        launch_spmv_tma_meta<8>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap);
     } else if (mode == 6) {  // 2 stages, 4 CTAs per SM
       if (gl.maxrow <= 5)
         launch_spmv_tma<5, 2, 4>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);

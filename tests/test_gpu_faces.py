@@ -85,7 +85,6 @@ np.save(sys.argv[2], np.array(out, dtype=object), allow_pickle=True)
 _VARIANTS = {  # face SpMV variants (all must give the CSR bits)
     "reg": {},                                            # default: 2 lanes / thread
     "v4": {"UQG_FACE_V4": "1"},                           # 4 lanes / thread (LDG.256)
-    "shfl": {"UQG_FACE_SHFL": "1"},                       # warp-shuffle neighbours
     "tma2": {"UQG_FACE_TMA": "2"},                        # TMA-banded
     "tma4": {"UQG_FACE_TMA": "4"},
     "fixed": {"UQG_OCC_BLOCKS": "0"},                     # with_groups block sizing

@@ -425,14 +425,14 @@ def test_tma_staged_spmv_bitwise_equals_register_path(tmp_path, lanes):
     from pathlib import Path
     root = str(Path(__file__).resolve().parents[1])
     out = {}
-    for tma, band in (("1", "1"), ("1", "0"), ("2", "0"), ("3", "1"), ("4", "1"), ("5", "1"),
-                      ("6", "1"), ("7", "1"), ("0", "0"), ("F", "F")):
+    for tma, band in (("1", "1"), ("1", "0"), ("4", "1"), ("6", "1"), ("7", "1"), ("0", "0"),
+                      ("F", "F")):
         env = dict(os.environ, UQG_SPMV_TMA=tma, UQG_BAND_HINT=band, UQG_LANES_PER_THREAD=lanes,
                    UQG_PCG_PERSISTENT="0", UQG_FV2D_FACES="1" if tma == "F" else "0")
         dst = tmp_path / f"r{tma}{band}.npy"
         subprocess.run([sys.executable, "-c", _TMA_SCRIPT, root, str(dst)], env=env, check=True)
         out[tma + band] = np.load(dst)
-    # value-staged (+L2 band prefetch), value-staged, metadata-staged, band-staged
-    # ... warp-specialized, paired tiles, 2/4-stage TMA, face-form FV2D operator
-    for k in ("11", "10", "20", "31", "41", "51", "61", "71", "FF"):
+    # value-staged (+L2 band prefetch), value-staged, warp-specialized, 2/4-stage TMA,
+    # face-form FV2D operator
+    for k in ("11", "10", "41", "61", "71", "FF"):
         assert np.array_equal(out[k], out["00"]), k
