@@ -179,18 +179,39 @@ class ClockSampler:
 # CPU legs (oracle = the reference algorithm restated; test infra, used here
 # only as the timed CPU baseline)
 
+_CPU_SETUP = {}
+
+
+def _cpu_setup(cfg_name):
+    """One-time per-process setup of the CPU path (field, mesh, mode table) -
+    excluded from the timed steps like the device arm's."""
+    if cfg_name not in _CPU_SETUP:
+        from threadpoolctl import threadpool_limits
+
+        from oracle import fv2d as ofv, field2d
+        from paper_1705_02003_b200.configs import get
+
+        cfg = get(cfg_name)
+        with threadpool_limits(limits=1):
+            fld = field2d.KL2D.select(**cfg.field_kwargs())
+            mesh = ofv.Mesh2D(cfg.cells)
+            _CPU_SETUP[cfg_name] = (cfg, fld, mesh, fld.mode_table(mesh.node_points))
+    return _CPU_SETUP[cfg_name]
+
+
+def _cpu_warm(cfg_name):
+    _cpu_setup(cfg_name)
+    return os.getpid()
+
+
 def _cpu_group_worker(args):
     cfg_name, samples = args
     from threadpoolctl import threadpool_limits
 
-    from oracle import fv2d as ofv, field2d, pcg as opcg
-    from paper_1705_02003_b200.configs import get
+    from oracle import fv2d as ofv, pcg as opcg
 
-    cfg = get(cfg_name)
+    cfg, fld, mesh, table = _cpu_setup(cfg_name)
     with threadpool_limits(limits=1):
-        fld = field2d.KL2D.select(**cfg.field_kwargs())
-        mesh = ofv.Mesh2D(cfg.cells)
-        table = fld.mode_table(mesh.node_points)
         t0 = time.perf_counter()
         sysm = ofv.assemble(mesh, fld, samples, table, cfg.a2)
         res = opcg.pcg(sysm.row_offsets, sysm.col_indices, sysm.values, sysm.rhs, tol=cfg.tol,
@@ -236,6 +257,10 @@ def run_reference(args, cfg):
     times, done = [], 0
     ctx = mproc.get_context("spawn")
     with ctx.Pool(P) as pool:
+        # untimed warm-up: worker start-up and the per-process setup
+        warm = 1 if args.warmup > 0 else 0
+        if warm:
+            pool.map(_cpu_warm, [cfg.name] * P, chunksize=1)
         for st in range(steps):
             chosen = [ens[(st * P + j) % len(ens)] for j in range(P)]
             t0 = time.perf_counter()
@@ -247,7 +272,7 @@ def run_reference(args, cfg):
     S = cfg.ensemble_size
     line = {
         "impl": "reference", "metric": METRIC, "value": value,
-        "unit": "sample-solves/s", "n_gpus": args.gpus, "steps": steps, "warmup": 0,
+        "unit": "sample-solves/s", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
         "ms_per_step": 1e3 * total / steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{cfg.name} final adaptive level, {P} groups per step",
