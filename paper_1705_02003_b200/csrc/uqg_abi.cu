@@ -160,8 +160,8 @@ size_t pcg_layout(Carver& c, long long N, const Geo& geo, int G, PcgState* st, d
   double* aa = c.take<double>(vec);
   PcgState s{};
   s.G = G;
-  s.part = c.take<double>((size_t)G * geo.chunks * 2 * geo.S);
-  s.ticket = c.take<unsigned int>(G);
+  s.part = c.take<double>((size_t)G * geo.pstride * 2 * geo.S);
+  s.ticket = c.take<unsigned int>((size_t)G * geo.tstride);
   s.rz = c.take<double>(lanes);
   s.thr = c.take<double>(lanes);
   s.alpha = c.take<double>(lanes);
@@ -428,13 +428,14 @@ int uqg_lane_dot(uqg_ctx* ctx, int N, int S, int G, const double* a, const doubl
   UQG_REQUIRE(N >= 0 && S >= 1 && S <= kMaxLanes && G >= 1, "uqg_lane_dot: bad sizes");
   cudaStream_t s = as_stream(stream);
   Geo geo = make_geo(N, S);
-  size_t need = (size_t)G * geo.chunks * geo.S * sizeof(double) + (size_t)G * sizeof(unsigned) + 1024;
+  size_t need = (size_t)G * geo.pstride * geo.S * sizeof(double) +
+                (size_t)G * geo.tstride * sizeof(unsigned) + 1024;
   int rc = ensure_ws(ctx, need);
   if (rc) return rc;
   Carver c{(char*)ws_base(ctx, need)};
-  double* part = c.take<double>((size_t)G * geo.chunks * geo.S);
-  unsigned* ticket = c.take<unsigned>(G);
-  UQG_TRY_CUDA(cudaMemsetAsync(ticket, 0, G * sizeof(unsigned), s));
+  double* part = c.take<double>((size_t)G * geo.pstride * geo.S);
+  unsigned* ticket = c.take<unsigned>((size_t)G * geo.tstride);
+  UQG_TRY_CUDA(cudaMemsetAsync(ticket, 0, (size_t)G * geo.tstride * sizeof(unsigned), s));
   UQG_LAUNCH(UQG_K_DOT, s, launch_lane_dot(geo, G, s, N, a, b, out, part, ticket));
   return UQG_OK;
 }
@@ -552,7 +553,7 @@ int pcg_impl(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const 
   st.frozen = frozen;
   st.hist = hist_host ? c.take<double>(hist_elems) : nullptr;
   st.hist_cap = hist_cap;
-  UQG_TRY_CUDA(cudaMemsetAsync(st.ticket, 0, G * sizeof(unsigned), s));
+  UQG_TRY_CUDA(cudaMemsetAsync(st.ticket, 0, (size_t)G * geo.tstride * sizeof(unsigned), s));
   UQG_TRY_CUDA(cudaMemsetAsync(st.ndone, 0, sizeof(int), s));
   UQG_TRY_CUDA(cudaMemsetAsync(st.overflow, 0, sizeof(int), s));
 
@@ -566,14 +567,16 @@ int pcg_impl(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const 
   const bool small = iter_bytes < 512e6;
   bool use_cluster = false;
   int pblocks = 0;
-  if (pmode == 2 || (pmode < 0 && small)) {
+  // (the persistent kernels reduce without super-chunks: geo.sc == 1 only)
+  if (geo.sc == 1 && (pmode == 2 || (pmode < 0 && small))) {
     const int cs = persistent_cluster_size(geo);
     if (cs >= 2) {
       use_cluster = true;
       pblocks = cs;
     }
   }
-  if (!use_cluster && (pmode == 1 || (pmode < 0 && small))) pblocks = persistent_blocks(geo, G);
+  if (!use_cluster && geo.sc == 1 && (pmode == 1 || (pmode < 0 && small)))
+    pblocks = persistent_blocks(geo, G);
   if (pblocks > 0) {
     PersistBufs pb = g_persist;
     UQG_TRY_CUDA(cudaMemsetAsync(pb.bar, 0, (2 * (size_t)G + 1) * sizeof(unsigned), s));

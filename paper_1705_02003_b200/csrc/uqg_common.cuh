@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 
@@ -60,6 +61,7 @@ void set_error(const std::string& msg);
 constexpr int kMaxChunks = 512;        // partials per group and reduction
 constexpr int kTargetBlocks = 2368;    // ~2 waves of 148 SMs x 8 resident CTAs
 constexpr int kMaxLanes = 512;         // S <= 512 keeps Lp <= 256 = block size
+constexpr int kMaxBatch = 8;           // chunks per batched reduction (reduce_lanes_batch)
 
 struct Geo {
   int S;          // lanes per group
@@ -74,6 +76,10 @@ struct Geo {
   int B;          // blocks per group in the launch (set by with_groups)
   int gact;       // groups still running (with_groups), for occupancy-aware sizing
   int maxrow;     // longest graph row if known (0 = unknown): picks the unrolled SpMV
+  int sc;         // chunks per super-chunk (1 = no super level: chunks <= kMaxChunks)
+  int nsc;        // super-chunks (sc > 1)
+  int pstride;    // partial rows per group: chunks (+ nsc super-partials when sc > 1)
+  int tstride;    // tickets per group: 1 (+ nsc super-chunk tickets when sc > 1)
 };
 
 // UQG_LANES_PER_THREAD=1 forces V = 1 (tuning experiments only; V changes the
@@ -98,16 +104,46 @@ inline Geo make_geo(long long N, int S, int maxrow = 0) {
   g.R = g.T / g.Lp;
   g.tiles = (N + g.R - 1) / g.R;
   if (g.tiles < 1) g.tiles = 1;
-  // aim for >= 64 chunks of <= 8 tiles (small N), at most kMaxChunks (large N)
-  long long ct = g.tiles / 64;
+  // Aim for >= 64 chunks of <= 8 tiles; groups with more tiles get longer
+  // chunks (at most kMaxChunks of them), but a chunk never spans more rows than
+  // ~sqrt(N) - the neighbour band of a 2D stencil - once that needs more than
+  // kMaxChunks chunks: a block sweeps its chunks' tiles in order, and a chunk
+  // longer than the band makes its own +m neighbours wait a whole band before
+  // reuse, so at large N the concurrently swept bands no longer fit in L2.
+  // Then consecutive chunks form super-chunks whose partials are summed (in
+  // chunk order) by the block completing the super-chunk, and the final stage
+  // sums the <= kMaxChunks super-partials.
   static const int ct_max = [] {  // UQG_CHUNK_TILES (tuning only: changes the trees)
     const char* e = getenv("UQG_CHUNK_TILES");
     return e ? atoi(e) : 8;
   }();
+  long long ct = g.tiles / 64;
   ct = ct < 1 ? 1 : (ct > ct_max ? ct_max : ct);
-  if ((g.tiles + ct - 1) / ct > kMaxChunks) ct = (g.tiles + kMaxChunks - 1) / kMaxChunks;
+  if ((g.tiles + ct - 1) / ct > kMaxChunks) {
+    long long band = (long long)sqrt((double)N);  // floor(sqrt(N))
+    while (band * band > N) --band;
+    while ((band + 1) * (band + 1) <= N) ++band;
+    long long ct_band = band / g.R;
+    if (ct_band < ct) ct_band = ct;
+    ct = (g.tiles + kMaxChunks - 1) / kMaxChunks;
+    // within 10% of the band: keep the single-level reduction (C3), else cap
+    // chunks at the band and add the super-chunk level (C4, C5: measured
+    // 1.0-band chunks 4.6 / 4.8 TB/s vs 4.0 / 3.9 at 1.1 bands)
+    if (ct * 10 > ct_band * 11) ct = ct_band;
+  }
   g.chunk_tiles = ct;
   g.chunks = (int)((g.tiles + ct - 1) / ct);
+  if (g.chunks > kMaxChunks) {
+    g.sc = (g.chunks + kMaxChunks - 1) / kMaxChunks;
+    g.nsc = (g.chunks + g.sc - 1) / g.sc;
+    g.pstride = g.chunks + g.nsc;
+    g.tstride = 1 + g.nsc;
+  } else {
+    g.sc = 1;
+    g.nsc = g.chunks;
+    g.pstride = g.chunks;
+    g.tstride = 1;
+  }
   g.B = g.chunks;
   g.gact = 1;
   return g;
@@ -239,8 +275,15 @@ __device__ __forceinline__ void stv(double* p, const double (&o)[V]) {
 // chunk, value, lane), and takes a ticket.  The block that completes the last
 // chunk of the group sums the chunk partials of each lane in a fixed order
 // (strided sequential sums, then the same binary tree) and returns true with
-// the total of value v, lane V*sl+j in red[(v*V + j)*T + sl].  No
-// floating-point atomics: the result is a pure function of the inputs.
+// the total of value v, lane V*sl+j in red[(v*V + j)*T + sl].  With
+// super-chunks (geo.sc > 1) the block completing a super-chunk first sums its
+// chunk partials sequentially in chunk order into a super-partial, and the
+// final stage runs over the super-partials.  No floating-point atomics: the
+// result is a pure function of the inputs.
+//
+// Layout per group g: part rows [g*pstride + r][NV][S] (r < chunks: chunk
+// partials, then super-partials); tickets [g*tstride]: group ticket, then one
+// per super-chunk.
 
 template <int NS>
 __device__ __forceinline__ void tree_rows(double* red, int T, int Lp, int R, int t) {
@@ -253,12 +296,111 @@ __device__ __forceinline__ void tree_rows(double* red, int T, int Lp, int R, int
   }
 }
 
+// Tickets of nk chunks (chunk0 + k*stride) whose partials are written and
+// fenced (all threads call after a __syncthreads).  Returns true in the one
+// block that completes the group, with the totals in red[].
+template <int NV, int V>
+__device__ bool finish_chunks(double* red, double* part, unsigned int* ticket, int g, int chunk0,
+                              int stride, int nk, const Geo& geo) {
+  constexpr int NS = NV * V;
+  const int t = threadIdx.x;
+  const int T = geo.T, Lp = geo.Lp, R = geo.R, L = geo.L, S = geo.S, C = geo.chunks;
+  unsigned int* gt = ticket + (size_t)g * geo.tstride;
+  double* gp = part + (size_t)g * geo.pstride * NV * S;
+  __shared__ int s_flag;
+  int rows = C, row0 = 0;
+  if (geo.sc == 1) {
+    if (t == 0) {
+      const unsigned int tk = atomicAdd(gt, (unsigned)nk);
+      s_flag = (tk + (unsigned)nk == (unsigned)C);
+    }
+    __syncthreads();
+    if (!s_flag) return false;
+  } else {
+    // one thread per chunk of the batch takes its super-chunk's ticket
+    __shared__ int s_super[kMaxBatch];
+    if (t < nk) {
+      const int c = chunk0 + t * stride, si = c / geo.sc;
+      const int c_lo = si * geo.sc, c_hi = c_lo + geo.sc < C ? c_lo + geo.sc : C;
+      const unsigned int tk = atomicAdd(gt + 1 + si, 1u);
+      s_super[t] = (tk + 1u == (unsigned)(c_hi - c_lo)) ? si : -1;
+    }
+    __syncthreads();
+    // every super-chunk this batch completed: its partials summed in chunk order
+    // (all completed super-chunks at once, the loads of one sum issued together)
+    __threadfence();
+    if (t < L) {
+      for (int k = 0; k < nk; ++k) {
+        const int si = s_super[k];
+        if (si < 0) continue;
+        const int c_lo = si * geo.sc, c_hi = c_lo + geo.sc < C ? c_lo + geo.sc : C;
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            double a = 0.0;
+            for (int c0 = c_lo; c0 < c_hi; c0 += 8) {
+              double q[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                q[u] = c0 + u < c_hi ? __ldcg(&gp[((size_t)(c0 + u) * NV + v) * S + V * t + j]) : 0.0;
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if (c0 + u < c_hi) a += q[u];
+            }
+            gp[((size_t)(C + si) * NV + v) * S + V * t + j] = a;
+          }
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (t == 0) {
+      int fin = 0;
+      for (int k = 0; k < nk; ++k) {
+        const int si = s_super[k];
+        if (si < 0) continue;
+        gt[1 + si] = 0u;
+        const unsigned int tk = atomicAdd(gt, 1u);
+        if (tk + 1u == (unsigned)geo.nsc) fin = 1;
+      }
+      s_flag = fin;
+    }
+    __syncthreads();
+    const bool last = s_flag;
+    if (!last) return false;
+    rows = geo.nsc;
+    row0 = C;
+  }
+  __threadfence();
+  const int sl = t % Lp, jr = t / Lp;
+  double acc[NS];
+#pragma unroll
+  for (int v = 0; v < NS; ++v) acc[v] = 0.0;
+  if (sl < L) {
+#pragma unroll 4
+    for (int cc = jr; cc < rows; cc += R) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+          acc[v * V + j] += __ldcg(&gp[((size_t)(row0 + cc) * NV + v) * S + V * sl + j]);
+    }
+  }
+  __syncthreads();  // red[] may still hold the caller's tree values
+#pragma unroll
+  for (int v = 0; v < NS; ++v) red[v * T + t] = acc[v];
+  __syncthreads();
+  tree_rows<NS>(red, T, Lp, R, t);
+  if (t == 0) gt[0] = 0u;  // ready for the next reduction on this counter
+  return true;
+}
+
 template <int NV, int V>
 __device__ bool reduce_lanes(const double (&val)[NV][V], double* red, double* part,
                              unsigned int* ticket, int g, int chunk, const Geo& geo) {
   constexpr int NS = NV * V;
   const int t = threadIdx.x;
-  const int T = geo.T, Lp = geo.Lp, R = geo.R, L = geo.L, S = geo.S, C = geo.chunks;
+  const int T = geo.T, Lp = geo.Lp, R = geo.R, L = geo.L, S = geo.S;
   __syncthreads();  // red[] may still be read by the previous chunk's tree
 #pragma unroll
   for (int v = 0; v < NV; ++v)
@@ -271,53 +413,26 @@ __device__ bool reduce_lanes(const double (&val)[NV][V], double* red, double* pa
     for (int v = 0; v < NV; ++v)
 #pragma unroll
       for (int j = 0; j < V; ++j)
-        part[(((size_t)g * C + chunk) * NV + v) * S + V * t + j] = red[(v * V + j) * T + t];
+        part[(((size_t)g * geo.pstride + chunk) * NV + v) * S + V * t + j] =
+            red[(v * V + j) * T + t];
   }
-  __shared__ int s_last;
   __threadfence();
   __syncthreads();
-  if (t == 0) {
-    unsigned int tk = atomicAdd(&ticket[g], 1u);
-    s_last = (tk == (unsigned)(C - 1));
-  }
-  __syncthreads();
-  if (!s_last) return false;
-  __threadfence();
-  const int sl = t % Lp, jr = t / Lp;
-  double acc[NS];
-#pragma unroll
-  for (int v = 0; v < NS; ++v) acc[v] = 0.0;
-  if (sl < L) {
-#pragma unroll 4
-    for (int cc = jr; cc < C; cc += R) {
-#pragma unroll
-      for (int v = 0; v < NV; ++v)
-#pragma unroll
-        for (int j = 0; j < V; ++j)
-          acc[v * V + j] += __ldcg(&part[(((size_t)g * C + cc) * NV + v) * S + V * sl + j]);
-    }
-  }
-#pragma unroll
-  for (int v = 0; v < NS; ++v) red[v * T + t] = acc[v];
-  __syncthreads();
-  tree_rows<NS>(red, T, Lp, R, t);
-  if (t == 0) ticket[g] = 0u;  // ready for the next reduction on this counter
-  return true;
+  return finish_chunks<NV, V>(red, part, ticket, g, chunk, 1, 1, geo);
 }
 
 // reduce_lanes over a batch of nk chunks chunk0 + k*stride (k < nk) whose
 // per-thread values the caller has stored in red[((k*NV + v)*V + j)*T + t]:
-// one in-block tree for the whole batch (instead of one per chunk), one
-// ticket add of nk, then the final stage of reduce_lanes.  Every partial and
-// the final sums are computed exactly as reduce_lanes<NV, V> computes them,
-// so results are bit-identical (same result layout in red).  red must hold
-// max(nk, 1) * NV * V * T doubles.
+// one in-block tree for the whole batch (instead of one per chunk), then the
+// chunks' tickets.  Every partial and the final sums are computed exactly as
+// reduce_lanes<NV, V> computes them, so results are bit-identical (same result
+// layout in red).  red must hold max(nk, 1) * NV * V * T doubles.
 template <int NV, int V>
 __device__ bool reduce_lanes_batch(double* red, double* part, unsigned int* ticket, int g,
                                    int chunk0, int stride, int nk, const Geo& geo) {
   constexpr int NS = NV * V;
   const int t = threadIdx.x;
-  const int T = geo.T, Lp = geo.Lp, R = geo.R, L = geo.L, S = geo.S, C = geo.chunks;
+  const int T = geo.T, Lp = geo.Lp, R = geo.R, L = geo.L, S = geo.S;
   const int ns = nk * NS;
   __syncthreads();
   for (int st = R >> 1; st > 0; st >>= 1) {
@@ -332,51 +447,25 @@ __device__ bool reduce_lanes_batch(double* red, double* part, unsigned int* tick
       for (int v = 0; v < NV; ++v)
 #pragma unroll
         for (int j = 0; j < V; ++j)
-          part[(((size_t)g * C + chunk0 + k * stride) * NV + v) * S + V * t + j] =
+          part[(((size_t)g * geo.pstride + chunk0 + k * stride) * NV + v) * S + V * t + j] =
               red[((k * NV + v) * V + j) * T + t];
   }
-  __shared__ int s_last;
   __threadfence();
   __syncthreads();
-  if (t == 0) {
-    unsigned int tk = atomicAdd(&ticket[g], (unsigned)nk);
-    s_last = (tk + (unsigned)nk == (unsigned)C);
-  }
-  __syncthreads();
-  if (!s_last) return false;
-  __threadfence();
-  const int sl = t % Lp, jr = t / Lp;
-  double acc[NS];
-#pragma unroll
-  for (int v = 0; v < NS; ++v) acc[v] = 0.0;
-  if (sl < L) {
-#pragma unroll 4
-    for (int cc = jr; cc < C; cc += R) {
-#pragma unroll
-      for (int v = 0; v < NV; ++v)
-#pragma unroll
-        for (int j = 0; j < V; ++j)
-          acc[v * V + j] += __ldcg(&part[(((size_t)g * C + cc) * NV + v) * S + V * sl + j]);
-    }
-  }
-  __syncthreads();  // the batch's tree values in red[] have been consumed
-#pragma unroll
-  for (int v = 0; v < NS; ++v) red[v * T + t] = acc[v];
-  __syncthreads();
-  tree_rows<NS>(red, T, Lp, R, t);
-  if (t == 0) ticket[g] = 0u;
-  return true;
+  return finish_chunks<NV, V>(red, part, ticket, g, chunk0, stride, nk, geo);
 }
 
-// "last block of the group" without values (for state transitions).
-__device__ __forceinline__ bool last_block(unsigned int* ticket, int g, int B) {
+// "last block of the group" without values (for state transitions); uses the
+// group ticket (slot 0 of the group's tickets).
+__device__ __forceinline__ bool last_block(unsigned int* ticket, int g, int B, int tstride) {
   __shared__ int s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    unsigned int tk = atomicAdd(&ticket[g], 1u);
+    unsigned int* gt = ticket + (size_t)g * tstride;
+    unsigned int tk = atomicAdd(gt, 1u);
     s_last = (tk == (unsigned)(B - 1));
-    if (s_last) ticket[g] = 0u;
+    if (s_last) *gt = 0u;
   }
   __syncthreads();
   return s_last;

@@ -319,6 +319,7 @@ struct FaceRow {
 // Chunks are reduced in batches of up to kFaceBatch (reduce_lanes_batch: one
 // tree and one ticket per batch, same bits as per-chunk reduce_lanes).
 constexpr int kFaceBatch = 8;
+static_assert(kFaceBatch <= kMaxBatch, "batch exceeds reduce_lanes_batch's limit");
 
 template <int V>
 __device__ __forceinline__ void face_spmv_body(long long N, const Geo& geo, const PcgState& st,
@@ -418,6 +419,7 @@ __global__ void __launch_bounds__(256) spmv_fv2d_kernel(long long N, Geo geo, Fv
 
 // chunks per batched reduction in pcg_update (reduce_lanes_batch)
 constexpr int kUpdateBatch = 4;
+static_assert(kUpdateBatch <= kMaxBatch, "batch exceeds reduce_lanes_batch's limit");
 
 template <int V>
 __global__ void __launch_bounds__(256, 3) pcg_update_kernel(long long N, Geo geo, PcgState st,
@@ -583,7 +585,7 @@ __global__ void __launch_bounds__(256, 3) pcg_dir_kernel(long long N, Geo geo, P
       }
     }
   }
-  if (state == kFinishing && last_block(st.ticket, g, gridDim.x) && t == 0) {
+  if (state == kFinishing && last_block(st.ticket, g, gridDim.x, geo.tstride) && t == 0) {
     st.done[g] = kDone;
     atomicAdd(st.ndone, 1);
   }
@@ -967,12 +969,13 @@ __device__ bool reduce_lanes_c(const double (&val)[NV][V], double* red, double* 
     for (int v = 0; v < NV; ++v)
 #pragma unroll
       for (int j = 0; j < V; ++j)
-        part[(((size_t)g * C + chunk) * NV + v) * S + V * t + j] = red[(v * V + j) * T + t];
+        part[(((size_t)g * geo.pstride + chunk) * NV + v) * S + V * t + j] =
+            red[(v * V + j) * T + t];
   }
   __threadfence();
   consumer_sync();
-  if (t == 0) {
-    unsigned int tk = atomicAdd(&ticket[g], 1u);
+  if (t == 0) {  // (no super-chunks: the host selects this kernel only when geo.sc == 1)
+    unsigned int tk = atomicAdd(&ticket[(size_t)g * geo.tstride], 1u);
     *s_last = (tk == (unsigned)(C - 1));
   }
   consumer_sync();
@@ -989,14 +992,15 @@ __device__ bool reduce_lanes_c(const double (&val)[NV][V], double* red, double* 
       for (int v = 0; v < NV; ++v)
 #pragma unroll
         for (int j = 0; j < V; ++j)
-          acc[v * V + j] += __ldcg(&part[(((size_t)g * C + cc) * NV + v) * S + V * sl + j]);
+          acc[v * V + j] +=
+              __ldcg(&part[(((size_t)g * geo.pstride + cc) * NV + v) * S + V * sl + j]);
     }
   }
 #pragma unroll
   for (int v = 0; v < NS; ++v) red[v * T + t] = acc[v];
   consumer_sync();
   tree_rows_c<NS>(red, T, Lp, R, t);
-  if (t == 0) ticket[g] = 0u;
+  if (t == 0) ticket[(size_t)g * geo.tstride] = 0u;
   return true;
 }
 
@@ -1315,7 +1319,7 @@ void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long lo
   const bool aligned = (reinterpret_cast<uintptr_t>(vals) & 15) == 0;
   const int mode = spmv_tma_mode();
   if (mode && gl.V == 2 && aligned && gl.maxrow >= 1 && gl.maxrow <= 8) {
-    if (mode == 4 && gl.T == 256) {
+    if (mode == 4 && gl.T == 256 && gl.sc == 1) {
       if (gl.maxrow <= 5)
         launch_spmv_ws<5>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
       else

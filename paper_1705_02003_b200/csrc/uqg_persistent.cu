@@ -97,7 +97,7 @@ __device__ void chunk_partial(const double (&val)[NV][V], double* red, double* p
     for (int v = 0; v < NV; ++v)
 #pragma unroll
       for (int j = 0; j < V; ++j)
-        part[(((size_t)g * C + chunk) * NV + v) * S + V * t + j] = red[(v * V + j) * T + t];
+        part[(((size_t)g * geo.pstride + chunk) * NV + v) * S + V * t + j] = red[(v * V + j) * T + t];
   }
 }
 
@@ -120,7 +120,7 @@ __device__ void final_partials(double* red, const double* part, int g, const Geo
       for (int v = 0; v < NV; ++v)
 #pragma unroll
         for (int j = 0; j < V; ++j)
-          acc[v * V + j] += __ldcg(&part[(((size_t)g * C + cc) * NV + v) * S + V * sl + j]);
+          acc[v * V + j] += __ldcg(&part[(((size_t)g * geo.pstride + cc) * NV + v) * S + V * sl + j]);
     }
   }
 #pragma unroll
