@@ -147,6 +147,7 @@ class EnsembleSolver:
         self.mem_fraction = mem_fraction
         self.max_groups_per_wave = max_groups_per_wave
         self._bufs = {}
+        self._pins = {}
         self._ws = None
 
     # -- memory planning ----------------------------------------------------
@@ -167,6 +168,15 @@ class EnsembleSolver:
         if self.max_groups_per_wave:
             g = min(g, self.max_groups_per_wave)
         return min(g, K)
+
+    def _pinned(self, name, n):
+        """Grow-only pinned host float64 staging buffer (first n entries)."""
+        torch = _lib._torch()
+        t = self._pins.get(name)
+        if t is None or t.numel() < n:
+            t = torch.empty((max(n, 1024),), dtype=torch.float64).pin_memory()
+            self._pins[name] = t
+        return t[:n]
 
     def _buf(self, name, n, dtype):
         torch = _lib._torch()
@@ -323,14 +333,22 @@ class EnsembleSolver:
         if coords.shape != (n, self.field.n_modes):
             raise FemError(f"coords must have shape ({n}, {self.field.n_modes})")
         dev = _lib.device()
-        h_c = torch.from_numpy(coords).pin_memory()
-        d_c = h_c.to(dev, non_blocking=True)
+        M = coords.shape[1]
+        # inputs through a reused pinned staging buffer (pinning per call costs
+        # more than the copy itself at small levels)
+        stage = self._pinned("in", n * M + (n if keys is not None else 0))
+        stage[:n * M].copy_(torch.from_numpy(coords.reshape(-1)))
+        d_c = stage[:n * M].to(dev, non_blocking=True).view(n, M)
         d_k = None
         if keys is not None:
-            h_k = torch.from_numpy(np.ascontiguousarray(keys, dtype=np.float64)).pin_memory()
-            d_k = h_k.to(dev, non_blocking=True)
+            stage[n * M:].copy_(torch.from_numpy(np.ascontiguousarray(keys, dtype=np.float64)))
+            d_k = stage[n * M:].to(dev, non_blocking=True)
         groups, pad, it, cv, en, q = self.run_level_device(d_c, n, size, d_k)
-        host = torch.cat([groups.double(), pad.double(), it.double(), cv.double(), q]).cpu().numpy()
+        d_out = torch.cat([groups.double(), pad.double(), it.double(), cv.double(), q])
+        h_out = self._pinned("out", d_out.numel())
+        h_out.copy_(d_out, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        host = h_out.numpy()
         K = pad.numel()
         KS = K * size
         g_idx = host[:KS].astype(np.int64).reshape(K, size)
