@@ -62,12 +62,15 @@ def parse():
 # ---------------------------------------------------------------------------
 # workload
 
-def bytes_model(cfg, op=None):
+def bytes_model(cfg, op=None, kx=1):
     """Algorithmic bytes per group per launch (DESIGN.md / SURVEY.md 8d).
 
     CSR operator: the SURVEY 8d figures.  Face-form FV2D operator (``op.faces``):
     the operator stream is ``op.n_op`` doubles per lane (faces) instead of nnz
     values + the int32 graph - the same formula with the smaller operator.
+    ``kx`` > 1 (deferred solution update, ``uqg_pcg_x_defer``): the direction
+    class moves 4 vector passes per iteration plus, every kx-th iteration, the
+    flush (x read + write, kx p reads): (4 + (2 + kx) / kx) passes.
     """
     S, N, nnz = cfg.ensemble_size, cfg.n_dofs, cfg.nnz
     if op is not None and getattr(op, "faces", False):
@@ -76,13 +79,17 @@ def bytes_model(cfg, op=None):
         n_op, graph = nnz, 4 * nnz + 4 * (N + 1)
     spmv = 8 * S * n_op + graph + 16 * S * N
     update = 4 * 8 * S * N      # read r, Ap, dinv; write r
-    direction = 6 * 8 * S * N   # read x, p, r, dinv; write x, p (x += alpha p deferred here)
+    if kx > 1:
+        direction = int((4 + (2 + kx) / kx) * 8 * S * N)
+    else:
+        direction = 6 * 8 * S * N   # read x, p, r, dinv; write x, p (x += alpha p deferred here)
     return {"spmv": spmv, "update": update, "dir": direction,
             # SURVEY 8d's algorithmic bytes per PCG iteration (13 vector passes) and
             # the bytes this implementation actually moves (12 passes)
             "pcg_iter": 8 * S * (n_op + 13 * N) + graph,
             "pcg_iter_moved": spmv + update + direction,
-            "operator": "fv2d faces" if graph == 0 else "csr"}
+            "operator": "fv2d faces" if graph == 0 else "csr",
+            **({"flush": kx} if kx > 1 else {})}
 
 
 def make_workload(cfg, solver=None):
@@ -438,7 +445,7 @@ def main():
     if args.max_iters:  # throughput mode: sample-iterations per second
         value *= args.max_iters
         unit = f"sample-iterations/s (throughput mode: {args.max_iters} PCG iterations per group)"
-    bm = bytes_model(cfg, solver.op)
+    bm = bytes_model(cfg, solver.op, int(lib.uqg_pcg_x_defer()))
     peaks = {}
     pk = ROOT / "MEASURED_PEAKS.json"
     if pk.exists():
@@ -453,8 +460,9 @@ def main():
     # one with the largest measured time share (the dominant kernel)
     spmv_name = "pcg_spmv_fv2d_kernel" if bm["operator"] != "csr" else "pcg_spmv_tma_kernel"
     per = {}
+    dir_name = "pcg_dir_kernel" + (" + pcg_flush_kernel" if "flush" in bm else "")
     for key, idx, kname in (("spmv", 3, spmv_name), ("update", 4, "pcg_update_kernel"),
-                            ("dir", 5, "pcg_dir_kernel")):
+                            ("dir", 5, dir_name)):
         t_ms = ms[idx]
         gbs = group_iters * bm[key] / (t_ms / 1e3) / 1e9 if t_ms else None
         tr = traffic_all.get(f"{cfg.name}:{kname}", {})

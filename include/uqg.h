@@ -46,11 +46,10 @@ int uqg_ctx_set_workspace(uqg_ctx* ctx, void* ptr, long long bytes);
 /* Structure hint for banded graphs (stencils), used by uqg_pcg on this ctx
  * until replaced (nbands = 0 clears): the columns of rows [r0, r0+R) lie in
  * the row bands [r0 + starts[b], r0 + starts[b] + R + extras[b]).  With it the
- * SpMV stages the p bands, values, columns and row offsets of each tile in
- * shared memory by bulk async copies (TMA).  A column outside every band is
- * read from global memory, so the hint never changes results.  graph_padded
- * != 0 promises >= 4 readable ints after row_offsets[N] and after
- * col_indices[nnz-1] (required for the staged path).  nbands <= 9. */
+ * TMA SpMV bulk-prefetches each tile's p bands into L2 when it issues the
+ * tile's values; the hint only moves data earlier, so it never changes
+ * results.  graph_padded != 0 promises >= 4 readable ints after
+ * row_offsets[N] and after col_indices[nnz-1].  nbands <= 9. */
 int uqg_ctx_set_band_hint(uqg_ctx* ctx, int nbands, const int* starts_host,
                           const int* extras_host, int graph_padded);
 
@@ -58,9 +57,9 @@ int uqg_ctx_set_band_hint(uqg_ctx* ctx, int nbands, const int* starts_host,
 #define UQG_K_KL 0
 #define UQG_K_ASSEMBLE 1
 #define UQG_K_PCG_INIT 2
-#define UQG_K_PCG_SPMV 3   /* Ap = A p + p.Ap          (dominant kernel) */
-#define UQG_K_PCG_UPDATE 4 /* x, r update + r.r, r.z                    */
-#define UQG_K_PCG_DIR 5    /* p = z + beta p                             */
+#define UQG_K_PCG_SPMV 3   /* Ap = A p + p.Ap                           */
+#define UQG_K_PCG_UPDATE 4 /* r update + r.r, r.z                       */
+#define UQG_K_PCG_DIR 5    /* p = z + beta p, deferred x updates         */
 #define UQG_K_DOT 6        /* lane_dot / qoi                             */
 #define UQG_K_GROUP 7      /* rank sort + chunk                          */
 #define UQG_K_SPMV 8       /* standalone spmv                            */
@@ -175,6 +174,11 @@ int uqg_pcg(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const i
 
 /* Device bytes of scratch uqg_pcg needs for (N, S, G) (r, p, Ap, partials). */
 long long uqg_pcg_workspace_bytes(int N, int nnz, int S, int G);
+
+/* Iterations per deferred solution update in the launch loop (UQG_X_DEFER,
+ * default 4; 1 = x updated every iteration): x += alpha_j p_j is applied kx
+ * iterations at a time in increasing j - identical bits for every kx. */
+int uqg_pcg_x_defer(void);
 
 /* Face form of the 2D 5-point FV operator (same matrix as uqg_assemble_fv2d,
  * stored once per face instead of once per CSR entry; fv2d.py:46-80 values).

@@ -50,6 +50,7 @@ SIGNATURES = {
                          _c_double, _c_int, _p, _p, _p, _p, _p, _p, _c_int,
                          ctypes.POINTER(_c_int), _p]),
     "uqg_pcg_workspace_bytes": (_c_ll, [_c_int, _c_int, _c_int, _c_int]),
+    "uqg_pcg_x_defer": (_c_int, []),
     "uqg_assemble_fv2d_faces": (_c_int, [_p, _c_int, _c_int, _c_int, _p, _c_double, _c_int, _p,
                                          _p, _p, _p]),
     "uqg_spmv_fv2d": (_c_int, [_p, _c_int, _c_int, _c_int, _p, _p, _c_double, _p, _p, _p]),

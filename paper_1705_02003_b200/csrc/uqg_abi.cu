@@ -151,20 +151,34 @@ int persistent_mode() {
   return m;
 }
 
+// UQG_X_DEFER: iterations per deferred solution update in the launch loop
+// (PcgState::kx; 1 = x updated every iteration).  Results are identical for
+// every value; the workspace grows by kx - 1 vectors per group.
+int x_defer() {
+  static const int k = [] {
+    const char* e = getenv("UQG_X_DEFER");
+    const int v = e ? atoi(e) : 4;
+    return v < 1 ? 1 : (v > kMaxKx ? kMaxKx : v);
+  }();
+  return k;
+}
+
 size_t pcg_layout(Carver& c, long long N, const Geo& geo, int G, PcgState* st, double** r,
-                  double** p, double** ap) {
+                  double** p, double** ap, int kx = x_defer()) {
   const size_t vec = (size_t)G * N * geo.S;
   const size_t lanes = (size_t)G * geo.S;
   double* rr = c.take<double>(vec);
-  double* pp = c.take<double>(vec);
+  double* pp = c.take<double>(vec * kx);
   double* aa = c.take<double>(vec);
   PcgState s{};
   s.G = G;
+  s.kx = kx;
+  s.pstride = vec;
   s.part = c.take<double>((size_t)G * geo.pstride * 2 * geo.S);
   s.ticket = c.take<unsigned int>((size_t)G * geo.tstride);
   s.rz = c.take<double>(lanes);
   s.thr = c.take<double>(lanes);
-  s.alpha = c.take<double>(lanes);
+  s.alpha = c.take<double>(lanes * kx);
   s.beta = c.take<double>(lanes);
   s.it = c.take<int>(G);
   s.done = c.take<int>(G);
@@ -440,6 +454,8 @@ int uqg_lane_dot(uqg_ctx* ctx, int N, int S, int G, const double* a, const doubl
   return UQG_OK;
 }
 
+int uqg_pcg_x_defer(void) { return x_defer(); }
+
 long long uqg_pcg_workspace_bytes(int N, int nnz, int S, int G) {
   (void)nnz;
   if (N < 0 || S < 1 || G < 1) return -1;
@@ -538,25 +554,6 @@ int pcg_impl(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const 
   UQG_REQUIRE(!hist_host || (hist_cap >= 0 && hist_rows_host), "uqg_pcg: bad history buffer");
   cudaStream_t s = as_stream(stream);
   Geo geo = make_geo(N, S, max_row_len);
-  Carver probe{nullptr};
-  size_t need = pcg_layout(probe, N, geo, G, nullptr, nullptr, nullptr, nullptr);
-  size_t hist_elems = hist_host ? (size_t)(hist_cap + 1) * G * S : 0;
-  need += hist_elems * sizeof(double) + 256;
-  int rc = ensure_ws(ctx, need);
-  if (rc) return rc;
-  Carver c{(char*)ws_base(ctx, need)};
-  PcgState st;
-  double *r, *p, *ap;
-  pcg_layout(c, N, geo, G, &st, &r, &p, &ap);
-  st.iters = iters;
-  st.conv = converged;
-  st.frozen = frozen;
-  st.hist = hist_host ? c.take<double>(hist_elems) : nullptr;
-  st.hist_cap = hist_cap;
-  UQG_TRY_CUDA(cudaMemsetAsync(st.ticket, 0, (size_t)G * geo.tstride * sizeof(unsigned), s));
-  UQG_TRY_CUDA(cudaMemsetAsync(st.ndone, 0, sizeof(int), s));
-  UQG_TRY_CUDA(cudaMemsetAsync(st.overflow, 0, sizeof(int), s));
-
   // Small batches: one cooperative launch runs the whole solve (uqg_persistent.cu).
   // UQG_PCG_PERSISTENT: 2 = cluster-barrier kernel, 1 = cooperative kernel,
   // 0 = launch loop; auto = cluster kernel for small batches (< 512 MB per
@@ -577,6 +574,27 @@ int pcg_impl(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const 
   }
   if (!use_cluster && geo.sc == 1 && (pmode == 1 || (pmode < 0 && small)))
     pblocks = persistent_blocks(geo, G);
+  // workspace: the persistent kernel updates x in place (kx = 1)
+  const int kx = pblocks > 0 ? 1 : x_defer();
+  Carver probe{nullptr};
+  size_t need = pcg_layout(probe, N, geo, G, nullptr, nullptr, nullptr, nullptr, kx);
+  size_t hist_elems = hist_host ? (size_t)(hist_cap + 1) * G * S : 0;
+  need += hist_elems * sizeof(double) + 256;
+  int rc = ensure_ws(ctx, need);
+  if (rc) return rc;
+  Carver c{(char*)ws_base(ctx, need)};
+  PcgState st;
+  double *r, *p, *ap;
+  pcg_layout(c, N, geo, G, &st, &r, &p, &ap, kx);
+  st.iters = iters;
+  st.conv = converged;
+  st.frozen = frozen;
+  st.hist = hist_host ? c.take<double>(hist_elems) : nullptr;
+  st.hist_cap = hist_cap;
+  UQG_TRY_CUDA(cudaMemsetAsync(st.ticket, 0, (size_t)G * geo.tstride * sizeof(unsigned), s));
+  UQG_TRY_CUDA(cudaMemsetAsync(st.ndone, 0, sizeof(int), s));
+  UQG_TRY_CUDA(cudaMemsetAsync(st.overflow, 0, sizeof(int), s));
+
   if (pblocks > 0) {
     PersistBufs pb = g_persist;
     UQG_TRY_CUDA(cudaMemsetAsync(pb.bar, 0, (2 * (size_t)G + 1) * sizeof(unsigned), s));
@@ -628,11 +646,15 @@ int pcg_impl(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const 
                    launch_pcg_spmv(gact, G, s, N, nnz, st, op.ro, op.ci, op.vals, p, ap,
                                    ctx->bands.nb ? &ctx->bands : nullptr));
       UQG_LAUNCH(UQG_K_PCG_UPDATE, s, launch_pcg_update(gact, G, s, N, st, dinv, maxit, r, ap));
+      if (kx > 1 && (launched + k + 1) % kx == 0)  // iteration launched + k closes a window
+        UQG_LAUNCH(UQG_K_PCG_DIR, s, launch_pcg_flush(gact, G, s, N, st, x, p, true));
       UQG_LAUNCH(UQG_K_PCG_DIR, s, launch_pcg_dir(gact, G, s, N, st, dinv, r, x, p));
     }
     launched += chunk;
     chunk = std::min(chunk * 2, 64);
   }
+  if (pblocks == 0 && kx > 1)  // deferred x updates still pending at termination
+    UQG_LAUNCH(UQG_K_PCG_DIR, s, launch_pcg_flush(with_groups(geo, G), G, s, N, st, x, p, false));
   UQG_LAUNCH(UQG_K_OTHER, s, launch_pcg_finalize(G, S, s, st, ens_iters));
   // breakdown / history bookkeeping
   std::vector<int> h_status(G);

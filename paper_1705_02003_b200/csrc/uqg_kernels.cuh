@@ -97,7 +97,7 @@ struct PcgState {
   unsigned int* ticket;    // [G] last-block tickets
   double* rz;              // [G*S] r.z of the current iterate
   double* thr;             // [G*S] tol * ||b||
-  double* alpha;           // [G*S]
+  double* alpha;           // [kx][G*S]
   double* beta;            // [G*S]
   int* iters;              // [G*S] -> caller's iterations_per_lane
   unsigned char* conv;     // [G*S] -> caller's converged_per_lane
@@ -109,7 +109,22 @@ struct PcgState {
   double* hist;            // [(hist_cap+1)][G][S] or nullptr
   int hist_cap;
   int* overflow;           // [1] history capacity exceeded
+  // Deferred solution update (launch loop): p_k lives in buffer k % kx of p
+  // ([kx][G][N][S], pstride doubles apart) and alpha_k in alpha[k % kx][G*S];
+  // x += alpha_j p_j is applied for kx iterations at once by pcg_flush (every
+  // kx-th iteration, and for the tail after the loop) in increasing j, i.e.
+  // the same roundings in the same order as one update per iteration.
+  // kx = 1: x and p updated in place every iteration by pcg_dir.
+  int kx;
+  size_t pstride;
 };
+
+constexpr int kMaxKx = 4;  // deepest supported deferral
+
+// Buffer slot of iteration `it`'s p / alpha.
+__device__ __forceinline__ int xslot(const PcgState& st, int it) {
+  return st.kx > 1 ? it % st.kx : 0;
+}
 
 // uqg_kernels.cu: KL coefficient, assembly, diagonal, grouping
 __global__ void kl_sep2d_kernel(int n1, const double* table1d, const int* mode_p,
@@ -157,6 +172,8 @@ void launch_pcg_spmv_fv2d(const Geo& geo, int G, cudaStream_t s, long long N, co
                           const Fv2dOp& op, const double* p, double* ap);
 void launch_pcg_update(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,
                        const double* dinv, int maxit, double* r, const double* ap);
+void launch_pcg_flush(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,
+                      double* x, const double* p, bool in_loop);
 void launch_pcg_dir(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,
                     const double* dinv, const double* r, double* x, double* p);
 void launch_pcg_finalize(int G, int S, cudaStream_t s, const PcgState& st, int* ens_iters);

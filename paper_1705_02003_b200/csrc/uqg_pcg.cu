@@ -234,6 +234,8 @@ __global__ void __launch_bounds__(256) pcg_spmv_kernel(long long N, long long nn
   extern __shared__ double red[];
   const int g = blockIdx.y, t = threadIdx.x;
   if (st.done[g] != kRunning) return;
+  const int xs = xslot(st, st.it[g]);  // buffer of p_k / alpha_k
+  p += (size_t)xs * st.pstride;
   const int sl = t % geo.Lp, rr = t / geo.Lp, S = geo.S;
   const double* vg = vals + (size_t)g * nnz * S + V * sl;
   const size_t base = (size_t)g * N * S + V * sl;
@@ -262,7 +264,7 @@ __global__ void __launch_bounds__(256) pcg_spmv_kernel(long long N, long long nn
         const double pap = red[j * geo.T + t];
         const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
         st.frozen[l] = fr;
-        st.alpha[l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
+        st.alpha[(size_t)xs * st.G * S + l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
       }
     }
     if (t == 0) st.it[g] += 1;
@@ -328,6 +330,8 @@ __device__ __forceinline__ void face_spmv_body(long long N, const Geo& geo, cons
   extern __shared__ __align__(16) double red[];
   const int g = blockIdx.y, t = threadIdx.x;
   if (st.done[g] != kRunning) return;
+  const int xs = xslot(st, st.it[g]);  // buffer of p_k / alpha_k
+  p += (size_t)xs * st.pstride;
   const int sl = t % geo.Lp, rr = t / geo.Lp, S = geo.S, R = geo.R, m = op.m;
   const int n = (int)N, B = gridDim.x, T = geo.T;
   const size_t base = (size_t)g * N * S + V * sl;
@@ -372,7 +376,7 @@ __device__ __forceinline__ void face_spmv_body(long long N, const Geo& geo, cons
         const double pap = red[j * geo.T + t];
         const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
         st.frozen[l] = fr;
-        st.alpha[l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
+        st.alpha[(size_t)xs * st.G * S + l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
       }
     }
     if (t == 0) st.it[g] += 1;
@@ -431,9 +435,12 @@ __global__ void __launch_bounds__(256, 3) pcg_update_kernel(long long N, Geo geo
   if (st.done[g] != kRunning) return;
   const int sl = t % geo.Lp, rr = t / geo.Lp, S = geo.S;
   const size_t base = (size_t)g * N * S + V * sl;
+  const int k_it = st.it[g] - 1;  // this is iteration k's update
+  const size_t GS = (size_t)st.G * S, l0 = (size_t)g * S + V * sl;
   double alpha[V];
 #pragma unroll
-  for (int j = 0; j < V; ++j) alpha[j] = sl < geo.L ? st.alpha[(size_t)g * S + V * sl + j] : 0.0;
+  for (int j = 0; j < V; ++j)
+    alpha[j] = sl < geo.L ? st.alpha[(size_t)xslot(st, k_it) * GS + l0 + j] : 0.0;
   const int B = gridDim.x, T = geo.T;
   for (int c0 = blockIdx.x; c0 < geo.chunks; c0 += kUpdateBatch * B) {
     int nk = (geo.chunks - 1 - c0) / B + 1;
@@ -527,6 +534,9 @@ __global__ void __launch_bounds__(256, 3) pcg_update_kernel(long long N, Geo geo
   }
 }
 
+// kx = 1: x += alpha p (deferred here from pcg_update) and p = z + beta p in
+// place.  kx > 1 (deferred solution update): only p_{k+1} = z + beta p_k, into
+// the next buffer; x is updated by pcg_update's FLUSH iterations and pcg_flush.
 template <int V>
 __global__ void __launch_bounds__(256, 3) pcg_dir_kernel(long long N, Geo geo, PcgState st,
                                                       const double* __restrict__ dinv,
@@ -537,15 +547,18 @@ __global__ void __launch_bounds__(256, 3) pcg_dir_kernel(long long N, Geo geo, P
   const int state = st.done[g];
   if (state == kDone) return;
   const int sl = t % geo.Lp, rr = t / geo.Lp, S = geo.S;
-  if (sl < geo.L) {
+  const bool running = state == kRunning, inplace = st.kx == 1;
+  if (sl < geo.L && (running || inplace)) {
+    const int it = st.it[g], k = it - 1;
     double alpha[V], beta[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) {
-      alpha[j] = st.alpha[(size_t)g * S + V * sl + j];
+      alpha[j] = st.alpha[(size_t)xslot(st, k) * st.G * S + (size_t)g * S + V * sl + j];
       beta[j] = st.beta[(size_t)g * S + V * sl + j];
     }
     const size_t base = (size_t)g * N * S + V * sl;
-    const bool running = state == kRunning;
+    const double* pk = p + (size_t)xslot(st, k) * st.pstride;
+    double* pn = p + (size_t)xslot(st, it) * st.pstride;  // == pk when kx = 1
     for (int chunk = blockIdx.x; chunk < geo.chunks; chunk += gridDim.x) {
       const ChunkRows cr = chunk_tiles(geo, chunk);
       // two tiles per step: all loads of both are issued before any store
@@ -559,8 +572,8 @@ __global__ void __launch_bounds__(256, 3) pcg_dir_kernel(long long N, Geo geo, P
           ok[u] = tile + u < cr.t1 && row < N;
           o[u] = base + (ok[u] ? row : 0) * S;
           if (ok[u]) {
-            ldv<V>(x + o[u], xv[u]);
-            ldv<V>(p + o[u], pv[u]);
+            if (inplace) ldv<V>(x + o[u], xv[u]);
+            ldv<V>(pk + o[u], pv[u]);
             if (running) {
               ldv<V>(r + o[u], rv[u]);
               if (dinv) ldgv<V>(dinv + o[u], dv[u]);
@@ -570,16 +583,18 @@ __global__ void __launch_bounds__(256, 3) pcg_dir_kernel(long long N, Geo geo, P
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           if (!ok[u]) continue;
+          if (inplace) {
 #pragma unroll
-          for (int j = 0; j < V; ++j) xv[u][j] = __dadd_rn(xv[u][j], __dmul_rn(alpha[j], pv[u][j]));
-          stv<V>(x + o[u], xv[u]);
+            for (int j = 0; j < V; ++j) xv[u][j] = __dadd_rn(xv[u][j], __dmul_rn(alpha[j], pv[u][j]));
+            stv<V>(x + o[u], xv[u]);
+          }
           if (running) {
 #pragma unroll
             for (int j = 0; j < V; ++j) {
               const double zv = dinv ? __dmul_rn(rv[u][j], dv[u][j]) : rv[u][j];
               pv[u][j] = __dadd_rn(zv, __dmul_rn(beta[j], pv[u][j]));
             }
-            stv<V>(p + o[u], pv[u]);
+            stv<V>(pn + o[u], pv[u]);
           }
         }
       }
@@ -588,6 +603,53 @@ __global__ void __launch_bounds__(256, 3) pcg_dir_kernel(long long N, Geo geo, P
   if (state == kFinishing && last_block(st.ticket, g, gridDim.x, geo.tstride) && t == 0) {
     st.done[g] = kDone;
     atomicAdd(st.ndone, 1);
+  }
+}
+
+// Deferred solution update (PcgState::kx > 1): x += alpha_j p_j over a window
+// of iterations j, in increasing j.  in_loop: launched between pcg_update and
+// pcg_dir of every kx-th iteration (it % kx == 0), window = the last kx
+// iterations of every group not yet DONE - before pcg_dir overwrites the
+// oldest p buffer.  Otherwise (after the loop): the it % kx updates still
+// pending for each group.
+template <int V>
+__global__ void __launch_bounds__(256) pcg_flush_kernel(long long N, Geo geo, PcgState st,
+                                                     double* __restrict__ x,
+                                                     const double* __restrict__ p, int in_loop) {
+  const int g = blockIdx.y, t = threadIdx.x;
+  const int it = st.it[g], kx = st.kx;
+  const int n = in_loop ? ((st.done[g] != kDone && it % kx == 0) ? kx : 0) : it % kx;
+  const int sl = t % geo.Lp, rr = t / geo.Lp, S = geo.S;
+  if (n == 0 || sl >= geo.L) return;
+  const size_t base = (size_t)g * N * S + V * sl, GS = (size_t)st.G * S;
+  const size_t l0 = (size_t)g * S + V * sl;
+  double aj[kMaxKx][V];
+  const double* pj[kMaxKx];
+#pragma unroll
+  for (int q = 0; q < kMaxKx; ++q) {  // oldest first: j = it - n + q
+    const int sj = q < n ? xslot(st, it - n + q) : 0;
+    pj[q] = p + (size_t)sj * st.pstride;
+#pragma unroll
+    for (int j = 0; j < V; ++j) aj[q][j] = q < n ? st.alpha[(size_t)sj * GS + l0 + j] : 0.0;
+  }
+  for (int chunk = blockIdx.x; chunk < geo.chunks; chunk += gridDim.x) {
+    const ChunkRows cr = chunk_tiles(geo, chunk);
+    for (long long tile = cr.t0; tile < cr.t1; ++tile) {
+      const long long row = tile * geo.R + rr;
+      if (row >= N) continue;
+      const size_t o = base + row * S;
+      double xv[V], pv[kMaxKx][V];
+      ldv<V>(x + o, xv);
+#pragma unroll
+      for (int q = 0; q < kMaxKx; ++q)
+        if (q < n) ldv<V>(pj[q] + o, pv[q]);
+#pragma unroll
+      for (int q = 0; q < kMaxKx; ++q)
+        if (q < n)
+#pragma unroll
+          for (int j = 0; j < V; ++j) xv[j] = __dadd_rn(xv[j], __dmul_rn(aj[q][j], pv[q][j]));
+      stv<V>(x + o, xv);
+    }
   }
 }
 
@@ -706,6 +768,8 @@ __global__ void __launch_bounds__(256, 4) pcg_spmv_fv2d_tma_kernel(long long N, 
   extern __shared__ __align__(128) double red[];
   const int g = blockIdx.y, t = threadIdx.x;
   if (st.done[g] != kRunning) return;
+  const int xs = xslot(st, st.it[g]);  // buffer of p_k / alpha_k
+  p += (size_t)xs * st.pstride;
   const int S = geo.S, R = geo.R, T = geo.T, m = op.m, n = (int)N, B = gridDim.x;
   const int sl = t % geo.Lp, rr = t / geo.Lp;
   const bool lane_ok = sl < geo.L;
@@ -802,7 +866,7 @@ __global__ void __launch_bounds__(256, 4) pcg_spmv_fv2d_tma_kernel(long long N, 
         const double pap = red[j * T + t];
         const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
         st.frozen[l] = fr;
-        st.alpha[l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
+        st.alpha[(size_t)xs * st.G * S + l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
       }
     }
     if (t == 0) st.it[g] += 1;
@@ -822,6 +886,8 @@ __global__ void __launch_bounds__(256, MINB) pcg_spmv_tma_kernel(long long N, lo
   extern __shared__ __align__(128) double red[];
   const int g = blockIdx.y, t = threadIdx.x;
   if (st.done[g] != kRunning) return;
+  const int xs = xslot(st, st.it[g]);  // buffer of p_k / alpha_k
+  p += (size_t)xs * st.pstride;
   const int S = geo.S, R = geo.R;
   const double* pg_all = p + (size_t)g * N * S;
   const size_t stage_doubles = (size_t)R * ML * S;
@@ -914,7 +980,7 @@ __global__ void __launch_bounds__(256, MINB) pcg_spmv_tma_kernel(long long N, lo
             const double pap = red[j * geo.T + t];
             const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
             st.frozen[l] = fr;
-            st.alpha[l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
+            st.alpha[(size_t)xs * st.G * S + l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
           }
         }
         if (t == 0) st.it[g] += 1;
@@ -1014,6 +1080,8 @@ __global__ void __launch_bounds__(288, 2) pcg_spmv_ws_kernel(
   __shared__ int s_last;
   const int g = blockIdx.y, t = threadIdx.x;
   if (st.done[g] != kRunning) return;
+  const int xs = xslot(st, st.it[g]);  // buffer of p_k / alpha_k
+  p += (size_t)xs * st.pstride;
   const int S = geo.S, R = geo.R, T = geo.T;  // T = 256 consumer threads
   const int stage_doubles = R * ML * S;
   double* stage = red + V * T;
@@ -1114,7 +1182,7 @@ __global__ void __launch_bounds__(288, 2) pcg_spmv_ws_kernel(
             const double pap = red[j * geo.T + t];
             const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
             st.frozen[l] = fr;
-            st.alpha[l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
+            st.alpha[(size_t)xs * st.G * S + l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
           }
         }
         if (t == 0) st.it[g] += 1;
@@ -1352,6 +1420,12 @@ void launch_pcg_update(const Geo& geo, int G, cudaStream_t s, long long N, const
   const Geo gl = geo.V == 2 ? sized(geo, c2, pcg_update_kernel<2>, geo.T, smem)
                             : sized(geo, c1, pcg_update_kernel<1>, geo.T, smem);
   UQG_DISPATCH_V(gl, pcg_update_kernel, dim3(gl.B, G), smem, s, N, gl, st, dinv, maxit, r, ap);
+}
+
+void launch_pcg_flush(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,
+                      double* x, const double* p, bool in_loop) {
+  const Geo& gl = geo;  // B preset by the caller
+  UQG_DISPATCH_V(gl, pcg_flush_kernel, dim3(gl.B, G), 0, s, N, gl, st, x, p, in_loop ? 1 : 0);
 }
 
 void launch_pcg_dir(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,

@@ -105,3 +105,18 @@ def test_face_pcg_bitwise_equal_csr_pcg(tmp_path, persistent, variant):
     assert np.array_equal(csr_c, fac_c)
     assert np.array_equal(csr_s, fac_s)
     assert not np.array_equal(csr_c, csr_s)  # the random y coefficient does change the solve
+
+
+def test_deferred_x_update_bitwise(tmp_path):
+    """x += alpha_j p_j applied kx iterations at a time (UQG_X_DEFER; pcg_update
+    FLUSH iterations + pcg_flush) rounds in the same order as the per-iteration
+    update: every kx gives the bits of kx = 1, CSR and face operator, launch loop."""
+    outs = {}
+    for kx in ("1", "2", "3", "4"):
+        env = dict(os.environ, UQG_PCG_PERSISTENT="0", UQG_X_DEFER=kx)
+        dst = tmp_path / f"x{kx}.npy"
+        subprocess.run([sys.executable, "-c", _SCRIPT, str(ROOT), str(dst)], env=env, check=True)
+        outs[kx] = np.load(dst, allow_pickle=True)
+    for kx in ("2", "3", "4"):
+        for a, b in zip(outs[kx], outs["1"]):
+            assert np.array_equal(a, b), kx
