@@ -39,17 +39,30 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
+    """Compile libuqg.so.  Safe under concurrent callers (e.g. every rank of a
+    torchrun job finding a stale library): one builds under an exclusive file
+    lock, the others wait and reuse its result."""
+    import fcntl
+
     if not force and not needs_build():
         return LIB
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I", str(PKG.parent / "include"), "-o", str(LIB) + ".tmp",
-           *[str(CSRC / s) for s in SOURCES]]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if verbose or res.returncode:
-        sys.stderr.write(res.stdout + res.stderr)
-    if res.returncode:
-        raise RuntimeError(f"nvcc failed ({res.returncode})")
-    os.replace(str(LIB) + ".tmp", LIB)
-    (PKG / "ptxas.log").write_text(res.stderr)
+    with open(PKG / ".build.lock", "w") as lock:
+        fcntl.flock(lock, fcntl.LOCK_EX)
+        try:
+            if not force and not needs_build():  # built by another process meanwhile
+                return LIB
+            tmp = f"{LIB}.tmp.{os.getpid()}"
+            cmd = [_nvcc(), *NVCC_FLAGS, "-I", str(PKG.parent / "include"), "-o", tmp,
+                   *[str(CSRC / s) for s in SOURCES]]
+            res = subprocess.run(cmd, capture_output=True, text=True)
+            if verbose or res.returncode:
+                sys.stderr.write(res.stdout + res.stderr)
+            if res.returncode:
+                raise RuntimeError(f"nvcc failed ({res.returncode})")
+            os.replace(tmp, LIB)
+            (PKG / "ptxas.log").write_text(res.stderr)
+        finally:
+            fcntl.flock(lock, fcntl.LOCK_UN)
     return LIB
 
 
