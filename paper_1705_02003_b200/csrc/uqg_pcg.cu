@@ -613,7 +613,7 @@ __global__ void __launch_bounds__(256, 3) pcg_dir_kernel(long long N, Geo geo, P
 // oldest p buffer.  Otherwise (after the loop): the it % kx updates still
 // pending for each group.
 template <int V>
-__global__ void __launch_bounds__(256) pcg_flush_kernel(long long N, Geo geo, PcgState st,
+__global__ void __launch_bounds__(256, 2) pcg_flush_kernel(long long N, Geo geo, PcgState st,
                                                      double* __restrict__ x,
                                                      const double* __restrict__ p, int in_loop) {
   const int g = blockIdx.y, t = threadIdx.x;
@@ -634,21 +634,34 @@ __global__ void __launch_bounds__(256) pcg_flush_kernel(long long N, Geo geo, Pc
   }
   for (int chunk = blockIdx.x; chunk < geo.chunks; chunk += gridDim.x) {
     const ChunkRows cr = chunk_tiles(geo, chunk);
-    for (long long tile = cr.t0; tile < cr.t1; ++tile) {
-      const long long row = tile * geo.R + rr;
-      if (row >= N) continue;
-      const size_t o = base + row * S;
-      double xv[V], pv[kMaxKx][V];
-      ldv<V>(x + o, xv);
+    // two tiles per step: all loads of both are issued before any store
+    for (long long tile = cr.t0; tile < cr.t1; tile += 2) {
+      double xv[2][V], pv[2][kMaxKx][V];
+      bool ok[2];
+      size_t o[2];
 #pragma unroll
-      for (int q = 0; q < kMaxKx; ++q)
-        if (q < n) ldv<V>(pj[q] + o, pv[q]);
+      for (int u = 0; u < 2; ++u) {
+        const long long row = (tile + u) * geo.R + rr;
+        ok[u] = tile + u < cr.t1 && row < N;
+        o[u] = base + (ok[u] ? row : 0) * S;
+        if (ok[u]) {
+          ldv<V>(x + o[u], xv[u]);
 #pragma unroll
-      for (int q = 0; q < kMaxKx; ++q)
-        if (q < n)
+          for (int q = 0; q < kMaxKx; ++q)
+            if (q < n) ldv<V>(pj[q] + o[u], pv[u][q]);
+        }
+      }
 #pragma unroll
-          for (int j = 0; j < V; ++j) xv[j] = __dadd_rn(xv[j], __dmul_rn(aj[q][j], pv[q][j]));
-      stv<V>(x + o, xv);
+      for (int u = 0; u < 2; ++u) {
+        if (!ok[u]) continue;
+#pragma unroll
+        for (int q = 0; q < kMaxKx; ++q)
+          if (q < n)
+#pragma unroll
+            for (int j = 0; j < V; ++j)
+              xv[u][j] = __dadd_rn(xv[u][j], __dmul_rn(aj[q][j], pv[u][q][j]));
+        stv<V>(x + o[u], xv[u]);
+      }
     }
   }
 }
