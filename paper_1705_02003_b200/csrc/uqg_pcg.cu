@@ -2,17 +2,21 @@
 // (reference ensemble.py:116-281), templated on V lanes per thread.
 //
 // One PCG iteration = three streaming kernels over every active group:
-//   pcg_spmv   Ap = A p (CSR order, no FMA: bitwise scipy), p.Ap
-//              last chunk: freeze (p.Ap <= DBL_MIN), alpha
+//   pcg_spmv   Ap = A p (CSR order, no FMA: bitwise scipy; CSR or the FV2D
+//              face form), p.Ap; last chunk: freeze (p.Ap <= DBL_MIN), alpha
 //   pcg_update r -= alpha Ap, r.r and r.z (z = dinv r)
 //              last chunk: residual norm, history, breakdown, convergence,
 //              termination, beta
-//   pcg_dir    x += alpha p ; p = z + beta p
-// x's update is deferred from pcg_update to pcg_dir (same operands, same
-// rounding, so identical bits): pcg_update then streams 4 vectors instead of 7
-// and pcg_dir 6 instead of 4.  A group that terminates in pcg_update is in
-// state FINISHING; its pcg_dir applies the last x update only and moves it to
-// DONE.  A DONE group turns every later launch into a no-op.
+//   pcg_dir    p = z + beta p, and the solution update x += alpha p:
+//              kx = 1: in place every iteration (x's update deferred from
+//              pcg_update to pcg_dir: same operands, same rounding);
+//              kx > 1: p_{k+1} goes to the next of kx p buffers and
+//              pcg_flush applies x += alpha_j p_j for kx iterations at a time
+//              (every kx-th iteration, between pcg_update and pcg_dir, and for
+//              the tail after the loop) - the same roundings in the same order.
+// A group that terminates in pcg_update is in state FINISHING; its pcg_dir
+// applies the last in-place x update (kx = 1) and moves it to DONE.  A DONE
+// group turns every later launch into a no-op.
 //
 // Work distribution: blocks of group g (blockIdx.y) grid-stride over the
 // group's reduction chunks (consecutive tiles of rows); see Geo.
