@@ -120,3 +120,18 @@ def test_deferred_x_update_bitwise(tmp_path):
     for kx in ("2", "3", "4"):
         for a, b in zip(outs[kx], outs["1"]):
             assert np.array_equal(a, b), kx
+
+
+@pytest.mark.parametrize("S", [6, 64, 130, 512])
+def test_face_pcg_wide_ensembles_bitwise(S):
+    """Wide and non-power-of-two ensembles (lane padding Lp > L, one row per
+    tile at S = 512): face-form solve == CSR solve, bit for bit."""
+    f = uq.build_field(0.2, 1.0, 3, 0.0)
+    ys = np.random.default_rng(S).uniform(-1, 1, (2, S, 3))
+    out = []
+    for faces in (False, True):
+        s = uq.EnsembleSolver2D(f, 24, 1e-8, 3000, faces=faces)
+        r = s.solve_groups(ys)
+        out.append((r.iterations, r.qoi, r.converged))
+    for a, b in zip(*out):
+        assert np.array_equal(a, b)
