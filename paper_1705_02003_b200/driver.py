@@ -48,8 +48,10 @@ def adaptive_run(cfg: StudyConfig, solver: EnsembleSolver | None = None, shard=N
 
     ``shard``: optional callable(plan, coords_by_id) -> (iters, qois, notes)
     replacing ``solver.solve_plan`` (multi-GPU sharded solve + allgather).
-    ``device_keys``: evaluate the iteration surrogate on the GPU
-    (``SparseGrid.evaluate_device``; bit-identical keys on this channel).
+    ``device_keys``: fit and evaluate the iteration surrogate on the GPU
+    (``SparseGrid.fit_device`` / ``evaluate_device``; bit-identical surpluses
+    and keys on this channel; the QoI channel, whose surpluses steer
+    refinement, stays on the host BLAS path).
     ``residual_sink(level, ensemble, history)``: per-ensemble lane residual
     histories, as the reference's ``adaptive_run(residual_sink=...)``
     (``report.residual_sink`` writes the reference's CSVs).
@@ -85,7 +87,7 @@ def adaptive_run(cfg: StudyConfig, solver: EnsembleSolver | None = None, shard=N
                                 level, "sur")
         iters, qois, notes = solve(plan, coords_by_id)
         grid.fit(QOI, {sid: qois[sid] for sid in ids})
-        grid.fit(ITER, {sid: iters[sid] for sid in ids})
+        (grid.fit_device if device_keys else grid.fit)(ITER, {sid: iters[sid] for sid in ids})
         records.append(LevelRecord(level, ids, coords, predicted, plan.ensembles, plan.padding,
                                    iters, qois, notes))
         if level >= cap:

@@ -154,26 +154,57 @@ class SparseGrid:
         channel (integer data on the dyadic grid) every term is exact, so the
         keys equal the host's bit for bit; on other channels they agree to
         rounding."""
-        from . import _lib
-
         c = self.surplus[channel]
         n = len(self.nodes) if n_nodes is None else n_nodes
         c = c[:n]
         if not np.all(np.isfinite(c)):
             raise ValueError(f"channel {channel!r} has unfitted surpluses")
-        pts = np.ascontiguousarray(self.to_canonical(np.asarray(points, dtype=float)))
-        d_pts = _lib.to_dev(pts)
-        out = d_pts.new_empty((len(pts),))
+        pts = self.to_canonical(np.asarray(points, dtype=float))
+        return self._basis_dot_device(pts, self._ctr[:n], self._hw[:n], c)
+
+    @staticmethod
+    def _basis_dot_device(pts_canonical, centers, widths, surplus) -> np.ndarray:
+        """``basis(pts, nodes) @ surplus`` on the GPU (one CTA per point, the
+        basis formed as hier_grid.py:317-328 forms it)."""
+        from . import _lib
+
+        pts = np.ascontiguousarray(pts_canonical, dtype=np.float64)
+        n_pts, n = len(pts), len(surplus)
+        if n_pts == 0:
+            return np.zeros(0)
         if n == 0:
-            return np.zeros(len(pts))
+            return np.zeros(n_pts)
         # keep the device copies referenced until the kernel has run (a temporary
         # freed before the launch could be handed to the next allocation)
-        d_ctr = _lib.to_dev(np.ascontiguousarray(self._ctr[:n]))
-        d_hw = _lib.to_dev(np.ascontiguousarray(self._hw[:n]))
-        d_c = _lib.to_dev(np.ascontiguousarray(c))
-        _lib.call("uqg_surrogate_eval", _lib.ctx(), _lib.ptr(d_pts), len(pts), self.dim,
+        d_pts = _lib.to_dev(pts)
+        out = d_pts.new_empty((n_pts,))
+        d_ctr = _lib.to_dev(np.ascontiguousarray(centers, dtype=np.float64))
+        d_hw = _lib.to_dev(np.ascontiguousarray(widths, dtype=np.float64))
+        d_c = _lib.to_dev(np.ascontiguousarray(surplus, dtype=np.float64))
+        _lib.call("uqg_surrogate_eval", _lib.ctx(), _lib.ptr(d_pts), n_pts, pts.shape[1],
                   _lib.ptr(d_ctr), _lib.ptr(d_hw), _lib.ptr(d_c), n, _lib.ptr(out), _lib.stream())
         return out.cpu().numpy()
+
+    def fit_device(self, channel: str, values_by_pos: dict):
+        """``fit`` with each cohort's prior-interpolant subtraction on the GPU
+        (``hier_grid.py:277-315``): the cohorts still run in
+        ascending total level, each one's ``basis(cohort, prior) @ surplus``
+        evaluated by ``uqg_surrogate_eval`` over the gathered prior nodes.  On
+        the iteration channel every term is an exact dyadic product, so the
+        surpluses equal ``fit``'s bit for bit; on other channels they agree to
+        rounding (the sum order differs from host BLAS)."""
+        c = self.surplus.setdefault(channel, np.full(len(self.nodes), np.nan))
+        cohorts: dict[int, list[int]] = {}
+        for pos in self.frontier:
+            cohorts.setdefault(int(self._tot[pos]), []).append(pos)
+        for tot in sorted(cohorts):
+            grp = cohorts[tot]
+            v = np.array([float(values_by_pos[p]) for p in grp])
+            prior = np.flatnonzero(self._tot < tot)
+            if prior.size:
+                v = v - self._basis_dot_device(self._ctr[grp], self._ctr[prior],
+                                               self._hw[prior], c[prior])
+            c[grp] = v
 
     def error_indicator(self, channel: str) -> float:
         if not self.frontier:

@@ -69,3 +69,42 @@ def test_study_with_device_keys_reproduces_golden(c1_golden):
         assert [list(g) for g in rec.ensembles] == gold["ensembles"]
         if gold["predicted"] is not None:
             assert np.array_equal(rec.predicted, np.array(gold["predicted"]))
+
+
+@pytest.mark.parametrize("study,dim,init,tau,nmax", [
+    ("c1_adaptive", 3, 0, 1e-5, 10_000),
+    ("pde_test1_study", 4, 1, 1e-3, 600),
+    ("pde_test2_study", 4, 1, 1e-3, 600),
+])
+def test_device_surplus_fit(study, dim, init, tau, nmax):
+    """Surplus fitting on the device along the reference's
+    studies: iteration-channel surpluses bit-identical to the host fit, QoI
+    channel to rounding."""
+    import copy
+
+    doc = json.loads((GOLDEN / f"{study}.json").read_text())
+    host = SparseGrid(dim)
+    batch = host.add_initial_levels(init)
+    for lv in doc["levels"]:
+        start = len(host) - len(batch)
+        ids = list(range(start, len(host)))
+        dev = copy.deepcopy(host)
+        host.fit("qoi", dict(zip(ids, lv["qoi"])))
+        host.fit("iterations", dict(zip(ids, lv["iterations"])))
+        dev.fit_device("qoi", dict(zip(ids, lv["qoi"])))
+        dev.fit_device("iterations", dict(zip(ids, lv["iterations"])))
+        assert np.array_equal(dev.surplus["iterations"], host.surplus["iterations"])
+        hq = host.surplus["qoi"]
+        np.testing.assert_allclose(dev.surplus["qoi"], hq, rtol=1e-11,
+                                   atol=1e-12 * np.abs(hq).max())
+        batch, _ = host.refine(tau, "qoi", nmax)
+        if not batch:
+            break
+
+
+def test_study_with_device_keys_and_fit_matches_golden_plans(c1_golden):
+    from paper_1705_02003_b200.driver import adaptive_run
+    records, _, _ = adaptive_run(uq.CONFIGS["C1"], device_keys=True)
+    assert len(records) == len(c1_golden["levels"])
+    for rec, gold in zip(records, c1_golden["levels"]):
+        assert [list(g) for g in rec.ensembles] == gold["ensembles"]
