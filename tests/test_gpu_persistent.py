@@ -51,3 +51,24 @@ def test_persistent_bitwise_equals_launch_loop(tmp_path):
     assert got["1"].shape == got["0"].shape
     assert np.array_equal(got["1"], got["0"])
     assert np.array_equal(got["2"], got["0"])
+
+
+def test_reference_semantics_through_the_launch_loop():
+    """The PCG semantics tests (reference goldens, trivial systems, frozen and
+    breakdown lanes, acceptance criterion 1) re-run with the small systems
+    forced through the launch loop - deferred solution update included - instead
+    of the persistent kernel they take by default."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, UQG_PCG_PERSISTENT="0", UQG_X_DEFER="4")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        str(root / "tests" / "test_gpu_parity.py"), "-k",
+                        "pcg_matches_reference_golden or trivial_systems or subnormal or "
+                        "nonfinite or acceptance_crit1 or duplicated_lanes or companions"],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout and "failed" not in r.stdout
