@@ -427,9 +427,12 @@ __device__ bool reduce_lanes(const double (&val)[NV][V], double* red, double* pa
 // chunks' tickets.  Every partial and the final sums are computed exactly as
 // reduce_lanes<NV, V> computes them, so results are bit-identical (same result
 // layout in red).  red must hold max(nk, 1) * NV * V * T doubles.
+// The in-block half of reduce_lanes_batch: one tree pass over the rows for all
+// nk chunks' values in red[((k*NV + v)*V + j)*T + t], then the chunk partials
+// written to part (no fence, no ticket).
 template <int NV, int V>
-__device__ bool reduce_lanes_batch(double* red, double* part, unsigned int* ticket, int g,
-                                   int chunk0, int stride, int nk, const Geo& geo) {
+__device__ void batch_tree_partials(double* red, double* part, int g, int chunk0, int stride,
+                                    int nk, const Geo& geo) {
   constexpr int NS = NV * V;
   const int t = threadIdx.x;
   const int T = geo.T, Lp = geo.Lp, R = geo.R, L = geo.L, S = geo.S;
@@ -450,6 +453,12 @@ __device__ bool reduce_lanes_batch(double* red, double* part, unsigned int* tick
           part[(((size_t)g * geo.pstride + chunk0 + k * stride) * NV + v) * S + V * t + j] =
               red[((k * NV + v) * V + j) * T + t];
   }
+}
+
+template <int NV, int V>
+__device__ bool reduce_lanes_batch(double* red, double* part, unsigned int* ticket, int g,
+                                   int chunk0, int stride, int nk, const Geo& geo) {
+  batch_tree_partials<NV, V>(red, part, g, chunk0, stride, nk, geo);
   __threadfence();
   __syncthreads();
   return finish_chunks<NV, V>(red, part, ticket, g, chunk0, stride, nk, geo);

@@ -79,30 +79,6 @@ __device__ __forceinline__ bool sync_group(unsigned* count, unsigned* gen, unsig
   }
 }
 
-// Per-chunk tree reduction (first half of reduce_lanes): writes the chunk's
-// per-lane partials, no ticket.
-template <int NV, int V>
-__device__ void chunk_partial(const double (&val)[NV][V], double* red, double* part, int g,
-                              int chunk, const Geo& geo) {
-  constexpr int NS = NV * V;
-  const int t = threadIdx.x;
-  const int T = geo.T, C = geo.chunks, S = geo.S;
-  __syncthreads();
-#pragma unroll
-  for (int v = 0; v < NV; ++v)
-#pragma unroll
-    for (int j = 0; j < V; ++j) red[(v * V + j) * T + t] = val[v][j];
-  __syncthreads();
-  tree_rows<NS>(red, T, geo.Lp, geo.R, t);
-  if (t < geo.L) {
-#pragma unroll
-    for (int v = 0; v < NV; ++v)
-#pragma unroll
-      for (int j = 0; j < V; ++j)
-        part[(((size_t)g * geo.pstride + chunk) * NV + v) * S + V * t + j] = red[(v * V + j) * T + t];
-  }
-}
-
 // Final reduction over a group's chunk partials (second half of reduce_lanes,
 // same order); result of value v, lane V*sl+j in red[(v*V+j)*T + sl].
 template <int NV, int V>
@@ -131,6 +107,24 @@ __device__ void final_partials(double* red, const double* part, int g, const Geo
   tree_rows<NS>(red, T, Lp, R, t);
 }
 
+// Chunks are reduced in batches of up to kPersistBatch per in-block tree
+// (batch_tree_partials: same partials, same bits as one tree per chunk).
+constexpr int kPersistBatch = 4;
+
+template <int NV, int V>
+__device__ __forceinline__ void stash(const double (&acc)[NV][V], double* red, int kb, int T,
+                                      int t) {
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int j = 0; j < V; ++j) red[((kb * NV + v) * V + j) * T + t] = acc[v][j];
+}
+
+__device__ __forceinline__ int batch_count(int c0, int C, int nb) {
+  const int n = (C - 1 - c0) / nb + 1;
+  return n < kPersistBatch ? n : kPersistBatch;
+}
+
 }  // namespace
 
 // Lane state kept (identically) in every block's shared memory.
@@ -155,7 +149,7 @@ __global__ void __launch_bounds__(256, 4) pcg_persistent_kernel(
   const int sl = t % geo.Lp, rr = t / geo.Lp;
   const unsigned nb = gridDim.x;
   LaneSmem ls;
-  ls.alpha = red + 2 * V * T;
+  ls.alpha = red + kPersistBatch * 2 * V * T;
   ls.beta = ls.alpha + S;
   ls.rz = ls.beta + S;
   ls.thr = ls.rz + S;
@@ -169,43 +163,48 @@ __global__ void __launch_bounds__(256, 4) pcg_persistent_kernel(
   const double* vg = vals ? vals + (size_t)g * nnz * S + V * sl : nullptr;
 
   // ---- init: x = 0, r = b, p = z, partials b.b and r.z
-  for (int chunk = blockIdx.x; chunk < C; chunk += nb) {
-    double acc[2][V] = {};
-    if (sl < L) {
-      const long long t0 = (long long)chunk * geo.chunk_tiles;
-      const long long t1 = t0 + geo.chunk_tiles < geo.tiles ? t0 + geo.chunk_tiles : geo.tiles;
-      for (long long tile = t0; tile < t1; ++tile) {
-        const long long row = tile * geo.R + rr;
-        if (row >= N) continue;
-        const size_t o = base + row * S;
-        double bv[V], zv[V], zero[V];
-        if (rhs) {
-          ldgv<V>(rhs + o, bv);
-        } else {
+  for (int c0 = blockIdx.x; c0 < C; c0 += kPersistBatch * nb) {
+    const int nk = batch_count(c0, C, nb);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int chunk = c0 + kb * nb;
+      double acc[2][V] = {};
+      if (sl < L) {
+        const long long t0 = (long long)chunk * geo.chunk_tiles;
+        const long long t1 = t0 + geo.chunk_tiles < geo.tiles ? t0 + geo.chunk_tiles : geo.tiles;
+        for (long long tile = t0; tile < t1; ++tile) {
+          const long long row = tile * geo.R + rr;
+          if (row >= N) continue;
+          const size_t o = base + row * S;
+          double bv[V], zv[V], zero[V];
+          if (rhs) {
+            ldgv<V>(rhs + o, bv);
+          } else {
 #pragma unroll
-          for (int j = 0; j < V; ++j) bv[j] = rhs_const;
+            for (int j = 0; j < V; ++j) bv[j] = rhs_const;
+          }
+          if (dinv) {
+            double dv[V];
+            ldgv<V>(dinv + o, dv);
+#pragma unroll
+            for (int j = 0; j < V; ++j) zv[j] = __dmul_rn(bv[j], dv[j]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < V; ++j) zv[j] = bv[j];
+          }
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            zero[j] = 0.0;
+            acc[0][j] = __fma_rn(bv[j], bv[j], acc[0][j]);
+            acc[1][j] = __fma_rn(bv[j], zv[j], acc[1][j]);
+          }
+          stv<V>(x + o, zero);
+          stv<V>(r + o, bv);
+          stv<V>(p + o, zv);
         }
-        if (dinv) {
-          double dv[V];
-          ldgv<V>(dinv + o, dv);
-#pragma unroll
-          for (int j = 0; j < V; ++j) zv[j] = __dmul_rn(bv[j], dv[j]);
-        } else {
-#pragma unroll
-          for (int j = 0; j < V; ++j) zv[j] = bv[j];
-        }
-#pragma unroll
-        for (int j = 0; j < V; ++j) {
-          zero[j] = 0.0;
-          acc[0][j] = __fma_rn(bv[j], bv[j], acc[0][j]);
-          acc[1][j] = __fma_rn(bv[j], zv[j], acc[1][j]);
-        }
-        stv<V>(x + o, zero);
-        stv<V>(r + o, bv);
-        stv<V>(p + o, zv);
       }
+      stash<2, V>(acc, red, kb, T, t);
     }
-    chunk_partial<2, V>(acc, red, partB, g, chunk, geo);
+    batch_tree_partials<2, V>(red, partB, g, c0, nb, nk, geo);
   }
   if (!sync_group<CL>(cnt, gen, nb, abort_flag)) return;
   final_partials<2, V>(red, partB, g, geo);
@@ -234,36 +233,41 @@ __global__ void __launch_bounds__(256, 4) pcg_persistent_kernel(
   while (!finish) {
     ++it;
     // ---- phase A: Ap = A p, partial p.Ap
-    for (int chunk = blockIdx.x; chunk < C; chunk += nb) {
-      double acc[1][V] = {};
-      if (sl < L) {
-        const long long t0 = (long long)chunk * geo.chunk_tiles;
-        const long long t1 = t0 + geo.chunk_tiles < geo.tiles ? t0 + geo.chunk_tiles : geo.tiles;
-        for (long long tile = t0; tile < t1; ++tile) {
-          const long long row = tile * geo.R + rr;
-          if (row >= N) continue;
-          double y[V], pv[V];
-          if (fv.tx) {
-            fv2d_row<V, true>(fv, N, S, g, V * sl, row, p + base, y, pv);
-          } else {
-            const int k0 = __ldg(&ro[row]), k1 = __ldg(&ro[row + 1]);
+    for (int c0 = blockIdx.x; c0 < C; c0 += kPersistBatch * nb) {
+      const int nk = batch_count(c0, C, nb);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int chunk = c0 + kb * nb;
+        double acc[1][V] = {};
+        if (sl < L) {
+          const long long t0 = (long long)chunk * geo.chunk_tiles;
+          const long long t1 = t0 + geo.chunk_tiles < geo.tiles ? t0 + geo.chunk_tiles : geo.tiles;
+          for (long long tile = t0; tile < t1; ++tile) {
+            const long long row = tile * geo.R + rr;
+            if (row >= N) continue;
+            double y[V], pv[V];
+            if (fv.tx) {
+              fv2d_row<V, true>(fv, N, S, g, V * sl, row, p + base, y, pv);
+            } else {
+              const int k0 = __ldg(&ro[row]), k1 = __ldg(&ro[row + 1]);
 #pragma unroll
-            for (int j = 0; j < V; ++j) y[j] = 0.0;
-            for (int k = k0; k < k1; ++k) {
-              double a[V], b[V];
-              ldgv<V>(vg + (size_t)k * S, a);
-              ldcgv<V>(p + base + (size_t)__ldg(&ci[k]) * S, b);
+              for (int j = 0; j < V; ++j) y[j] = 0.0;
+              for (int k = k0; k < k1; ++k) {
+                double a[V], b[V];
+                ldgv<V>(vg + (size_t)k * S, a);
+                ldcgv<V>(p + base + (size_t)__ldg(&ci[k]) * S, b);
 #pragma unroll
-              for (int j = 0; j < V; ++j) y[j] = __dadd_rn(y[j], __dmul_rn(a[j], b[j]));
+                for (int j = 0; j < V; ++j) y[j] = __dadd_rn(y[j], __dmul_rn(a[j], b[j]));
+              }
+              ldcgv<V>(p + base + row * S, pv);
             }
-            ldcgv<V>(p + base + row * S, pv);
-          }
-          stv<V>(ap + base + row * S, y);
+            stv<V>(ap + base + row * S, y);
 #pragma unroll
-          for (int j = 0; j < V; ++j) acc[0][j] = __fma_rn(pv[j], y[j], acc[0][j]);
+            for (int j = 0; j < V; ++j) acc[0][j] = __fma_rn(pv[j], y[j], acc[0][j]);
+          }
         }
+        stash<1, V>(acc, red, kb, T, t);
       }
-      chunk_partial<1, V>(acc, red, partA, g, chunk, geo);
+      batch_tree_partials<1, V>(red, partA, g, c0, nb, nk, geo);
     }
     if (!sync_group<CL>(cnt, gen, nb, abort_flag)) return;
     final_partials<1, V>(red, partA, g, geo);
@@ -282,38 +286,43 @@ __global__ void __launch_bounds__(256, 4) pcg_persistent_kernel(
     double alpha[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) alpha[j] = sl < L ? ls.alpha[V * sl + j] : 0.0;
-    for (int chunk = blockIdx.x; chunk < C; chunk += nb) {
-      double acc[2][V] = {};
-      if (sl < L) {
-        const long long t0 = (long long)chunk * geo.chunk_tiles;
-        const long long t1 = t0 + geo.chunk_tiles < geo.tiles ? t0 + geo.chunk_tiles : geo.tiles;
-        for (long long tile = t0; tile < t1; ++tile) {
-          const long long row = tile * geo.R + rr;
-          if (row >= N) continue;
-          const size_t o = base + row * S;
-          double rv[V], av[V], zv[V];
-          ldcgv<V>(r + o, rv);
-          ldcgv<V>(ap + o, av);
+    for (int c0 = blockIdx.x; c0 < C; c0 += kPersistBatch * nb) {
+      const int nk = batch_count(c0, C, nb);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int chunk = c0 + kb * nb;
+        double acc[2][V] = {};
+        if (sl < L) {
+          const long long t0 = (long long)chunk * geo.chunk_tiles;
+          const long long t1 = t0 + geo.chunk_tiles < geo.tiles ? t0 + geo.chunk_tiles : geo.tiles;
+          for (long long tile = t0; tile < t1; ++tile) {
+            const long long row = tile * geo.R + rr;
+            if (row >= N) continue;
+            const size_t o = base + row * S;
+            double rv[V], av[V], zv[V];
+            ldcgv<V>(r + o, rv);
+            ldcgv<V>(ap + o, av);
 #pragma unroll
-          for (int j = 0; j < V; ++j) rv[j] = __dsub_rn(rv[j], __dmul_rn(alpha[j], av[j]));
-          stv<V>(r + o, rv);
-          if (dinv) {
-            double dv[V];
-            ldgv<V>(dinv + o, dv);
+            for (int j = 0; j < V; ++j) rv[j] = __dsub_rn(rv[j], __dmul_rn(alpha[j], av[j]));
+            stv<V>(r + o, rv);
+            if (dinv) {
+              double dv[V];
+              ldgv<V>(dinv + o, dv);
 #pragma unroll
-            for (int j = 0; j < V; ++j) zv[j] = __dmul_rn(rv[j], dv[j]);
-          } else {
+              for (int j = 0; j < V; ++j) zv[j] = __dmul_rn(rv[j], dv[j]);
+            } else {
 #pragma unroll
-            for (int j = 0; j < V; ++j) zv[j] = rv[j];
-          }
+              for (int j = 0; j < V; ++j) zv[j] = rv[j];
+            }
 #pragma unroll
-          for (int j = 0; j < V; ++j) {
-            acc[0][j] = __fma_rn(rv[j], rv[j], acc[0][j]);
-            acc[1][j] = __fma_rn(rv[j], zv[j], acc[1][j]);
+            for (int j = 0; j < V; ++j) {
+              acc[0][j] = __fma_rn(rv[j], rv[j], acc[0][j]);
+              acc[1][j] = __fma_rn(rv[j], zv[j], acc[1][j]);
+            }
           }
         }
+        stash<2, V>(acc, red, kb, T, t);
       }
-      chunk_partial<2, V>(acc, red, partB, g, chunk, geo);
+      batch_tree_partials<2, V>(red, partB, g, c0, nb, nk, geo);
     }
     if (!sync_group<CL>(cnt, gen, nb, abort_flag)) return;
     final_partials<2, V>(red, partB, g, geo);
@@ -407,8 +416,24 @@ __global__ void __launch_bounds__(256, 4) pcg_persistent_kernel(
   }
 }
 
+// Lets every persistent instantiation take `smem` bytes of dynamic shared
+// memory (above the 48 KB default at large S); called before the occupancy
+// queries and the launch.
+static void allow_smem(size_t smem) {
+  static size_t configured = 48 * 1024;
+  if (smem <= configured) return;
+  const void* fns[] = {(const void*)pcg_persistent_kernel<2, false>,
+                       (const void*)pcg_persistent_kernel<1, false>,
+                       (const void*)pcg_persistent_kernel<2, true>,
+                       (const void*)pcg_persistent_kernel<1, true>};
+  for (const void* f : fns)
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  configured = smem;
+}
+
 size_t persistent_smem(const Geo& geo) {
-  return (size_t)2 * geo.V * geo.T * sizeof(double) + (size_t)4 * geo.S * sizeof(double) +
+  return (size_t)kPersistBatch * 2 * geo.V * geo.T * sizeof(double) +
+         (size_t)4 * geo.S * sizeof(double) +
          (size_t)geo.S * (sizeof(int) + 2) + 16;
 }
 
@@ -421,14 +446,18 @@ static const void* persistent_fn(int V) {
 // (non-portable) and at most the group's chunk count; 0 if not launchable.
 int persistent_cluster_size(const Geo& geo) {
   static int cached[2] = {-1, -1};
+  static size_t cached_smem[2] = {0, 0};
   const int vi = geo.V == 2;
-  if (cached[vi] < 0) {
+  const size_t smem = persistent_smem(geo);
+  if (cached[vi] < 0 || cached_smem[vi] != smem) {  // per (V, shared-memory size)
     const void* fn = persistent_fn<true>(geo.V);
     cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(16, 1, 1);
     cfg.blockDim = dim3(geo.T, 1, 1);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = smem;
+    allow_smem(smem);
+    cached_smem[vi] = smem;
     cudaLaunchAttribute attr;
     attr.id = cudaLaunchAttributeClusterDimension;
     attr.val.clusterDim.x = 16;
@@ -456,6 +485,7 @@ int persistent_blocks(const Geo& geo, int G) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t smem = persistent_smem(geo);
+  allow_smem(smem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, persistent_fn<false>(geo.V), geo.T, smem);
   const long long cap = (long long)per_sm * sms;
   long long b = cap / (G < 1 ? 1 : G);
@@ -478,6 +508,7 @@ cudaError_t launch_pcg_persistent(const Geo& geo, int G, int blocks, bool cluste
                   &rhs, &rhs_const, &dinv, &tol,       &maxit, &x,     &r,
                   &p,   &ap,        &partA, &partB,    &bar_count, &bar_gen, &abort_flag};
   const size_t smem = persistent_smem(gl);
+  allow_smem(smem);
   if (!cluster)
     return cudaLaunchCooperativeKernel(persistent_fn<false>(gl.V), dim3(blocks, G), dim3(gl.T),
                                        args, smem, s);
