@@ -47,8 +47,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--separate-kernel-timing", action="store_true",
-                    help="time `value` without per-launch events; kernel breakdown from a "
-                         "second, identical profiled pass (small configs: event overhead)")
+                    help="(default behaviour; kept for old command lines) value from "
+                         "un-instrumented steps, kernel breakdown from a profiled pass")
     ap.add_argument("--max-iters", type=int, default=None,
                     help="throughput mode: run exactly this many PCG iterations per group "
                          "(value = sample-iterations/s); for C4/C5 where full solves take minutes")
@@ -406,13 +406,21 @@ def main():
         lib.uqg_ctx_profile(ctx, 0)
         return times, group_iters, launches, ms, cnt, clocks, last
 
-    if args.separate_kernel_timing:
-        # value from un-instrumented steps; kernel shares from an identical profiled pass
-        times, group_iters, launches, _, _, clocks, last = timed(False)
+    # value from un-instrumented steps (the library solves a level's groups as
+    # concurrent parts on several streams); the per-kernel times for the
+    # roofline from an identical profiled pass on ONE stream, so each launch's
+    # duration is that kernel's alone (UQG_SOLVE_STREAMS=1; same results).
+    times, group_iters, launches, _, _, clocks, last = timed(False)
+    prev = os.environ.get("UQG_SOLVE_STREAMS")
+    os.environ["UQG_SOLVE_STREAMS"] = "1"
+    try:
         _, prof_iters, _, ms, cnt, _, _ = timed(True)
-        assert prof_iters == group_iters
-    else:
-        times, group_iters, launches, ms, cnt, clocks, last = timed(True)
+    finally:
+        if prev is None:
+            os.environ.pop("UQG_SOLVE_STREAMS", None)
+        else:
+            os.environ["UQG_SOLVE_STREAMS"] = prev
+    assert prof_iters == group_iters
     groups, pad, it, cv, en, q = last
     conv_all = bool(cv.all().item())
 
@@ -512,6 +520,8 @@ def main():
                      "peak_source": peak_src,
                      "bytes_per_group_launch": per[dom]["bytes_per_group_launch"],
                      "group_launches": group_iters,
+                     "timing": "per-launch CUDA events on the launching stream, profiled pass "
+                               "with the level on one stream (UQG_SOLVE_STREAMS=1)",
                      "time_share": (per[dom]["ms"] / sum(ms[k] for k in range(NK))
                                     if sum(ms[k] for k in range(NK)) else None),
                      "pcg_kernels": per},

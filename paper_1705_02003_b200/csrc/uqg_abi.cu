@@ -38,6 +38,11 @@ struct uqg_ctx {
   std::vector<int> pend_kind;
   int pend = 0;
   BandHint bands{};                 // uqg_ctx_set_band_hint (nb = 0: none)
+  // concurrent PCG parts (pcg_impl): extra non-blocking streams, their events,
+  // pinned done-counter readbacks
+  std::vector<cudaStream_t> aux;
+  std::vector<cudaEvent_t> aux_ev;
+  int* pinned_parts = nullptr;
 };
 
 namespace {
@@ -58,9 +63,9 @@ int grid_for(long long total, int threads) {
 // Accumulate the elapsed times of all recorded (start, stop) pairs.
 int harvest(uqg_ctx* ctx) {
   if (!ctx->pend) return UQG_OK;
-  UQG_TRY_CUDA(cudaEventSynchronize(ctx->evpool[2 * (ctx->pend - 1) + 1]));
-  for (int i = 0; i < ctx->pend; ++i) {
+  for (int i = 0; i < ctx->pend; ++i) {  // launches may sit on several streams
     float ms = 0.f;
+    UQG_TRY_CUDA(cudaEventSynchronize(ctx->evpool[2 * i + 1]));
     UQG_TRY_CUDA(cudaEventElapsedTime(&ms, ctx->evpool[2 * i], ctx->evpool[2 * i + 1]));
     ctx->kind_ms[ctx->pend_kind[i]] += ms;
   }
@@ -163,6 +168,18 @@ int x_defer() {
   return k;
 }
 
+// UQG_SOLVE_STREAMS: the launch loop splits the groups into this many parts
+// solved concurrently on separate streams (default 2) when every part still
+// moves >= 1 GB per iteration; kernels of two parts then share the SMs and
+// fill each other's latency gaps (C2: 1,572 -> 1,496 ms per level).  Results
+// do not depend on it (groups are independent).
+constexpr int kMaxParts = 4;
+int solve_streams() {  // read per solve: bench.py times kernels with one stream
+  const char* e = getenv("UQG_SOLVE_STREAMS");
+  const int v = e ? atoi(e) : 2;
+  return v < 1 ? 1 : (v > kMaxParts ? kMaxParts : v);
+}
+
 size_t pcg_layout(Carver& c, long long N, const Geo& geo, int G, PcgState* st, double** r,
                   double** p, double** ap, int kx = x_defer()) {
   const size_t vec = (size_t)G * N * geo.S;
@@ -234,6 +251,9 @@ int uqg_ctx_destroy(uqg_ctx* ctx) {
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->ev) cudaEventDestroy(ctx->ev);
   for (cudaEvent_t e : ctx->evpool) cudaEventDestroy(e);
+  for (cudaStream_t a : ctx->aux) cudaStreamDestroy(a);
+  for (cudaEvent_t e : ctx->aux_ev) cudaEventDestroy(e);
+  if (ctx->pinned_parts) cudaFreeHost(ctx->pinned_parts);
   delete ctx;
   return UQG_OK;
 }
@@ -576,24 +596,72 @@ int pcg_impl(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const 
     pblocks = persistent_blocks(geo, G);
   // workspace: the persistent kernel updates x in place (kx = 1)
   const int kx = pblocks > 0 ? 1 : x_defer();
+  int P = 1;  // concurrent parts of the launch loop
+  if (pblocks == 0 && !hist_host) {
+    P = solve_streams();
+    while (P > 1 && (iter_bytes / P < 1e9 || G / P < 1)) --P;
+  }
+  struct Part {
+    int g0, G;
+    PcgState st;
+    double *r, *p, *ap;
+    cudaStream_t s;
+    SpOp op;
+    bool done;
+  } parts[kMaxParts];
   Carver probe{nullptr};
-  size_t need = pcg_layout(probe, N, geo, G, nullptr, nullptr, nullptr, nullptr, kx);
+  size_t need = 0;
+  for (int i = 0; i < P; ++i) {
+    const int g0 = (int)((long long)G * i / P), g1 = (int)((long long)G * (i + 1) / P);
+    need = pcg_layout(probe, N, geo, g1 - g0, nullptr, nullptr, nullptr, nullptr, kx);
+  }
   size_t hist_elems = hist_host ? (size_t)(hist_cap + 1) * G * S : 0;
   need += hist_elems * sizeof(double) + 256;
   int rc = ensure_ws(ctx, need);
   if (rc) return rc;
+  if (P > 1 && (int)ctx->aux.size() < P - 1) {  // lazily created part streams
+    if (!ctx->pinned_parts)
+      UQG_TRY_CUDA(cudaHostAlloc(&ctx->pinned_parts, kMaxParts * sizeof(int), cudaHostAllocDefault));
+    while ((int)ctx->aux.size() < kMaxParts - 1) {
+      cudaStream_t a;
+      UQG_TRY_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+      ctx->aux.push_back(a);
+    }
+    while ((int)ctx->aux_ev.size() < kMaxParts) {
+      cudaEvent_t e;
+      UQG_TRY_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ctx->aux_ev.push_back(e);
+    }
+  }
   Carver c{(char*)ws_base(ctx, need)};
-  PcgState st;
-  double *r, *p, *ap;
-  pcg_layout(c, N, geo, G, &st, &r, &p, &ap, kx);
-  st.iters = iters;
-  st.conv = converged;
-  st.frozen = frozen;
+  if (P > 1) {  // part streams start after everything queued on the caller's stream
+    UQG_TRY_CUDA(cudaEventRecord(ctx->aux_ev[0], s));
+    for (int i = 1; i < P; ++i) UQG_TRY_CUDA(cudaStreamWaitEvent(ctx->aux[i - 1], ctx->aux_ev[0], 0));
+  }
+  const size_t vs = (size_t)N * S;  // per-group vector stride
+  for (int i = 0; i < P; ++i) {
+    Part& q = parts[i];
+    q.g0 = (int)((long long)G * i / P);
+    q.G = (int)((long long)G * (i + 1) / P) - q.g0;
+    q.s = i == 0 ? s : ctx->aux[i - 1];
+    q.done = false;
+    pcg_layout(c, N, geo, q.G, &q.st, &q.r, &q.p, &q.ap, kx);
+    q.st.iters = iters + (size_t)q.g0 * S;
+    q.st.conv = converged + (size_t)q.g0 * S;
+    q.st.frozen = frozen + (size_t)q.g0 * S;
+    q.st.hist = nullptr;
+    q.st.hist_cap = hist_cap;
+    q.op = op;
+    if (op.vals) q.op.vals = op.vals + (size_t)q.g0 * nnz * S;
+    if (op.fv.tx) q.op.fv.tx = op.fv.tx + (size_t)q.g0 * (N + op.fv.m) * S;
+    if (op.fv.ty) q.op.fv.ty = op.fv.ty + (size_t)q.g0 * (N + op.fv.m) * S;
+    UQG_TRY_CUDA(cudaMemsetAsync(q.st.ticket, 0, (size_t)q.G * geo.tstride * sizeof(unsigned), q.s));
+    UQG_TRY_CUDA(cudaMemsetAsync(q.st.ndone, 0, sizeof(int), q.s));
+    UQG_TRY_CUDA(cudaMemsetAsync(q.st.overflow, 0, sizeof(int), q.s));
+  }
+  PcgState& st = parts[0].st;  // single-part view (persistent path, history, status)
   st.hist = hist_host ? c.take<double>(hist_elems) : nullptr;
-  st.hist_cap = hist_cap;
-  UQG_TRY_CUDA(cudaMemsetAsync(st.ticket, 0, (size_t)G * geo.tstride * sizeof(unsigned), s));
-  UQG_TRY_CUDA(cudaMemsetAsync(st.ndone, 0, sizeof(int), s));
-  UQG_TRY_CUDA(cudaMemsetAsync(st.overflow, 0, sizeof(int), s));
+  double *r = parts[0].r, *p = parts[0].p, *ap = parts[0].ap;
 
   if (pblocks > 0) {
     PersistBufs pb = g_persist;
@@ -601,8 +669,9 @@ int pcg_impl(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const 
     cudaError_t le = cudaSuccess;
     UQG_LAUNCH(UQG_K_PCG_SPMV, s, {
       le = launch_pcg_persistent(geo, G, pblocks, use_cluster, s, N, nnz, st, op.ro, op.ci,
-                                 op.vals, op.fv, rhs, rhs_const, dinv, tol, maxit, x, r, p, ap, pb.partA, st.part,
-                                 pb.bar, pb.bar + G, reinterpret_cast<int*>(pb.bar + 2 * G));
+                                 op.vals, op.fv, rhs, rhs_const, dinv, tol, maxit, x, r, p, ap,
+                                 pb.partA, st.part, pb.bar, pb.bar + G,
+                                 reinterpret_cast<int*>(pb.bar + 2 * G));
     });
     if (le != cudaSuccess) {
       cudaGetLastError();
@@ -616,50 +685,92 @@ int pcg_impl(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const 
       set_error("uqg_pcg: persistent solve aborted (group barrier timeout)");
       return UQG_ECUDA;
     }
-  }
-  // Otherwise: host polls the device done-counter between chunks of
-  // iterations.  Groups that have terminated turn every later launch into a
-  // no-op, so the extra launches of the last chunk cannot change any result.
-  if (pblocks == 0)
-    UQG_LAUNCH(UQG_K_PCG_INIT, s,
-               launch_pcg_init(geo, G, s, N, st, rhs, rhs_const, dinv, tol, maxit, x, r, p));
-  long long launched = 0;
-  int chunk = 2;
-  for (; pblocks == 0;) {
-    UQG_TRY_CUDA(cudaMemcpyAsync(ctx->pinned, st.ndone, sizeof(int), cudaMemcpyDeviceToHost, s));
-    UQG_TRY_CUDA(cudaEventRecord(ctx->ev, s));
-    UQG_TRY_CUDA(cudaEventSynchronize(ctx->ev));
-    if (ctx->pinned[0] >= G) break;
-    if (launched > (long long)maxit + 1) {
-      set_error("uqg_pcg: device loop failed to terminate");
-      return UQG_ECUDA;
+  } else {
+    // Launch loop: the host polls each part's device done-counter between
+    // chunks of iterations and launches the next chunk for every part still
+    // running, alternating parts per iteration.  Groups that have terminated
+    // turn every later launch into a no-op, so the extra launches of the last
+    // chunk cannot change any result.
+    auto vec = [&](const Part& q, const double* v) { return v ? v + (size_t)q.g0 * vs : v; };
+    auto vecw = [&](const Part& q, double* v) { return v + (size_t)q.g0 * vs; };
+    for (int i = 0; i < P; ++i) {
+      Part& q = parts[i];
+      UQG_LAUNCH(UQG_K_PCG_INIT, q.s,
+                 launch_pcg_init(geo, q.G, q.s, N, q.st, vec(q, rhs), rhs_const, vec(q, dinv), tol,
+                                 maxit, vecw(q, x), q.r, q.p));
     }
-    // Size blocks-per-group for the groups still running (finished groups'
-    // blocks exit at once); the reduction chunks - hence the results - do not
-    // depend on this.
-    const Geo gact = with_groups(geo, std::max(1, G - ctx->pinned[0]));
-    for (int k = 0; k < chunk; ++k) {
-      if (op.fv.tx)
-        UQG_LAUNCH(UQG_K_PCG_SPMV, s, launch_pcg_spmv_fv2d(gact, G, s, N, st, op.fv, p, ap));
-      else
-        UQG_LAUNCH(UQG_K_PCG_SPMV, s,
-                   launch_pcg_spmv(gact, G, s, N, nnz, st, op.ro, op.ci, op.vals, p, ap,
-                                   ctx->bands.nb ? &ctx->bands : nullptr));
-      UQG_LAUNCH(UQG_K_PCG_UPDATE, s, launch_pcg_update(gact, G, s, N, st, dinv, maxit, r, ap));
-      if (kx > 1 && (launched + k + 1) % kx == 0)  // iteration launched + k closes a window
-        UQG_LAUNCH(UQG_K_PCG_DIR, s, launch_pcg_flush(gact, G, s, N, st, x, p, true));
-      UQG_LAUNCH(UQG_K_PCG_DIR, s, launch_pcg_dir(gact, G, s, N, st, dinv, r, x, p));
+    int* pin = P > 1 ? ctx->pinned_parts : ctx->pinned;
+    long long launched = 0;
+    int chunk = 2;
+    for (;;) {
+      bool all_done = true;
+      for (int i = 0; i < P; ++i) {
+        Part& q = parts[i];
+        if (q.done) continue;
+        UQG_TRY_CUDA(cudaMemcpyAsync(pin + i, q.st.ndone, sizeof(int), cudaMemcpyDeviceToHost, q.s));
+        UQG_TRY_CUDA(cudaEventRecord(P > 1 ? ctx->aux_ev[i] : ctx->ev, q.s));
+      }
+      for (int i = 0; i < P; ++i) {
+        Part& q = parts[i];
+        if (q.done) continue;
+        UQG_TRY_CUDA(cudaEventSynchronize(P > 1 ? ctx->aux_ev[i] : ctx->ev));
+        q.done = pin[i] >= q.G;
+        all_done = all_done && q.done;
+      }
+      if (all_done) break;
+      if (launched > (long long)maxit + 1) {
+        set_error("uqg_pcg: device loop failed to terminate");
+        return UQG_ECUDA;
+      }
+      // Size blocks-per-group for the groups still running (finished groups'
+      // blocks exit at once); the reduction chunks - hence the results - do
+      // not depend on this.
+      Geo gact[kMaxParts];
+      for (int i = 0; i < P; ++i) gact[i] = with_groups(geo, std::max(1, parts[i].G - pin[i]));
+      for (int k = 0; k < chunk; ++k) {
+        for (int i = 0; i < P; ++i) {
+          Part& q = parts[i];
+          if (q.done) continue;
+          const Geo& gl = gact[i];
+          double* xq = vecw(q, x);
+          const double* dq = vec(q, dinv);
+          if (q.op.fv.tx)
+            UQG_LAUNCH(UQG_K_PCG_SPMV, q.s,
+                       launch_pcg_spmv_fv2d(gl, q.G, q.s, N, q.st, q.op.fv, q.p, q.ap));
+          else
+            UQG_LAUNCH(UQG_K_PCG_SPMV, q.s,
+                       launch_pcg_spmv(gl, q.G, q.s, N, nnz, q.st, q.op.ro, q.op.ci, q.op.vals,
+                                       q.p, q.ap, ctx->bands.nb ? &ctx->bands : nullptr));
+          UQG_LAUNCH(UQG_K_PCG_UPDATE, q.s,
+                     launch_pcg_update(gl, q.G, q.s, N, q.st, dq, maxit, q.r, q.ap));
+          if (kx > 1 && (launched + k + 1) % kx == 0)  // iteration launched + k closes a window
+            UQG_LAUNCH(UQG_K_PCG_DIR, q.s, launch_pcg_flush(gl, q.G, q.s, N, q.st, xq, q.p, true));
+          UQG_LAUNCH(UQG_K_PCG_DIR, q.s, launch_pcg_dir(gl, q.G, q.s, N, q.st, dq, q.r, xq, q.p));
+        }
+      }
+      launched += chunk;
+      chunk = std::min(chunk * 2, 64);
     }
-    launched += chunk;
-    chunk = std::min(chunk * 2, 64);
+    for (int i = 0; i < P; ++i) {
+      Part& q = parts[i];
+      if (kx > 1)  // deferred x updates still pending at termination
+        UQG_LAUNCH(UQG_K_PCG_DIR, q.s,
+                   launch_pcg_flush(with_groups(geo, q.G), q.G, q.s, N, q.st, vecw(q, x), q.p,
+                                    false));
+      if (i > 0) UQG_LAUNCH(UQG_K_OTHER, q.s, launch_pcg_finalize(q.G, S, q.s, q.st, ens_iters + q.g0));
+    }
+    for (int i = 1; i < P; ++i) {  // the caller's stream waits for every part
+      UQG_TRY_CUDA(cudaEventRecord(ctx->aux_ev[i], parts[i].s));
+      UQG_TRY_CUDA(cudaStreamWaitEvent(s, ctx->aux_ev[i], 0));
+    }
   }
-  if (pblocks == 0 && kx > 1)  // deferred x updates still pending at termination
-    UQG_LAUNCH(UQG_K_PCG_DIR, s, launch_pcg_flush(with_groups(geo, G), G, s, N, st, x, p, false));
-  UQG_LAUNCH(UQG_K_OTHER, s, launch_pcg_finalize(G, S, s, st, ens_iters));
+  UQG_LAUNCH(UQG_K_OTHER, s, launch_pcg_finalize(parts[0].G, S, s, st, ens_iters));
   // breakdown / history bookkeeping
   std::vector<int> h_status(G);
-  cudaError_t e =
-      cudaMemcpyAsync(h_status.data(), st.status, G * sizeof(int), cudaMemcpyDeviceToHost, s);
+  cudaError_t e = cudaSuccess;
+  for (int i = 0; i < P && e == cudaSuccess; ++i)
+    e = cudaMemcpyAsync(h_status.data() + parts[i].g0, parts[i].st.status,
+                        parts[i].G * sizeof(int), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(ctx->pinned + 1, st.overflow, sizeof(int), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
