@@ -47,3 +47,17 @@ def test_byte_model_faces():
     assert bm["operator"] == "fv2d faces"
     assert bm["spmv"] == 8 * S * (256 * 255) + 16 * S * N
     assert bm["pcg_iter"] == 8 * S * (256 * 255 + 13 * N)
+
+
+def test_byte_model_deferred_update():
+    sys.path.insert(0, str(ROOT))
+    import bench
+    from paper_1705_02003_b200.configs import get
+
+    cfg = get("C2")
+    S, N = cfg.ensemble_size, cfg.n_dofs
+    one = bench.bytes_model(cfg, kx=1)
+    four = bench.bytes_model(cfg, kx=4)
+    assert one["dir"] == 48 * S * N and "flush" not in one
+    assert four["dir"] == int(5.5 * 8 * S * N) and four["flush"] == 4
+    assert four["pcg_iter_moved"] < one["pcg_iter_moved"]
