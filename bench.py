@@ -518,6 +518,9 @@ def main():
                      "traffic_algorithmic_same_launch": per[dom]["traffic_algorithmic_same_launch"],
                      "traffic_source": per[dom]["traffic_source"],
                      "peak_source": peak_src,
+                     # also against the 8 TB/s HBM3e specification
+                     "peak_spec": 8000.0,
+                     "frac_spec": (per[dom]["achieved"] / 8000.0) if per[dom]["achieved"] else None,
                      "bytes_per_group_launch": per[dom]["bytes_per_group_launch"],
                      "group_launches": group_iters,
                      "timing": "per-launch CUDA events on the launching stream, profiled pass "
