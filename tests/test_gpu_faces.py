@@ -143,18 +143,21 @@ sys.path.insert(0, sys.argv[1])
 import paper_1705_02003_b200 as uq
 cfg = uq.CONFIGS["C2"]
 f = uq.build_field(**cfg.field_kwargs())
-s = uq.EnsembleSolver2D(f, cfg.cells, cfg.tol, cfg.maxit)
-ys = np.random.default_rng(11).uniform(-1, 1, (21, cfg.ensemble_size, cfg.n_modes))
-r = s.solve_groups(ys)
-np.save(sys.argv[2], np.concatenate([r.iterations.ravel().astype(float), r.qoi.ravel(),
-                                     r.ensemble_iterations.astype(float)]))
+out = []
+for a2 in ("const", "same"):
+    s = uq.EnsembleSolver2D(f, cfg.cells, cfg.tol, cfg.maxit, a2=a2)
+    ys = np.random.default_rng(11).uniform(-1, 1, (21, cfg.ensemble_size, cfg.n_modes))
+    r = s.solve_groups(ys)
+    out.append(np.concatenate([r.iterations.ravel().astype(float), r.qoi.ravel(),
+                               r.ensemble_iterations.astype(float)]))
+np.save(sys.argv[2], np.concatenate(out))
 """
 
 
 def test_concurrent_parts_bitwise(tmp_path):
     """A level solved as 1, 2 or 3 concurrent parts on separate streams
-    (UQG_SOLVE_STREAMS; C2 size, 21 groups: > 1 GB per part and iteration)
-    gives identical results."""
+    (UQG_SOLVE_STREAMS; C2 size, 21 groups: > 1 GB per part and iteration;
+    constant and random y-faces) gives identical results."""
     outs = {}
     for k in ("1", "2", "3"):
         env = dict(os.environ, UQG_SOLVE_STREAMS=k)
