@@ -164,7 +164,11 @@ int uqg_lane_dot(uqg_ctx* ctx, int N, int S, int G, const double* a, const doubl
  *   hist_host: NULL, or host buffer [(hist_cap+1)][G][S] receiving the lane
  *   residual norms per iteration (row 0 = ||b||); *hist_rows_host = rows used.
  * Runs the whole loop on the device; the host only polls a done-counter.
- * max_row_len as for uqg_spmv.
+ * Small batches run as one persistent launch (cluster barriers); large ones
+ * as a launch loop, split into up to UQG_SOLVE_STREAMS concurrent parts on
+ * context-owned streams that start after, and are joined back into,
+ * `stream` - the call stays stream-ordered and results do not depend on the
+ * split.  max_row_len as for uqg_spmv.
  * Returns UQG_EBREAKDOWN on a non-finite residual in an active lane. */
 int uqg_pcg(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const int* row_offsets,
             const int* col_indices, const double* vals, const double* rhs, double rhs_const,
