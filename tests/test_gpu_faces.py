@@ -166,3 +166,40 @@ def test_concurrent_parts_bitwise(tmp_path):
                        check=True)
         outs[k] = np.load(dst)
     assert np.array_equal(outs["2"], outs["1"]) and np.array_equal(outs["3"], outs["1"])
+
+
+_MAXIT_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1705_02003_b200 as uq
+cfg = uq.CONFIGS["C1"]
+f = uq.build_field(**cfg.field_kwargs())
+out = []
+for faces in (False, True):
+    s = uq.EnsembleSolver2D(f, cfg.cells, cfg.tol, 37, faces=faces)   # maxit 37: 1 mod 4
+    ys = np.random.default_rng(2).uniform(-1, 1, (5, cfg.ensemble_size, cfg.n_modes))
+    r = s.solve_groups(ys)
+    out.append(np.concatenate([r.iterations.ravel().astype(float), r.qoi.ravel(),
+                               r.converged.ravel().astype(float)]))
+np.save(sys.argv[2], np.array(out))
+"""
+
+
+def test_maxit_termination_with_deferred_update(tmp_path):
+    """Groups stopped by maxit (unconverged lanes report the iterations run)
+    with a pending deferred-update tail: identical for kx = 1 and 4, CSR and
+    face operator, launch loop and persistent kernel."""
+    outs = {}
+    for tag, env_extra in (("loop1", {"UQG_PCG_PERSISTENT": "0", "UQG_X_DEFER": "1"}),
+                           ("loop4", {"UQG_PCG_PERSISTENT": "0", "UQG_X_DEFER": "4"}),
+                           ("persistent", {})):
+        dst = tmp_path / f"{tag}.npy"
+        subprocess.run([sys.executable, "-c", _MAXIT_SCRIPT, str(ROOT), str(dst)],
+                       env=dict(os.environ, **env_extra), check=True)
+        outs[tag] = np.load(dst)
+    ref = outs["loop1"]
+    n = ref.shape[1] // 3
+    assert (ref[0][:n] == 37).any() and not ref[0][2 * n:].all()  # some lanes hit maxit
+    for tag in ("loop4", "persistent"):
+        assert np.array_equal(outs[tag], ref), tag
+    assert np.array_equal(ref[0], ref[1])  # CSR == faces
