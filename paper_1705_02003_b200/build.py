@@ -52,7 +52,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             if not force and not needs_build():  # built by another process meanwhile
                 return LIB
             tmp = f"{LIB}.tmp.{os.getpid()}"
-            cmd = [_nvcc(), *NVCC_FLAGS, "-I", str(PKG.parent / "include"), "-o", tmp,
+            extra = os.environ.get("UQG_NVCC_EXTRA", "").split()  # tuning experiments
+            cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-I", str(PKG.parent / "include"), "-o", tmp,
                    *[str(CSRC / s) for s in SOURCES]]
             res = subprocess.run(cmd, capture_output=True, text=True)
             if verbose or res.returncode:

@@ -324,6 +324,9 @@ struct FaceRow {
 
 // Chunks are reduced in batches of up to kFaceBatch (reduce_lanes_batch: one
 // tree and one ticket per batch, same bits as per-chunk reduce_lanes).
+#ifndef UQG_FACE_MINB
+#define UQG_FACE_MINB 4
+#endif
 constexpr int kFaceBatch = 8;
 static_assert(kFaceBatch <= kMaxBatch, "batch exceeds reduce_lanes_batch's limit");
 
@@ -388,7 +391,7 @@ __device__ __forceinline__ void face_spmv_body(long long N, const Geo& geo, cons
 }
 
 template <int V>
-__global__ void __launch_bounds__(256, 4) pcg_spmv_fv2d_kernel(
+__global__ void __launch_bounds__(256, UQG_FACE_MINB) pcg_spmv_fv2d_kernel(
     long long N, Geo geo, PcgState st, Fv2dOp op, const double* __restrict__ p,
     double* __restrict__ ap) {
   face_spmv_body<V>(N, geo, st, op, p, ap);
