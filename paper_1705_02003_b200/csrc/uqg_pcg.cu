@@ -429,11 +429,14 @@ __global__ void __launch_bounds__(256) spmv_fv2d_kernel(long long N, Geo geo, Fv
 }
 
 // chunks per batched reduction in pcg_update (reduce_lanes_batch)
+#ifndef UQG_UPDATE_MINB
+#define UQG_UPDATE_MINB 3
+#endif
 constexpr int kUpdateBatch = 4;
 static_assert(kUpdateBatch <= kMaxBatch, "batch exceeds reduce_lanes_batch's limit");
 
 template <int V>
-__global__ void __launch_bounds__(256, 3) pcg_update_kernel(long long N, Geo geo, PcgState st,
+__global__ void __launch_bounds__(256, UQG_UPDATE_MINB) pcg_update_kernel(long long N, Geo geo, PcgState st,
                                                          const double* __restrict__ dinv,
                                                          int maxit, double* __restrict__ r,
                                                          const double* __restrict__ ap) {
