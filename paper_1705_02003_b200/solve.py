@@ -364,6 +364,8 @@ class EnsembleSolver:
     def solve_plan(self, plan, coords_by_id, residual_sink=None):
         """Drop-in for ``_PdeProblem.solve_plan`` (``harness.py:399-431``)."""
         groups = plan.ensembles
+        if not groups:  # the reference's loop over no ensembles
+            return {}, {}, []
         samples = np.array([[coords_by_id[sid] for sid in grp] for grp in groups], dtype=np.float64)
         res = self.solve_groups(samples, record_history=residual_sink is not None)
         return self.collect(plan, res, residual_sink)

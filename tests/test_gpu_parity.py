@@ -436,3 +436,16 @@ def test_tma_staged_spmv_bitwise_equals_register_path(tmp_path, lanes):
     # face-form FV2D operator
     for k in ("11", "10", "41", "61", "71", "FF"):
         assert np.array_equal(out[k], out["00"]), k
+
+
+def test_empty_plan_and_level():
+    """Edge cases as the reference handles them: an empty plan solves nothing
+    (harness.py:409 loops over no ensembles); an empty level cannot be grouped
+    (grouping.py:100-101, 115-116)."""
+    from paper_1705_02003_b200.grouping import GroupingPlan
+    cfg = uq.CONFIGS["C1"]
+    solver = uq.EnsembleSolver2D(uq.build_field(**cfg.field_kwargs()), cfg.cells, cfg.tol,
+                                 cfg.maxit)
+    assert solver.solve_plan(GroupingPlan(1, 4, (), (), "sur"), {}) == ({}, {}, [])
+    with pytest.raises(uq.GroupingError):
+        solver.solve_level([], np.zeros((0, cfg.n_modes)), 4)
