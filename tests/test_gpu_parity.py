@@ -449,3 +449,13 @@ def test_empty_plan_and_level():
     assert solver.solve_plan(GroupingPlan(1, 4, (), (), "sur"), {}) == ({}, {}, [])
     with pytest.raises(uq.GroupingError):
         solver.solve_level([], np.zeros((0, cfg.n_modes)), 4)
+
+
+def test_lane_limit_raises_cleanly():
+    """S > 512 lanes (kMaxLanes: one tile row per 256-thread block at most) is
+    rejected with EnsembleError instead of launching."""
+    d = np.ones((513, 3))
+    with pytest.raises(uq.EnsembleError):
+        uq.ensemble_pcg(diag_ensemble(d), np.ones((513, 3)))
+    r = uq.ensemble_pcg(diag_ensemble(np.ones((512, 3))), np.ones((512, 3)))
+    assert r.converged_per_lane.all()
