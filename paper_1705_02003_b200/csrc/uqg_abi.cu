@@ -43,6 +43,10 @@ struct uqg_ctx {
   std::vector<cudaStream_t> aux;
   std::vector<cudaEvent_t> aux_ev;
   int* pinned_parts = nullptr;
+  // graph launch loop (pcg_impl): capture stream, device pass counter, pinned readback
+  cudaStream_t cap = nullptr;
+  int* loops_dev = nullptr;
+  int* loops_host = nullptr;
 };
 
 namespace {
@@ -180,6 +184,16 @@ int solve_streams() {  // read per solve: bench.py times kernels with one stream
   return v < 1 ? 1 : (v > kMaxParts ? kMaxParts : v);
 }
 
+// UQG_PCG_GRAPH: run the launch loop of a single-part solve as ONE CUDA graph
+// launch - a while-conditional node repeating kx iterations, the condition
+// cleared on the device once every group is DONE - instead of host-polled
+// launch chunks (1 = on; read per solve).  Not used while profiling (per-launch
+// events cannot be recorded inside a graph).
+int graph_mode() {
+  const char* e = getenv("UQG_PCG_GRAPH");
+  return e ? atoi(e) : 0;
+}
+
 size_t pcg_layout(Carver& c, long long N, const Geo& geo, int G, PcgState* st, double** r,
                   double** p, double** ap, int kx = x_defer()) {
   const size_t vec = (size_t)G * N * geo.S;
@@ -254,6 +268,9 @@ int uqg_ctx_destroy(uqg_ctx* ctx) {
   for (cudaStream_t a : ctx->aux) cudaStreamDestroy(a);
   for (cudaEvent_t e : ctx->aux_ev) cudaEventDestroy(e);
   if (ctx->pinned_parts) cudaFreeHost(ctx->pinned_parts);
+  if (ctx->cap) cudaStreamDestroy(ctx->cap);
+  if (ctx->loops_dev) cudaFree(ctx->loops_dev);
+  if (ctx->loops_host) cudaFreeHost(ctx->loops_host);
   delete ctx;
   return UQG_OK;
 }
@@ -685,6 +702,90 @@ int pcg_impl(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const 
       set_error("uqg_pcg: persistent solve aborted (group barrier timeout)");
       return UQG_ECUDA;
     }
+  } else if (P == 1 && !ctx->prof && graph_mode() > 0) {
+    // Graph launch loop: the same kernels and per-iteration order as the
+    // host-polled loop below, blocks sized for all G groups (finished groups'
+    // blocks exit at once; results do not depend on the block count).
+    UQG_LAUNCH(UQG_K_PCG_INIT, s,
+               launch_pcg_init(geo, G, s, N, st, rhs, rhs_const, dinv, tol, maxit, x, r, p));
+    if (!ctx->cap) {
+      UQG_TRY_CUDA(cudaStreamCreateWithFlags(&ctx->cap, cudaStreamNonBlocking));
+      UQG_TRY_CUDA(cudaMalloc(&ctx->loops_dev, sizeof(int)));
+      UQG_TRY_CUDA(cudaHostAlloc(&ctx->loops_host, 2 * sizeof(int), cudaHostAllocDefault));
+    }
+    UQG_TRY_CUDA(cudaMemsetAsync(ctx->loops_dev, 0, sizeof(int), s));
+    const Geo gl = with_groups(geo, G);
+    const int max_loops = (maxit + 2) / kx + 2;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphConditionalHandle hc;
+    UQG_TRY_CUDA(cudaGraphCreate(&graph, 0));
+    cudaError_t ge = cudaGraphConditionalHandleCreate(&hc, graph, 1, cudaGraphCondAssignDefault);
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = hc;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    if (ge == cudaSuccess) ge = cudaGraphAddNode(&node, graph, nullptr, 0, &cp);
+    if (ge == cudaSuccess)
+      ge = cudaStreamBeginCaptureToGraph(ctx->cap, cp.conditional.phGraph_out[0], nullptr, nullptr,
+                                         0, cudaStreamCaptureModeRelaxed);
+    int brc = UQG_OK;
+    long long per_pass = 0;
+    if (ge == cudaSuccess) {
+      const long long before = ctx->launches;
+      cudaStream_t cs = ctx->cap;
+      brc = [&]() -> int {  // the body: iterations k = 0..kx-1 of a window
+        for (int k = 0; k < kx; ++k) {
+          if (op.fv.tx)
+            UQG_LAUNCH(UQG_K_PCG_SPMV, cs, launch_pcg_spmv_fv2d(gl, G, cs, N, st, op.fv, p, ap));
+          else
+            UQG_LAUNCH(UQG_K_PCG_SPMV, cs,
+                       launch_pcg_spmv(gl, G, cs, N, nnz, st, op.ro, op.ci, op.vals, p, ap,
+                                       ctx->bands.nb ? &ctx->bands : nullptr));
+          UQG_LAUNCH(UQG_K_PCG_UPDATE, cs, launch_pcg_update(gl, G, cs, N, st, dinv, maxit, r, ap));
+          if (kx > 1 && k == kx - 1)
+            UQG_LAUNCH(UQG_K_PCG_DIR, cs, launch_pcg_flush(gl, G, cs, N, st, x, p, true));
+          UQG_LAUNCH(UQG_K_PCG_DIR, cs, launch_pcg_dir(gl, G, cs, N, st, dinv, r, x, p));
+        }
+        UQG_LAUNCH(UQG_K_OTHER, cs,
+                   launch_pcg_loop_cond(cs, hc, st.ndone, G, ctx->loops_dev, max_loops));
+        return UQG_OK;
+      }();
+      cudaGraph_t body = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(ctx->cap, &body);
+      if (ge == cudaSuccess) ge = ce;
+      per_pass = ctx->launches - before;
+    }
+    if (ge == cudaSuccess && brc == UQG_OK) ge = cudaGraphInstantiate(&exec, graph, 0);
+    if (ge == cudaSuccess && brc == UQG_OK) ge = cudaGraphLaunch(exec, s);
+    if (exec) cudaGraphExecDestroy(exec);  // freed once the launch completes
+    cudaGraphDestroy(graph);
+    if (brc) return brc;
+    if (ge != cudaSuccess) {
+      cudaGetLastError();
+      set_error(std::string("uqg_pcg graph loop: ") + cudaGetErrorString(ge));
+      return UQG_ECUDA;
+    }
+    if (kx > 1)  // deferred x updates still pending at termination
+      UQG_LAUNCH(UQG_K_PCG_DIR, s, launch_pcg_flush(gl, G, s, N, st, x, p, false));
+    UQG_TRY_CUDA(cudaMemcpyAsync(ctx->loops_host, ctx->loops_dev, sizeof(int),
+                                 cudaMemcpyDeviceToHost, s));
+    UQG_TRY_CUDA(cudaMemcpyAsync(ctx->loops_host + 1, st.ndone, sizeof(int),
+                                 cudaMemcpyDeviceToHost, s));
+    UQG_TRY_CUDA(cudaStreamSynchronize(s));
+    const int passes = ctx->loops_host[0];
+    if (ctx->loops_host[1] < G) {
+      set_error("uqg_pcg: device loop failed to terminate");
+      return UQG_ECUDA;
+    }
+    // launch accounting: the body was counted once at capture
+    ctx->launches += per_pass * (passes - 1);
+    ctx->kind_launches[UQG_K_PCG_SPMV] += (long long)kx * (passes - 1);
+    ctx->kind_launches[UQG_K_PCG_UPDATE] += (long long)kx * (passes - 1);
+    ctx->kind_launches[UQG_K_PCG_DIR] += (long long)(kx + (kx > 1)) * (passes - 1);
+    ctx->kind_launches[UQG_K_OTHER] += passes - 1;
   } else {
     // Launch loop: the host polls each part's device done-counter between
     // chunks of iterations and launches the next chunk for every part still

@@ -177,6 +177,11 @@ void launch_pcg_flush(const Geo& geo, int G, cudaStream_t s, long long N, const 
 void launch_pcg_dir(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,
                     const double* dinv, const double* r, double* x, double* p);
 void launch_pcg_finalize(int G, int S, cudaStream_t s, const PcgState& st, int* ens_iters);
+// While-condition of the graph launch loop: one more pass of the body unless
+// every group is DONE (ndone >= G) or the pass cap is reached (*loops counts
+// the passes; the host turns a capped loop into an error).
+void launch_pcg_loop_cond(cudaStream_t s, cudaGraphConditionalHandle h, const int* ndone, int G,
+                          int* loops, int max_loops);
 
 // uqg_surrogate.cu: grouping keys on the device
 void launch_surrogate_eval(cudaStream_t s, const double* points, int n, int dim,

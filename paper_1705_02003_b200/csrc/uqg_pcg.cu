@@ -1459,6 +1459,17 @@ void launch_pcg_dir(const Geo& geo, int G, cudaStream_t s, long long N, const Pc
   UQG_DISPATCH_V(gl, pcg_dir_kernel, dim3(gl.B, G), 0, s, N, gl, st, dinv, r, x, p);
 }
 
+__global__ void pcg_loop_cond_kernel(cudaGraphConditionalHandle h, const int* ndone, int G,
+                                     int* loops, int max_loops) {
+  const int l = ++*loops;
+  if (*ndone >= G || l >= max_loops) cudaGraphSetConditional(h, 0);
+}
+
+void launch_pcg_loop_cond(cudaStream_t s, cudaGraphConditionalHandle h, const int* ndone, int G,
+                          int* loops, int max_loops) {
+  pcg_loop_cond_kernel<<<1, 1, 0, s>>>(h, ndone, G, loops, max_loops);
+}
+
 void launch_pcg_finalize(int G, int S, cudaStream_t s, const PcgState& st, int* ens_iters) {
   pcg_finalize_kernel<<<(G + 127) / 128, 128, 0, s>>>(st, G, S, ens_iters);
 }

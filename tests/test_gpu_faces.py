@@ -88,6 +88,7 @@ _VARIANTS = {  # face SpMV variants (all must give the CSR bits)
     "tma2": {"UQG_FACE_TMA": "2"},                        # TMA-banded
     "tma4": {"UQG_FACE_TMA": "4"},
     "fixed": {"UQG_OCC_BLOCKS": "0"},                     # with_groups block sizing
+    "graph": {"UQG_PCG_GRAPH": "1"},                      # launch loop as one graph launch
 }
 
 
@@ -113,13 +114,15 @@ def test_deferred_x_update_bitwise(tmp_path):
     update: every kx gives the bits of kx = 1, CSR and face operator, launch loop."""
     outs = {}
     for kx in ("1", "2", "3", "4"):
-        env = dict(os.environ, UQG_PCG_PERSISTENT="0", UQG_X_DEFER=kx)
-        dst = tmp_path / f"x{kx}.npy"
-        subprocess.run([sys.executable, "-c", _SCRIPT, str(ROOT), str(dst)], env=env, check=True)
-        outs[kx] = np.load(dst, allow_pickle=True)
-    for kx in ("2", "3", "4"):
-        for a, b in zip(outs[kx], outs["1"]):
-            assert np.array_equal(a, b), kx
+        for graph in ("0", "1"):  # host-polled / graph launch loop
+            env = dict(os.environ, UQG_PCG_PERSISTENT="0", UQG_X_DEFER=kx, UQG_PCG_GRAPH=graph)
+            dst = tmp_path / f"x{kx}{graph}.npy"
+            subprocess.run([sys.executable, "-c", _SCRIPT, str(ROOT), str(dst)], env=env,
+                           check=True)
+            outs[kx + graph] = np.load(dst, allow_pickle=True)
+    for key in outs:
+        for a, b in zip(outs[key], outs["10"]):
+            assert np.array_equal(a, b), key
 
 
 @pytest.mark.parametrize("S", [6, 64, 130, 512])
@@ -192,6 +195,8 @@ def test_maxit_termination_with_deferred_update(tmp_path):
     outs = {}
     for tag, env_extra in (("loop1", {"UQG_PCG_PERSISTENT": "0", "UQG_X_DEFER": "1"}),
                            ("loop4", {"UQG_PCG_PERSISTENT": "0", "UQG_X_DEFER": "4"}),
+                           ("graph4", {"UQG_PCG_PERSISTENT": "0", "UQG_X_DEFER": "4",
+                                       "UQG_PCG_GRAPH": "1"}),
                            ("persistent", {})):
         dst = tmp_path / f"{tag}.npy"
         subprocess.run([sys.executable, "-c", _MAXIT_SCRIPT, str(ROOT), str(dst)],
@@ -200,6 +205,6 @@ def test_maxit_termination_with_deferred_update(tmp_path):
     ref = outs["loop1"]
     n = ref.shape[1] // 3
     assert (ref[0][:n] == 37).any() and not ref[0][2 * n:].all()  # some lanes hit maxit
-    for tag in ("loop4", "persistent"):
+    for tag in ("loop4", "graph4", "persistent"):
         assert np.array_equal(outs[tag], ref), tag
     assert np.array_equal(ref[0], ref[1])  # CSR == faces

@@ -42,8 +42,9 @@ np.save(sys.argv[2], np.concatenate(out))
 
 def test_persistent_bitwise_equals_launch_loop(tmp_path):
     got = {}
-    for mode in ("2", "1", "0"):  # cluster barriers, cooperative barriers, launch loop
-        env = dict(os.environ, UQG_PCG_PERSISTENT=mode)
+    # cluster barriers, cooperative barriers, host-polled launch loop, graph launch loop
+    for mode in ("2", "1", "0", "0g"):
+        env = dict(os.environ, UQG_PCG_PERSISTENT=mode[0], UQG_PCG_GRAPH=str(int(mode == "0g")))
         dst = tmp_path / f"p{mode}.npy"
         subprocess.run([sys.executable, "-c", _SCRIPT, str(ROOT), str(dst)], env=env, check=True,
                        timeout=600)
@@ -51,20 +52,23 @@ def test_persistent_bitwise_equals_launch_loop(tmp_path):
     assert got["1"].shape == got["0"].shape
     assert np.array_equal(got["1"], got["0"])
     assert np.array_equal(got["2"], got["0"])
+    assert np.array_equal(got["0g"], got["0"])
 
 
-def test_reference_semantics_through_the_launch_loop():
+@pytest.mark.parametrize("graph", ["0", "1"])
+def test_reference_semantics_through_the_launch_loop(graph):
     """The PCG semantics tests (reference goldens, trivial systems, frozen and
     breakdown lanes, acceptance criterion 1) re-run with the small systems
-    forced through the launch loop - deferred solution update included - instead
-    of the persistent kernel they take by default."""
+    forced through the launch loop - deferred solution update included, host-
+    polled or as one graph launch - instead of the persistent kernel they take
+    by default."""
     import os
     import subprocess
     import sys
     from pathlib import Path
 
     root = Path(__file__).resolve().parents[1]
-    env = dict(os.environ, UQG_PCG_PERSISTENT="0", UQG_X_DEFER="4")
+    env = dict(os.environ, UQG_PCG_PERSISTENT="0", UQG_X_DEFER="4", UQG_PCG_GRAPH=graph)
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
                         str(root / "tests" / "test_gpu_parity.py"), "-k",
                         "pcg_matches_reference_golden or trivial_systems or subnormal or "
