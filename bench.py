@@ -480,6 +480,22 @@ def main():
                     "traffic": tr.get("dram_bytes_per_launch"),
                     "traffic_algorithmic_same_launch": tr.get("algorithmic_bytes_per_launch"),
                     "traffic_source": tr.get("source")}
+    if cnt[3] and not cnt[4] and not cnt[5]:
+        # small batches: the whole solve is ONE persistent launch (cluster or
+        # cooperative kernel; SpMV, update and direction as phases of each
+        # iteration, x updated in place) - its roofline is the loop's
+        bm1 = bytes_model(cfg, solver.op, 1)
+        b_it = bm1["spmv"] + bm1["update"] + bm1["dir"]
+        gbs = group_iters * b_it / (ms[3] / 1e3) / 1e9 if ms[3] else None
+        tr = traffic_all.get(f"{cfg.name}:pcg_persistent_kernel", {})
+        per = {"persistent": {
+            "kernel": "pcg_persistent_kernel (whole solve; per group-iteration: SpMV + update "
+                      "+ direction phases)",
+            "ms": ms[3], "achieved": gbs, "frac": gbs / peak if gbs else None,
+            "bytes_per_group_launch": b_it,
+            "traffic": tr.get("dram_bytes_per_launch"),
+            "traffic_algorithmic_same_launch": tr.get("algorithmic_bytes_per_launch"),
+            "traffic_source": tr.get("source")}}
     dom = max(per, key=lambda k: per[k]["ms"] or 0.0)
     loop_ms = ms[3] + ms[4] + ms[5]
     loop_gbs = group_iters * bm["pcg_iter"] / (loop_ms / 1e3) / 1e9 if loop_ms else None
