@@ -208,3 +208,37 @@ def test_maxit_termination_with_deferred_update(tmp_path):
     for tag in ("loop4", "graph4", "persistent"):
         assert np.array_equal(outs[tag], ref), tag
     assert np.array_equal(ref[0], ref[1])  # CSR == faces
+
+
+@pytest.mark.parametrize("cells,S", [(2, 1), (3, 3), (7, 5), (17, 1), (33, 2)])
+@pytest.mark.parametrize("maxit", [0, 1, 3000])
+def test_small_and_odd_meshes_match_oracle(cells, S, maxit):
+    """Edge shapes through the default (face-form) level solve: one-cell and
+    few-cell meshes, single-lane and odd ensembles, a padded last group, and
+    maxit 0 / 1 (unconverged lanes) - iterations and notes equal to the oracle's
+    solve_plan, QoIs within 1e-8, and bit-identical to the CSR path."""
+    sys.path.insert(0, str(ROOT))
+    from oracle import driver as odriver, field2d, fv2d as ofv
+
+    cfg = uq.CONFIGS["C1"]
+    f = uq.build_field(**cfg.field_kwargs())
+    o = field2d.KL2D.select(**cfg.field_kwargs())
+    omesh = ofv.Mesh2D(cells)
+    rng = np.random.default_rng(cells * 100 + S)
+    ids = list(range(2 * S + 1))
+    coords = {i: rng.uniform(-1, 1, cfg.n_modes) for i in ids}
+    plan = uq.group_natural(ids, S, level=1)
+    got = {}
+    for faces in (True, False):
+        solver = uq.EnsembleSolver2D(f, cells, cfg.tol, maxit, faces=faces)
+        got[faces] = solver.solve_plan(plan, coords)
+    it_d, q_d, notes_d = got[True]
+    it_o, q_o, notes_o = odriver.solve_plan(omesh, o, o.mode_table(omesh.node_points),
+                                            plan.ensembles, coords, cfg.tol, maxit, level=1)
+    assert it_d == it_o and notes_d == notes_o
+    if maxit == 0:
+        assert notes_o and all(v == 0 for v in it_o.values())
+    for i in ids:
+        assert abs(q_d[i] - q_o[i]) <= 1e-8 * abs(q_o[i])
+    assert got[False][0] == it_d and got[False][2] == notes_d
+    assert all(got[False][1][i] == q_d[i] for i in ids)
