@@ -327,7 +327,10 @@ struct FaceRow {
 #ifndef UQG_FACE_MINB
 #define UQG_FACE_MINB 4
 #endif
-constexpr int kFaceBatch = 8;
+#ifndef UQG_FACE_BATCH
+#define UQG_FACE_BATCH 8
+#endif
+constexpr int kFaceBatch = UQG_FACE_BATCH;
 static_assert(kFaceBatch <= kMaxBatch, "batch exceeds reduce_lanes_batch's limit");
 
 template <int V>
