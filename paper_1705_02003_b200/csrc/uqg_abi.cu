@@ -676,6 +676,23 @@ int pcg_impl(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const 
     UQG_TRY_CUDA(cudaMemsetAsync(q.st.ndone, 0, sizeof(int), q.s));
     UQG_TRY_CUDA(cudaMemsetAsync(q.st.overflow, 0, sizeof(int), q.s));
   }
+  // One PCG iteration of part q on stream qs, blocks per group from gl; flush:
+  // the iteration closes a deferral window (pcg_flush before pcg_dir).
+  auto launch_iteration = [&](const Part& q, const Geo& gl, cudaStream_t qs, bool flush) -> int {
+    double* xq = x + (size_t)q.g0 * vs;
+    const double* dq = dinv ? dinv + (size_t)q.g0 * vs : nullptr;
+    if (q.op.fv.tx)
+      UQG_LAUNCH(UQG_K_PCG_SPMV, qs,
+                 launch_pcg_spmv_fv2d(gl, q.G, qs, N, q.st, q.op.fv, q.p, q.ap));
+    else
+      UQG_LAUNCH(UQG_K_PCG_SPMV, qs,
+                 launch_pcg_spmv(gl, q.G, qs, N, nnz, q.st, q.op.ro, q.op.ci, q.op.vals, q.p,
+                                 q.ap, ctx->bands.nb ? &ctx->bands : nullptr));
+    UQG_LAUNCH(UQG_K_PCG_UPDATE, qs, launch_pcg_update(gl, q.G, qs, N, q.st, dq, maxit, q.r, q.ap));
+    if (flush) UQG_LAUNCH(UQG_K_PCG_DIR, qs, launch_pcg_flush(gl, q.G, qs, N, q.st, xq, q.p, true));
+    UQG_LAUNCH(UQG_K_PCG_DIR, qs, launch_pcg_dir(gl, q.G, qs, N, q.st, dq, q.r, xq, q.p));
+    return UQG_OK;
+  };
   PcgState& st = parts[0].st;  // single-part view (persistent path, history, status)
   st.hist = hist_host ? c.take<double>(hist_elems) : nullptr;
   double *r = parts[0].r, *p = parts[0].p, *ap = parts[0].ap;
@@ -738,16 +755,8 @@ int pcg_impl(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const 
       cudaStream_t cs = ctx->cap;
       brc = [&]() -> int {  // the body: iterations k = 0..kx-1 of a window
         for (int k = 0; k < kx; ++k) {
-          if (op.fv.tx)
-            UQG_LAUNCH(UQG_K_PCG_SPMV, cs, launch_pcg_spmv_fv2d(gl, G, cs, N, st, op.fv, p, ap));
-          else
-            UQG_LAUNCH(UQG_K_PCG_SPMV, cs,
-                       launch_pcg_spmv(gl, G, cs, N, nnz, st, op.ro, op.ci, op.vals, p, ap,
-                                       ctx->bands.nb ? &ctx->bands : nullptr));
-          UQG_LAUNCH(UQG_K_PCG_UPDATE, cs, launch_pcg_update(gl, G, cs, N, st, dinv, maxit, r, ap));
-          if (kx > 1 && k == kx - 1)
-            UQG_LAUNCH(UQG_K_PCG_DIR, cs, launch_pcg_flush(gl, G, cs, N, st, x, p, true));
-          UQG_LAUNCH(UQG_K_PCG_DIR, cs, launch_pcg_dir(gl, G, cs, N, st, dinv, r, x, p));
+          const int rc = launch_iteration(parts[0], gl, cs, kx > 1 && k == kx - 1);
+          if (rc) return rc;
         }
         UQG_LAUNCH(UQG_K_OTHER, cs,
                    launch_pcg_loop_cond(cs, hc, st.ndone, G, ctx->loops_dev, max_loops));
@@ -830,23 +839,11 @@ int pcg_impl(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const 
       for (int i = 0; i < P; ++i) gact[i] = with_groups(geo, std::max(1, parts[i].G - pin[i]));
       for (int k = 0; k < chunk; ++k) {
         for (int i = 0; i < P; ++i) {
-          Part& q = parts[i];
-          if (q.done) continue;
-          const Geo& gl = gact[i];
-          double* xq = vecw(q, x);
-          const double* dq = vec(q, dinv);
-          if (q.op.fv.tx)
-            UQG_LAUNCH(UQG_K_PCG_SPMV, q.s,
-                       launch_pcg_spmv_fv2d(gl, q.G, q.s, N, q.st, q.op.fv, q.p, q.ap));
-          else
-            UQG_LAUNCH(UQG_K_PCG_SPMV, q.s,
-                       launch_pcg_spmv(gl, q.G, q.s, N, nnz, q.st, q.op.ro, q.op.ci, q.op.vals,
-                                       q.p, q.ap, ctx->bands.nb ? &ctx->bands : nullptr));
-          UQG_LAUNCH(UQG_K_PCG_UPDATE, q.s,
-                     launch_pcg_update(gl, q.G, q.s, N, q.st, dq, maxit, q.r, q.ap));
-          if (kx > 1 && (launched + k + 1) % kx == 0)  // iteration launched + k closes a window
-            UQG_LAUNCH(UQG_K_PCG_DIR, q.s, launch_pcg_flush(gl, q.G, q.s, N, q.st, xq, q.p, true));
-          UQG_LAUNCH(UQG_K_PCG_DIR, q.s, launch_pcg_dir(gl, q.G, q.s, N, q.st, dq, q.r, xq, q.p));
+          if (parts[i].done) continue;
+          // iteration launched + k closes a deferral window: flush before pcg_dir
+          const int rc = launch_iteration(parts[i], gact[i], parts[i].s,
+                                          kx > 1 && (launched + k + 1) % kx == 0);
+          if (rc) return rc;
         }
       }
       launched += chunk;

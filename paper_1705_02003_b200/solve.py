@@ -18,6 +18,7 @@ first-occurrence rule for replica slots (``harness.py:427-430``) and the
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 from dataclasses import dataclass, field as dc_field
@@ -187,7 +188,11 @@ class EnsembleSolver:
             self._bufs[name] = t
         return t[:n]
 
+    @contextlib.contextmanager
     def _workspace(self, G, S):
+        """The solver's PCG workspace, registered with the library context for
+        one wave only: the context never keeps the address of a tensor that a
+        dropped solver would hand back to torch's allocator for reuse."""
         torch = _lib._torch()
         m = self.op
         need = int(_lib.load().uqg_pcg_workspace_bytes(m.n_dofs, m.nnz, S, G)) + (1 << 20)
@@ -195,6 +200,10 @@ class EnsembleSolver:
             self._ws = None
             self._ws = torch.empty((need,), dtype=torch.uint8, device=_lib.device())
         _lib.call("uqg_ctx_set_workspace", _lib.ctx(), _lib.ptr(self._ws), self._ws.numel())
+        try:
+            yield
+        finally:
+            _lib.call("uqg_ctx_set_workspace", _lib.ctx(), None, 0)
 
     def release(self):
         self._bufs.clear()
@@ -220,15 +229,14 @@ class EnsembleSolver:
             tx = self._buf("vals", G * F * S, torch.float64)
             ty = self._buf("ty", G * F * S, torch.float64) if o.a2 == "same" else None
             o.assemble_faces(a, G, S, tx, ty, dinv)
-            self._workspace(G, S)
-            x, iters, conv, frz, ens, hist = run_pcg_fv2d(
-                o.mesh.cells, S, G, tx, ty, o.field.a_y, None, o.rhs_const, dinv, self.tol,
-                self.maxit, record_history)
-            return self._finish(x, iters, conv, frz, ens, hist, G, S)
+            with self._workspace(G, S):
+                x, iters, conv, frz, ens, hist = run_pcg_fv2d(
+                    o.mesh.cells, S, G, tx, ty, o.field.a_y, None, o.rhs_const, dinv, self.tol,
+                    self.maxit, record_history)
+                return self._finish(x, iters, conv, frz, ens, hist, G, S)
         vals = self._buf("vals", G * o.nnz * S, torch.float64)
         o.assemble(a, G, S, vals, dinv)
         rowptr, col = o.graph()
-        self._workspace(G, S)
         # banded-graph hint: the SpMV bulk-prefetches each tile's p bands into L2
         # (UQG_SPMV_TMA=3 stages them in shared memory instead); UQG_BAND_HINT=0
         # disables it.  Results are identical either way.
@@ -240,13 +248,14 @@ class EnsembleSolver:
                       (ctypes.c_int * len(starts))(*starts), (ctypes.c_int * len(extras))(*extras),
                       1)
         try:
-            x, iters, conv, frz, ens, hist = run_pcg(
-                o.n_dofs, o.nnz, S, G, rowptr, col, vals, None, o.rhs_const, dinv, self.tol,
-                self.maxit, record_history, max_row_len=o.max_row_len)
+            with self._workspace(G, S):
+                x, iters, conv, frz, ens, hist = run_pcg(
+                    o.n_dofs, o.nnz, S, G, rowptr, col, vals, None, o.rhs_const, dinv, self.tol,
+                    self.maxit, record_history, max_row_len=o.max_row_len)
+                return self._finish(x, iters, conv, frz, ens, hist, G, S)
         finally:
             if hint:
                 _lib.call("uqg_ctx_set_band_hint", _lib.ctx(), 0, None, None, 0)
-        return self._finish(x, iters, conv, frz, ens, hist, G, S)
 
     def _finish(self, x, iters, conv, frz, ens, hist, G, S):
         torch = _lib._torch()

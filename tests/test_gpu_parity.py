@@ -459,3 +459,28 @@ def test_lane_limit_raises_cleanly():
         uq.ensemble_pcg(diag_ensemble(d), np.ones((513, 3)))
     r = uq.ensemble_pcg(diag_ensemble(np.ones((512, 3))), np.ones((512, 3)))
     assert r.converged_per_lane.all()
+
+
+def test_dropped_solver_leaves_no_workspace_behind():
+    """A solver's workspace is registered with the library context only while
+    its wave runs: after the solver is dropped and torch reuses that memory,
+    other library calls (here the drop-in lane_dot) must not carve scratch out
+    of it (regression: an intermittent lane_dot mismatch)."""
+    import gc
+
+    import torch
+
+    cfg = uq.CONFIGS["C1"]
+    f = uq.build_field(**cfg.field_kwargs())
+    for faces in (True, False):
+        solver = uq.EnsembleSolver2D(f, cfg.cells, cfg.tol, cfg.maxit, faces=faces)
+        solver.solve_groups(np.random.default_rng(0).uniform(-1, 1, (2, 8, cfg.n_modes)))
+        nbytes = solver._ws.numel()
+        del solver
+        gc.collect()
+        guard = torch.full((nbytes // 8,), 7.0, dtype=torch.float64, device=_lib.device())
+        rng = np.random.default_rng(3)
+        a, b = rng.standard_normal((64, 4097)), rng.standard_normal((64, 4097))
+        got = uq.lane_dot(a, b)
+        np.testing.assert_allclose(got, np.einsum("sn,sn->s", a, b), rtol=1e-12)
+        assert bool((guard == 7.0).all())
