@@ -484,3 +484,37 @@ def test_dropped_solver_leaves_no_workspace_behind():
         got = uq.lane_dot(a, b)
         np.testing.assert_allclose(got, np.einsum("sn,sn->s", a, b), rtol=1e-12)
         assert bool((guard == 7.0).all())
+
+
+def test_interleaved_entry_points_are_deterministic():
+    """Level solves of two mesh sizes (faces and CSR), drop-in ensemble_pcg
+    and lane_dot calls interleaved, solvers created and dropped between
+    rounds: every round reproduces the first round's results bit for bit
+    (workspace reuse, growth and context state leave no trace)."""
+    import gc
+
+    cfg = uq.CONFIGS["C1"]
+    f = uq.build_field(**cfg.field_kwargs())
+    rng = np.random.default_rng(4)
+    ys_small = rng.uniform(-1, 1, (3, 8, cfg.n_modes))
+    ys_big = rng.uniform(-1, 1, (2, 16, cfg.n_modes))
+    lanes, rhs = spd_system(np.random.default_rng(9), 40, 3)
+    ens = uq.EnsembleCsrMatrix.from_scipy_lanes(lanes)
+    a, b = rng.standard_normal((16, 3000)), rng.standard_normal((16, 3000))
+
+    def one_round():
+        out = []
+        for cells, ys, faces in ((cfg.cells, ys_small, True), (96, ys_big, False),
+                                 (96, ys_big, True), (cfg.cells, ys_small, False)):
+            s = uq.EnsembleSolver2D(f, cells, cfg.tol, cfg.maxit, faces=faces)
+            r = s.solve_groups(ys)
+            out += [r.iterations.ravel().astype(float), r.qoi.ravel()]
+            res = uq.ensemble_pcg(ens, rhs, tol=1e-10, maxit=300)
+            out += [res.solution.ravel(), uq.lane_dot(a, b)]
+            del s
+            gc.collect()
+        return np.concatenate(out)
+
+    first = one_round()
+    for _ in range(3):
+        assert np.array_equal(one_round(), first)
