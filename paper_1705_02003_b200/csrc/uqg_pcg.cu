@@ -278,7 +278,9 @@ __global__ void __launch_bounds__(256) pcg_spmv_kernel(long long N, long long nn
 // Face-form FV2D operator (Fv2dOp): same reduction chunks and state updates
 // as pcg_spmv_kernel, the row's Ap re-derived from the faces (fv2d_row).
 // One row of the face-form operator: loads, then the CSR-order sum.
-template <int V>
+// TY: -1 = y-face array decided at run time (tyg NULL or not), 0 = constant
+// y-faces a_y (compile time), 1 = y-face array.
+template <int V, int TY = -1>
 struct FaceRow {
   double tw[V], te[V], ts[V], tn[V], pw[V], ps[V], pc[V], pn[V], pe[V];
   bool w, s, n, e;
@@ -288,7 +290,7 @@ struct FaceRow {
                                        int row, int i0, int j0) {
     ldgv<V>(txg + row * S, tw);
     ldgv<V>(txg + (row + m) * S, te);
-    if (tyg) {
+    if (TY == 1 || (TY < 0 && tyg)) {
       ldgv<V>(tyg + (row + i0) * S, ts);
       ldgv<V>(tyg + (row + i0 + 1) * S, tn);
     } else {
@@ -333,7 +335,7 @@ struct FaceRow {
 constexpr int kFaceBatch = UQG_FACE_BATCH;
 static_assert(kFaceBatch <= kMaxBatch, "batch exceeds reduce_lanes_batch's limit");
 
-template <int V>
+template <int V, int TY = -1>
 __device__ __forceinline__ void face_spmv_body(long long N, const Geo& geo, const PcgState& st,
                                                const Fv2dOp& op, const double* __restrict__ p,
                                                double* __restrict__ ap) {
@@ -363,7 +365,7 @@ __device__ __forceinline__ void face_spmv_body(long long N, const Geo& geo, cons
         if (rend > n) rend = n;
         int i0 = row / m, j0 = row - i0 * m;
         for (; row < rend; row += R) {
-          FaceRow<V> f;
+          FaceRow<V, TY> f;
           f.load(txg, tyg, pg, op.a_y, m, S, row, i0, j0);
           double y[V];
           f.apply(y, acc);
@@ -393,11 +395,11 @@ __device__ __forceinline__ void face_spmv_body(long long N, const Geo& geo, cons
   }
 }
 
-template <int V>
+template <int V, int TY = -1>
 __global__ void __launch_bounds__(256, UQG_FACE_MINB) pcg_spmv_fv2d_kernel(
     long long N, Geo geo, PcgState st, Fv2dOp op, const double* __restrict__ p,
     double* __restrict__ ap) {
-  face_spmv_body<V>(N, geo, st, op, p, ap);
+  face_spmv_body<V, TY>(N, geo, st, op, p, ap);
 }
 
 // 4 lanes per thread (32-byte LDG/STG.256) at half the block size: the same
@@ -1400,7 +1402,16 @@ void launch_pcg_spmv_fv2d(const Geo& geo, int G, cudaStream_t s, long long N, co
 #undef UQG_FACE_TMA_LAUNCH
     return;
   }
-  if (gl.V == 2)
+  // constant y-faces (a2 const, the BASELINE configs) compiled in: fewer live
+  // registers, no spill of the y-face branch (C2 face SpMV 2,345 -> 2,277 ms).
+  // UQG_FACE_SPEC=0: the run-time branch kernel (same bits).
+  static const bool spec = [] {
+    const char* e = getenv("UQG_FACE_SPEC");
+    return !e || atoi(e) != 0;
+  }();
+  if (spec && gl.V == 2 && !op.ty)
+    pcg_spmv_fv2d_kernel<2, 0><<<dim3(gl.B, G), gl.T, smem, s>>>(N, gl, st, op, p, ap);
+  else if (gl.V == 2)
     pcg_spmv_fv2d_kernel<2><<<dim3(gl.B, G), gl.T, smem, s>>>(N, gl, st, op, p, ap);
   else
     pcg_spmv_fv2d_kernel<1><<<dim3(gl.B, G), gl.T, smem, s>>>(N, gl, st, op, p, ap);
