@@ -437,7 +437,10 @@ __global__ void __launch_bounds__(256) spmv_fv2d_kernel(long long N, Geo geo, Fv
 #ifndef UQG_UPDATE_MINB
 #define UQG_UPDATE_MINB 3
 #endif
-constexpr int kUpdateBatch = 4;
+#ifndef UQG_UPDATE_BATCH
+#define UQG_UPDATE_BATCH 4
+#endif
+constexpr int kUpdateBatch = UQG_UPDATE_BATCH;
 static_assert(kUpdateBatch <= kMaxBatch, "batch exceeds reduce_lanes_batch's limit");
 
 template <int V>
@@ -1454,6 +1457,14 @@ void launch_pcg_update(const Geo& geo, int G, cudaStream_t s, long long N, const
                        const double* dinv, int maxit, double* r, const double* ap) {
   static SlotCache c1, c2;
   const size_t smem = red_bytes(geo, 2 * kUpdateBatch);
+  static size_t opted = 48 * 1024;  // > 48 KB of dynamic shared memory needs an opt-in
+  if (smem > opted) {
+    cudaFuncSetAttribute(pcg_update_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    cudaFuncSetAttribute(pcg_update_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    opted = smem;
+  }
   const Geo gl = geo.V == 2 ? sized(geo, c2, pcg_update_kernel<2>, geo.T, smem)
                             : sized(geo, c1, pcg_update_kernel<1>, geo.T, smem);
   UQG_DISPATCH_V(gl, pcg_update_kernel, dim3(gl.B, G), smem, s, N, gl, st, dinv, maxit, r, ap);
