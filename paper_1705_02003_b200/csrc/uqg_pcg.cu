@@ -443,7 +443,8 @@ __global__ void __launch_bounds__(256) spmv_fv2d_kernel(long long N, Geo geo, Fv
 constexpr int kUpdateBatch = UQG_UPDATE_BATCH;
 static_assert(kUpdateBatch <= kMaxBatch, "batch exceeds reduce_lanes_batch's limit");
 
-template <int V>
+// HD: 1 = Jacobi scaling present (compiled in), -1 = decided by dinv at run time
+template <int V, int HD = -1>
 __global__ void __launch_bounds__(256, UQG_UPDATE_MINB) pcg_update_kernel(long long N, Geo geo, PcgState st,
                                                          const double* __restrict__ dinv,
                                                          int maxit, double* __restrict__ r,
@@ -481,7 +482,7 @@ __global__ void __launch_bounds__(256, UQG_UPDATE_MINB) pcg_update_kernel(long l
             if (ok[u]) {
               ldv<V>(r + o[u], rv[u]);
               ldv<V>(ap + o[u], av[u]);
-              if (dinv) ldgv<V>(dinv + o[u], dv[u]);
+              if (HD == 1 || (HD < 0 && dinv)) ldgv<V>(dinv + o[u], dv[u]);
             }
           }
 #pragma unroll
@@ -491,7 +492,7 @@ __global__ void __launch_bounds__(256, UQG_UPDATE_MINB) pcg_update_kernel(long l
 #pragma unroll
             for (int j = 0; j < V; ++j) {
               rv[u][j] = __dsub_rn(rv[u][j], __dmul_rn(alpha[j], av[u][j]));
-              zv[j] = dinv ? __dmul_rn(rv[u][j], dv[u][j]) : rv[u][j];
+              zv[j] = (HD == 1 || (HD < 0 && dinv)) ? __dmul_rn(rv[u][j], dv[u][j]) : rv[u][j];
               acc[0][j] = __fma_rn(rv[u][j], rv[u][j], acc[0][j]);
               acc[1][j] = __fma_rn(rv[u][j], zv[j], acc[1][j]);
             }
@@ -1463,7 +1464,20 @@ void launch_pcg_update(const Geo& geo, int G, cudaStream_t s, long long N, const
                          (int)smem);
     cudaFuncSetAttribute(pcg_update_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
+    cudaFuncSetAttribute(pcg_update_kernel<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
     opted = smem;
+  }
+  // UQG_UPDATE_SPEC=0: the run-time dinv branch kernel for Jacobi solves too (same bits)
+  static const bool spec = [] {
+    const char* e = getenv("UQG_UPDATE_SPEC");
+    return !e || atoi(e) != 0;
+  }();
+  if (spec && geo.V == 2 && dinv) {
+    static SlotCache cj;
+    const Geo gl = sized(geo, cj, pcg_update_kernel<2, 1>, geo.T, smem);
+    pcg_update_kernel<2, 1><<<dim3(gl.B, G), gl.T, smem, s>>>(N, gl, st, dinv, maxit, r, ap);
+    return;
   }
   const Geo gl = geo.V == 2 ? sized(geo, c2, pcg_update_kernel<2>, geo.T, smem)
                             : sized(geo, c1, pcg_update_kernel<1>, geo.T, smem);

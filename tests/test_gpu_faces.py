@@ -89,7 +89,7 @@ _VARIANTS = {  # face SpMV variants (all must give the CSR bits)
     "tma4": {"UQG_FACE_TMA": "4"},
     "fixed": {"UQG_OCC_BLOCKS": "0"},                     # with_groups block sizing
     "graph": {"UQG_PCG_GRAPH": "1"},                      # launch loop as one graph launch
-    "nospec": {"UQG_FACE_SPEC": "0"},                     # run-time y-face branch kernel
+    "nospec": {"UQG_FACE_SPEC": "0", "UQG_UPDATE_SPEC": "0"},  # run-time branch kernels
 }
 
 
