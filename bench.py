@@ -4,16 +4,23 @@ One *step* = the hot path over one level's batch of samples: device stable
 sort of the surrogate keys + chunking into width-S groups, KL coefficient at
 every node, sample-interleaved assembly of every group's operator, batched
 Jacobi-PCG of all groups to their own termination, per-lane QoI.  The
-workload (default C2: n=256, M=4, S=16, rtol 1e-8, adaptive grid to total
-level 5) is the last adaptive level of the study: levels 1..L-1 are solved in
-the untimed setup to fit the iteration surrogate that keys the final level.
+workload (default C3: n=512, M=6, sigma=1.5, S=32, rtol 1e-8 - the config
+BASELINE.json's 1/2/4/8-GPU metric is quoted on) is the study's last adaptive
+level (``bench_workloads/C3.npz``: its samples and the surrogate keys that
+grouped it).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3]
+                    [--impl ours|reference] [--scaling strong|weak]
 
-N>1 (torchrun): weak scaling - rank r solves the final level's sample set
-reflected through the sign pattern of r's bits (same grid, same shape of
-work, distinct samples), no collective on the solve path; the step time is
-the max over ranks.  Prints ONE JSON line on rank 0.
+N>1 (torchrun, one rank per GPU, NCCL): strong scaling by default - every
+rank builds the identical plan, solves the groups k = rank (mod N) of it
+(``dist.LevelShard``) and one ``all_gather_into_tensor`` returns the whole
+level's iterations and QoIs to every rank (the input of the surrogate
+refit); the step time is the max over ranks.  ``--scaling weak`` gives every
+rank a mirrored copy of the whole level instead.  Prints ONE JSON line on
+rank 0.  ``--impl reference`` times the reference's CPU path (the oracle
+port: uqgroup's algorithm with scipy csr_matvec and numpy dots) on every host
+core on the same workload and config.
 """
 
 from __future__ import annotations
@@ -32,9 +39,18 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 WORKLOADS = ROOT / "bench_workloads"
+GOLDEN = ROOT / "tests" / "golden"
 # BASELINE.json's metric, verbatim (value = ensemble sample-solves/s; the
 # SpMV/PCG HBM GB/s vs peak part is reported in `roofline` / `pcg_loop`)
 METRIC = "ensemble sample-solves/s at 1/2/4/8 B200; SpMV+PCG HBM GB/s vs peak"
+
+# CPU legs: PCG iterations timed per group (None = full solve).  Full solves
+# of a C2-C5 group take 15 s to many minutes on one core, so the
+# CPU legs time a fixed number of iterations per group and project the full
+# solve with the reference's own iteration count for that group
+# (tests/golden, from uqgroup's ensemble_pcg) - BASELINE.md 4.
+REF_ITERS = {"C1": None, "C2": 40, "C3": 8, "C4": 3, "C5": 2}      # --impl reference, per step
+BASE_ITERS = {"C1": None, "C2": None, "C3": 30, "C4": 6, "C5": 3}  # cpu_baseline (1 core)
 
 
 def parse():
@@ -42,13 +58,17 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N>1: strong = the level's groups sharded over ranks + one allgather "
+                         "(default); weak = every rank solves a mirrored copy of the level")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--prof-steps", type=int, default=1,
+                    help="steps of the profiled (per-launch CUDA events, one stream) pass")
     ap.add_argument("--separate-kernel-timing", action="store_true",
-                    help="(default behaviour; kept for old command lines) value from "
-                         "un-instrumented steps, kernel breakdown from a profiled pass")
+                    help="(default behaviour; kept for old command lines)")
     ap.add_argument("--max-iters", type=int, default=None,
                     help="throughput mode: run exactly this many PCG iterations per group "
                          "(value = sample-iterations/s); for C4/C5 where full solves take minutes")
@@ -146,10 +166,16 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200", "-i", str(self.index)], stdout=subprocess.PIPE,
+                 "-lms", "20", "-i", str(self.index)], stdout=subprocess.PIPE,
                 stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
+            # wait for the first sample, so short timed regions (C1: ~0.1 s)
+            # are sampled from their start
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.01)
+            self.lines.clear()
         except FileNotFoundError:
             self.proc = None
         return self
@@ -183,6 +209,85 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
+# shared by both arms: the config dict, the reference's results, the host
+
+def config_dict(cfg, n, K, world, scaling, meta, extra=None):
+    """The `config` object of the JSON line - identical for both arms."""
+    d = {"workload": f"{cfg.name}: final adaptive level ({n} samples, {K} groups of "
+                     f"S={cfg.ensemble_size}) - group sort + KL + assembly + batched "
+                     "Jacobi-PCG + QoI",
+         "n": cfg.cells, "unknowns": cfg.n_dofs, "M": cfg.n_modes, "S": cfg.ensemble_size,
+         "rtol": cfg.tol, "delta": cfg.delta, "sigma": cfg.sigma0,
+         "parallelism": (f"groups round-robin over {world} GPU(s) + 1 allgather"
+                         if scaling == "strong" else f"weak x{world} (mirrored level per rank)"),
+         "workload_source": meta.get("source")}
+    d.update(extra or {})
+    return d
+
+
+def golden_level(cfg_name, ids, coords):
+    """The reference's own results for this workload's level - uqgroup's
+    ``group_by_key`` + ``ensemble_pcg`` on the oracle 2D operator, committed by
+    ``tests/golden/make_golden.py`` - or None when no fixture covers it.
+    Returns {ensembles, iterations {sid: it}, qoi {sid: q}, ensemble_iterations [K]}."""
+    ids = [int(i) for i in ids]
+    if cfg_name in ("C1", "C2"):
+        path = GOLDEN / f"{cfg_name.lower()}_adaptive.json"
+        if not path.exists():
+            return None
+        lv = json.loads(path.read_text())["levels"][-1]
+        if lv["ids"] != ids or not np.array_equal(np.asarray(lv["coords"]), coords):
+            return None
+        return {"ensembles": [list(g) for g in lv["ensembles"]],
+                "iterations": dict(zip(lv["ids"], lv["iterations"])),
+                "qoi": dict(zip(lv["ids"], lv["qoi"])),
+                "ensemble_iterations": lv["ensemble_iterations"], "source": path.name}
+    if cfg_name == "C3":
+        path = GOLDEN / "c3_level.json"
+        if not path.exists():
+            return None
+        doc = json.loads(path.read_text())
+        it, q = {}, {}
+        for grp, res in zip(doc["ensembles"], doc["groups"]):
+            for s, sid in enumerate(grp):
+                if sid not in it:
+                    it[sid], q[sid] = res["iterations"][s], res["qoi"][s]
+        if sorted(it) != sorted(ids):
+            return None
+        return {"ensembles": doc["ensembles"], "iterations": it, "qoi": q,
+                "ensemble_iterations": [r["ensemble_iterations"] for r in doc["groups"]],
+                "source": path.name}
+    return None
+
+
+def parity(gold, ensembles, iters, qois):
+    """GPU level vs the reference's: plan identity, per-sample iteration and
+    QoI differences (north_star gates: +-1, 1e-8 relative)."""
+    if gold is None:
+        return None
+    same_plan = [list(g) for g in ensembles] == gold["ensembles"]
+    d_it = max(abs(iters[s] - gold["iterations"][s]) for s in gold["iterations"])
+    d_q = max(abs(qois[s] - gold["qoi"][s]) / abs(gold["qoi"][s]) for s in gold["qoi"])
+    return {"reference": f"tests/golden/{gold['source']} (uqgroup group_by_key + ensemble_pcg)",
+            "samples": len(gold["iterations"]), "groups": len(gold["ensembles"]),
+            "identical_plan": bool(same_plan), "max_iter_diff": int(d_it),
+            "max_qoi_rel": float(d_q),
+            "ok": bool(same_plan and d_it <= 1 and d_q <= 1e-8)}
+
+
+def host_info():
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.lower().startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return {"cpu_model": model, "cpu_count": os.cpu_count()}
+
+
+# ---------------------------------------------------------------------------
 # CPU legs (oracle = the reference algorithm restated; test infra, used here
 # only as the timed CPU baseline)
 
@@ -212,7 +317,11 @@ def _cpu_warm(cfg_name):
 
 
 def _cpu_group_worker(args):
-    cfg_name, samples = args
+    """One group through the CPU path, 1 thread.  ``maxit`` None: full solve.
+    Otherwise the PCG runs ``maxit`` iterations, and its initialisation
+    (Jacobi inverse, r = b, norms) is timed separately by a maxit=0 run, so
+    the per-iteration time excludes it."""
+    cfg_name, samples, maxit = args
     from threadpoolctl import threadpool_limits
 
     from oracle import fv2d as ofv, pcg as opcg
@@ -221,10 +330,33 @@ def _cpu_group_worker(args):
     with threadpool_limits(limits=1):
         t0 = time.perf_counter()
         sysm = ofv.assemble(mesh, fld, samples, table, cfg.a2)
+        t_asm = time.perf_counter() - t0
+        t_init = 0.0
+        if maxit is not None:
+            t0 = time.perf_counter()
+            opcg.pcg(sysm.row_offsets, sysm.col_indices, sysm.values, sysm.rhs, tol=cfg.tol,
+                     maxit=0)
+            t_init = time.perf_counter() - t0
+        t0 = time.perf_counter()
         res = opcg.pcg(sysm.row_offsets, sysm.col_indices, sysm.values, sysm.rhs, tol=cfg.tol,
-                       maxit=cfg.maxit)
+                       maxit=cfg.maxit if maxit is None else maxit)
+        t_pcg = time.perf_counter() - t0
+        t0 = time.perf_counter()
         q = [ofv.qoi(u) for u in res.solution]
-        return time.perf_counter() - t0, res.ensemble_iterations, q
+        t_qoi = time.perf_counter() - t0
+    # fixed-iteration runs: the PCG's initialisation counts as setup, so
+    # "pcg" is exactly iters_run iterations
+    return {"setup": t_asm + t_init + t_qoi, "pcg": t_pcg - t_init,
+            "iters_run": int(res.ensemble_iterations), "full": maxit is None,
+            "iterations": [int(v) for v in res.iterations], "qoi": q}
+
+
+def _projected_seconds(r, its_full):
+    """Full-solve seconds of a group from a fixed-iteration sample: setup +
+    per-iteration time x the group's full iteration count."""
+    if r["full"]:
+        return r["setup"] + r["pcg"]
+    return r["setup"] + r["pcg"] / max(1, r["iters_run"]) * its_full
 
 
 def cpu_plan(cfg, coords, keys):
@@ -235,62 +367,137 @@ def cpu_plan(cfg, coords, keys):
     return ogrp.by_key(ids, dict(zip(ids, keys)), cfg.ensemble_size)[0]
 
 
-def cpu_baseline(cfg, coords, keys):
-    """Oracle port, 1 thread, one median-cost group of the same level."""
+def full_iterations(cfg, plan_rows, gold, keys, max_iters):
+    """Per-group full-solve iteration counts used to project fixed-iteration
+    CPU samples: the reference's own counts (golden) when they cover the
+    workload, else the surrogate's prediction (max key of the group)."""
+    if max_iters:
+        return [max_iters] * len(plan_rows), f"throughput mode: {max_iters} iterations per group"
+    if gold is not None:
+        return list(gold["ensemble_iterations"]), f"reference counts, tests/golden/{gold['source']}"
+    if keys is not None:
+        return ([int(np.ceil(max(keys[j] for j in g))) for g in plan_rows],
+                "surrogate-predicted counts (max key per group)")
+    return None, "no full iteration counts for this workload"
+
+
+def cpu_baseline(cfg, ids, coords, keys, gold, max_iters, gpu_rows=None):
+    """Oracle port, 1 thread, the median-cost group of the same level (bounded
+    ~10-30 s: a full solve at C1/C2, BASE_ITERS iterations projected with the
+    reference's iteration count at C3-C5)."""
     ens = cpu_plan(cfg, coords, keys)
-    g = ens[len(ens) // 2]
-    dt, its, _ = _cpu_group_worker((cfg.name, coords[list(g)]))
+    k = len(ens) // 2
+    g = ens[k]
+    maxit = BASE_ITERS.get(cfg.name)
+    if max_iters:
+        maxit = min(maxit or max_iters, max_iters)
+    r = _cpu_group_worker((cfg.name, coords[list(g)], maxit))
+    full, src = full_iterations(cfg, ens, gold, keys, max_iters)
     S = cfg.ensemble_size
-    return {"value": S / dt, "unit": "sample-solves/s", "cores": 1, "kind": "port",
-            "sample": f"1 group (S={S}) of the {cfg.name} final level (group {len(ens) // 2} of "
-                      f"{len(ens)} in surrogate order): 2D KL + assembly + Jacobi-PCG "
-                      f"({its} iterations) + QoI, oracle/ numpy+scipy, 1 thread, {dt:.1f}s"}
+    out = {"unit": "sample-solves/s" if not max_iters else "sample-iterations/s", "cores": 1,
+           "kind": "port" if r["full"] else "port (projected)", **host_info()}
+    if full is None and not r["full"]:
+        out.update(value=None, sample="no iteration counts to project a full solve")
+        return out
+    t = _projected_seconds(r, full[k] if full else r["iters_run"])
+    out["value"] = S / t * (max_iters or 1)
+    how = ("full solve" if r["full"] else
+           f"{r['iters_run']} PCG iterations timed ({r['pcg']:.1f}s) + setup {r['setup']:.1f}s, "
+           f"projected to {full[k]} iterations ({src})")
+    out["sample"] = (f"group {k} of {len(ens)} (S={S}, median in surrogate order) of the {cfg.name} "
+                     f"final level: 2D KL + assembly + Jacobi-PCG + QoI, oracle/ numpy+scipy, "
+                     f"1 thread; {how}")
+    if r["full"] and gpu_rows is not None:
+        it_g, q_g = gpu_rows(k)
+        out["parity_vs_gpu"] = {
+            "group": k, "max_iter_diff": int(max(abs(a - b) for a, b in zip(it_g, r["iterations"]))),
+            "max_qoi_rel": float(max(abs(a - b) / abs(b) for a, b in zip(q_g, r["qoi"])))}
+    return out
 
 
 def run_reference(args, cfg):
-    """--impl reference: the CPU path on all host cores (multiprocessing, 1 thread each)."""
+    """--impl reference: the CPU path on all host cores (multiprocessing, one
+    process per core, 1 BLAS thread each) on the SAME workload and config as
+    the GPU arm.  Each step solves a stratified sample of the level's groups
+    (every (K/P)-th group in surrogate order, shifted by one per step; never a
+    cheapest prefix), one group per process; at C2-C5 each group runs
+    REF_ITERS PCG iterations and the step projects the WHOLE level's time from
+    the per-iteration rate and every group's full iteration count (the
+    reference's own counts, tests/golden) over P cores with perfect load
+    balance - which favours the reference."""
     import multiprocessing as mproc
 
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     ids, coords, keys, meta = make_workload(cfg)
+    if args.max_samples and len(ids) > args.max_samples:
+        ids, coords = ids[: args.max_samples], coords[: args.max_samples]
+        keys = None if keys is None else keys[: args.max_samples]
+    n, S = len(ids), cfg.ensemble_size
     cores = os.cpu_count() or 1
-    t0 = time.perf_counter()
     ens = cpu_plan(cfg, coords, keys)
-    t_group = time.perf_counter() - t0
-    P = max(1, min(cores, len(ens)))
-    steps = max(1, min(args.steps, 3))
-    times, done = [], 0
+    K = len(ens)
+    gold = golden_level(cfg.name, ids, coords)
+    full, src = full_iterations(cfg, ens, gold, keys, args.max_iters)
+    P = max(1, min(cores, K))
+    maxit = REF_ITERS.get(cfg.name)
+    if args.max_iters:
+        maxit = min(maxit or args.max_iters, args.max_iters)
+    if full is None and maxit is not None:
+        print(json.dumps({"impl": "reference", "unavailable": src}), flush=True)
+        return
+    times, samples = [], []
     ctx = mproc.get_context("spawn")
     with ctx.Pool(P) as pool:
-        # untimed warm-up: worker start-up and the per-process setup
-        warm = 1 if args.warmup > 0 else 0
-        if warm:
-            pool.map(_cpu_warm, [cfg.name] * P, chunksize=1)
-        for st in range(steps):
-            chosen = [ens[(st * P + j) % len(ens)] for j in range(P)]
-            t0 = time.perf_counter()
-            out = pool.map(_cpu_group_worker, [(cfg.name, coords[list(g)]) for g in chosen])
-            times.append(time.perf_counter() - t0 + t_group)
-            done += P * cfg.ensemble_size
-    total = sum(times)
-    value = done / total
-    S = cfg.ensemble_size
+        pool.map(_cpu_warm, [cfg.name] * P, chunksize=1)  # worker start-up + per-process setup
+
+        def one(st):
+            if maxit is None:  # full solves of the whole level (C1): its wall time
+                chosen = list(range(K))
+                t0 = time.perf_counter()
+                rs = pool.map(_cpu_group_worker, [(cfg.name, coords[list(ens[k])], None)
+                                                  for k in chosen], chunksize=1)
+                return n / (time.perf_counter() - t0), chosen, rs
+            chosen = sorted({(j * K // P + st) % K for j in range(P)})
+            rs = pool.map(_cpu_group_worker, [(cfg.name, coords[list(ens[k])], maxit)
+                                              for k in chosen], chunksize=1)
+            t_iter = sum(r["pcg"] / max(1, r["iters_run"]) for r in rs) / len(rs)
+            t_setup = sum(r["setup"] for r in rs) / len(rs)
+            level_s = (t_setup * K + t_iter * sum(full)) / P
+            return n / level_s * (args.max_iters or 1), chosen, rs
+
+        for st in range(args.warmup):
+            one(K - 1 - st)
+        t0 = time.perf_counter()
+        for st in range(args.steps):
+            v, chosen, rs = one(st)
+            times.append(v)
+            samples.append(chosen)
+        wall = time.perf_counter() - t0
+    value = float(np.mean(times))
+    unit = "sample-solves/s" if not args.max_iters else \
+        f"sample-iterations/s (throughput mode: {args.max_iters} PCG iterations per group)"
+    how = ("full solves of every group" if maxit is None else
+           f"{maxit} PCG iterations per group timed, the whole level projected with every "
+           f"group's full iteration count ({src}) over {P} cores")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value,
-        "unit": "sample-solves/s", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
-        "ms_per_step": 1e3 * total / steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg.name} final adaptive level, {P} groups per step",
-                   "n": cfg.cells, "M": cfg.n_modes, "S": S, "rtol": cfg.tol},
-        "cpu_baseline": {"value": value, "unit": "sample-solves/s", "cores": P, "kind": "port",
-                         "sample": f"{P} groups x S={S} per step (one group per process, "
-                                   "1 BLAS thread each) of the final level; oracle/ restatement "
-                                   "of uqgroup's path (reference is pure Python; its 2D operator "
-                                   "does not exist, see DESIGN.md)"},
-        "e2e": {"value": value, "unit": "sample-solves/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": unit,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * wall / max(1, args.steps), "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (committed bench workload; see DESIGN.md)",
+        "config": config_dict(cfg, n, K, world, args.scaling, meta),
+        "cpu_baseline": {
+            "value": value, "unit": unit, "cores": P,
+            "kind": "port" if maxit is None else "port (projected)",
+            "sample": f"per step {len(samples[0]) if samples else 0} of {K} groups (stratified: "
+                      f"every {K / P:.1f}th in surrogate order, offset = step), one per process, "
+                      f"1 BLAS thread each; {how}; oracle/ restatement of uqgroup's path (the "
+                      "reference is pure Python; its 2D operator does not exist, DESIGN.md)",
+            "step_values": times, **host_info()},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -327,6 +534,7 @@ def main():
     import paper_1705_02003_b200 as uq
     from paper_1705_02003_b200 import _lib
     from paper_1705_02003_b200.build import needs_build, build
+    from paper_1705_02003_b200.dist import LevelShard
 
     if needs_build():
         build()
@@ -343,30 +551,34 @@ def main():
     if args.max_samples and len(ids) > args.max_samples:
         ids, coords = ids[: args.max_samples], coords[: args.max_samples]
         keys = None if keys is None else keys[: args.max_samples]
-    # weak scaling: rank r solves the mirror images of the level's samples and
-    # groups them by the keys of their originals (same sort work, same costs shape)
-    coords = reflect(coords, rank)
+    strong = args.scaling == "strong"
+    if not strong:
+        # weak scaling: rank r solves the mirror images of the level's samples and
+        # groups them by the keys of their originals (same sort work, same costs shape)
+        coords = reflect(coords, rank)
     n, S = len(ids), cfg.ensemble_size
+    K = -(-n // S)
     dev = _lib.device()
     coll_dev = torch.device("cpu") if share else dev  # gloo test hook collects on the host
+    shard = LevelShard(rank, world, None, coll_dev) if (strong and world > 1) else None
     d_coords = torch.from_numpy(np.ascontiguousarray(coords)).to(dev)
     d_keys = None if keys is None else torch.from_numpy(np.ascontiguousarray(keys)).to(dev)
     lib, ctx = _lib.load(), _lib.ctx()
     stream = torch.cuda.current_stream()
+    mine = list(range(rank, K, world)) if shard is not None else list(range(K))
 
     def barrier():
         if world > 1:
             dist.barrier()
 
     def step():
-        out = solver.run_level_device(d_coords, n, S, d_keys)
-        if world > 1:
-            # the study's one collective: per-slot iterations + QoIs of every rank's
-            # groups allgathered (NCCL) for the surrogate refit (harness.py:658-660)
+        out = solver.run_level_device(d_coords, n, S, d_keys, shard)
+        if world > 1 and not strong:
+            # weak mode: the study's one collective on each rank's own level
             groups, pad, it, cv, en, q = out
-            mine = torch.cat([it.double(), q]).to(coll_dev)
-            allv = torch.empty(world * mine.numel(), dtype=mine.dtype, device=coll_dev)
-            dist.all_gather_into_tensor(allv, mine)
+            m = torch.cat([it.double(), q]).to(coll_dev)
+            allv = torch.empty(world * m.numel(), dtype=m.dtype, device=coll_dev)
+            dist.all_gather_into_tensor(allv, m)
         return out
 
     for _ in range(max(3, args.warmup)):
@@ -376,16 +588,16 @@ def main():
     import ctypes
     NK = 10
 
-    def timed(profile: bool):
-        """K timed steps; per-launch CUDA-event kernel timing when `profile`."""
+    def timed(profile: bool, steps: int):
+        """`steps` timed steps; per-launch CUDA-event kernel timing when `profile`."""
         ms = (ctypes.c_double * NK)()
         cnt = (ctypes.c_longlong * NK)()
         lib.uqg_ctx_profile_read(ctx, ms, cnt, 1)
         lib.uqg_ctx_profile(ctx, int(profile))
         launches0 = lib.uqg_ctx_launch_count(ctx)
-        times, group_iters, last = [], 0, None
+        times, local_iters, last = [], 0, None
         with ClockSampler(torch.cuda.current_device()) as clocks:
-            for _ in range(args.steps):
+            for _ in range(steps):
                 barrier()
                 torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -399,30 +611,33 @@ def main():
                     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
                     t = float(tt.item())
                 times.append(t)
-                group_iters += int(last[4].sum().item())
+                # this rank's group-iterations (its own kernels' work)
+                local_iters += int(last[4][mine].sum().item())
                 barrier()
         launches = lib.uqg_ctx_launch_count(ctx) - launches0
         lib.uqg_ctx_profile_read(ctx, ms, cnt, 1)
         lib.uqg_ctx_profile(ctx, 0)
-        return times, group_iters, launches, ms, cnt, clocks, last
+        return times, local_iters, launches, ms, cnt, clocks, last
 
     # value from un-instrumented steps (the library solves a level's groups as
     # concurrent parts on several streams); the per-kernel times for the
     # roofline from an identical profiled pass on ONE stream, so each launch's
     # duration is that kernel's alone (UQG_SOLVE_STREAMS=1; same results).
-    times, group_iters, launches, _, _, clocks, last = timed(False)
+    times, local_iters, launches, _, _, clocks, last = timed(False, args.steps)
     prev = os.environ.get("UQG_SOLVE_STREAMS")
     os.environ["UQG_SOLVE_STREAMS"] = "1"
     try:
-        _, prof_iters, _, ms, cnt, _, _ = timed(True)
+        prof_steps = max(1, min(args.prof_steps, args.steps))
+        _, prof_iters, _, ms, cnt, _, _ = timed(True, prof_steps)
     finally:
         if prev is None:
             os.environ.pop("UQG_SOLVE_STREAMS", None)
         else:
             os.environ["UQG_SOLVE_STREAMS"] = prev
-    assert prof_iters == group_iters
+    assert prof_iters * args.steps == local_iters * prof_steps
     groups, pad, it, cv, en, q = last
     conv_all = bool(cv.all().item())
+    load = shard.last_load if shard is not None else None
 
     # ---- end to end through the public API: host inputs, host results -------
     e2e_steps = args.e2e_steps or args.steps
@@ -431,7 +646,8 @@ def main():
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        plan, iters, qois, notes = solver.solve_level(ids, coords, S, keys=keys, level=99)
+        plan, iters, qois, notes = solver.solve_level(ids, coords, S, keys=keys, level=99,
+                                                      shard=shard)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if world > 1:
@@ -439,7 +655,6 @@ def main():
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             dt = float(tt.item())
         e2e_t.append(dt)
-    K = len(plan.ensembles)
     h2d = coords.nbytes + (0 if keys is None else 8 * n)
     d2h = 8 * (K * S * 4 + K)
 
@@ -448,7 +663,8 @@ def main():
             dist.destroy_process_group()
         return
     total_ms = sum(times)
-    value = world * n * len(times) / (total_ms / 1e3)
+    per_step = n if strong else world * n
+    value = per_step * len(times) / (total_ms / 1e3)
     unit = "sample-solves/s"
     if args.max_iters:  # throughput mode: sample-iterations per second
         value *= args.max_iters
@@ -464,15 +680,16 @@ def main():
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
         traffic_all = json.loads(tf.read_text())
-    # per-kernel rooflines of the three PCG kernels; the line's "roofline" is the
-    # one with the largest measured time share (the dominant kernel)
+    # per-kernel rooflines of the PCG kernels (group-iterations of THIS rank's
+    # groups in the profiled pass); the line's "roofline" is the single
+    # kernel with the largest measured time share (the dominant kernel)
     spmv_name = "pcg_spmv_fv2d_kernel" if bm["operator"] != "csr" else "pcg_spmv_tma_kernel"
     per = {}
-    dir_name = "pcg_dir_kernel" + (" + pcg_flush_kernel" if "flush" in bm else "")
     for key, idx, kname in (("spmv", 3, spmv_name), ("update", 4, "pcg_update_kernel"),
-                            ("dir", 5, dir_name)):
+                            ("dir", 5, "pcg_dir_kernel + pcg_flush_kernel" if "flush" in bm
+                             else "pcg_dir_kernel")):
         t_ms = ms[idx]
-        gbs = group_iters * bm[key] / (t_ms / 1e3) / 1e9 if t_ms else None
+        gbs = prof_iters * bm[key] / (t_ms / 1e3) / 1e9 if t_ms else None
         tr = traffic_all.get(f"{cfg.name}:{kname}", {})
         per[key] = {"kernel": kname, "ms": t_ms, "achieved": gbs,
                     "frac": gbs / peak if gbs else None,
@@ -486,7 +703,7 @@ def main():
         # iteration, x updated in place) - its roofline is the loop's
         bm1 = bytes_model(cfg, solver.op, 1)
         b_it = bm1["spmv"] + bm1["update"] + bm1["dir"]
-        gbs = group_iters * b_it / (ms[3] / 1e3) / 1e9 if ms[3] else None
+        gbs = prof_iters * b_it / (ms[3] / 1e3) / 1e9 if ms[3] else None
         tr = traffic_all.get(f"{cfg.name}:pcg_persistent_kernel", {})
         per = {"persistent": {
             "kernel": "pcg_persistent_kernel (whole solve; per group-iteration: SpMV + update "
@@ -498,11 +715,27 @@ def main():
             "traffic_source": tr.get("source")}}
     dom = max(per, key=lambda k: per[k]["ms"] or 0.0)
     loop_ms = ms[3] + ms[4] + ms[5]
-    loop_gbs = group_iters * bm["pcg_iter"] / (loop_ms / 1e3) / 1e9 if loop_ms else None
-    step_gbs = group_iters * bm["pcg_iter"] / (total_ms / 1e3) / 1e9
+    loop_gbs = prof_iters * bm["pcg_iter"] / (loop_ms / 1e3) / 1e9 if loop_ms else None
+    step_gbs = local_iters * bm["pcg_iter"] / (total_ms / 1e3) / 1e9
     kern = {name: {"ms": ms[k], "launches": int(cnt[k])} for k, name in enumerate(
         ["kl", "assemble", "pcg_init", "pcg_spmv", "pcg_update", "pcg_dir", "dot_qoi", "group",
          "spmv", "other"]) if cnt[k]}
+    all_ms = sum(ms[k] for k in range(NK))
+
+    # ---- parity of this run's level against the reference's results ----------
+    g_host = groups.cpu().numpy().reshape(K, S)
+    ens_ids = [[int(ids[j]) for j in row] for row in g_host]
+    it_h = it.cpu().numpy().reshape(K, S)
+    q_h = q.cpu().numpy().reshape(K, S)
+    first_it, first_q = {}, {}
+    for k_, row in enumerate(ens_ids):
+        for s_, sid in enumerate(row):
+            if sid not in first_it:
+                first_it[sid], first_q[sid] = int(it_h[k_, s_]), float(q_h[k_, s_])
+    gold = None if (args.max_iters or args.max_samples or not strong and world > 1) else \
+        golden_level(cfg.name, ids, coords)
+    par = parity(gold, ens_ids, first_it, first_q)
+
     line = {
         "metric": METRIC,
         "value": value,
@@ -512,21 +745,16 @@ def main():
         "warmup": max(3, args.warmup),
         "ms_per_step": total_ms / len(times),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: final adaptive level ({n} samples/rank, {K} groups "
-                               f"of S={S}) - group sort + KL + assembly + batched Jacobi-PCG + QoI",
-                   "n": cfg.cells, "unknowns": cfg.n_dofs, "M": cfg.n_modes, "S": S,
-                   "rtol": cfg.tol, "delta": cfg.delta, "sigma": cfg.sigma0,
-                   "parallelism": f"groups sharded weak x{world}",
-                   "l2": "inputs larger than L2 (operator+vectors of all groups ~"
-                         f"{solver.bytes_per_group(S) * K / 1e9:.1f} GB per step)",
-                   "workload_source": meta.get("source")},
+        "data": "synthetic (committed bench workload; see DESIGN.md)",
+        "config": config_dict(cfg, n, K, world, args.scaling, meta, {
+            "l2": "inputs larger than L2 (operator+vectors of all groups ~"
+                  f"{solver.bytes_per_group(S) * K / 1e9:.1f} GB per step)"}),
         "gpu_launches": int(launches),
-        "e2e": {"value": world * n * len(e2e_t) / sum(e2e_t) * (args.max_iters or 1),
-                "unit": unit,
+        "e2e": {"value": per_step * len(e2e_t) / sum(e2e_t) * (args.max_iters or 1),
+                "unit": unit, "steps": len(e2e_t),
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "roofline": {"bound": "hbm", "kernel": per[dom]["kernel"], "operator": bm["operator"],
                      "achieved": per[dom]["achieved"], "peak": peak, "unit": "GB/s",
@@ -538,24 +766,32 @@ def main():
                      "peak_spec": 8000.0,
                      "frac_spec": (per[dom]["achieved"] / 8000.0) if per[dom]["achieved"] else None,
                      "bytes_per_group_launch": per[dom]["bytes_per_group_launch"],
-                     "group_launches": group_iters,
-                     "timing": "per-launch CUDA events on the launching stream, profiled pass "
-                               "with the level on one stream (UQG_SOLVE_STREAMS=1)",
-                     "time_share": (per[dom]["ms"] / sum(ms[k] for k in range(NK))
-                                    if sum(ms[k] for k in range(NK)) else None),
+                     "group_launches": prof_iters,
+                     "timing": f"per-launch CUDA events on the launching stream, {prof_steps} "
+                               "profiled step(s) with the level on one stream "
+                               "(UQG_SOLVE_STREAMS=1)",
+                     "time_share": per[dom]["ms"] / all_ms if all_ms else None,
                      "pcg_kernels": per},
         "pcg_loop": {"achieved_gbs": loop_gbs, "frac": loop_gbs / peak if loop_gbs else None,
                      "bytes_per_group_iter": bm["pcg_iter"],
                      "moved_gbs": (loop_gbs * bm["pcg_iter_moved"] / bm["pcg_iter"])
                      if loop_gbs else None,
                      "moved_bytes_per_group_iter": bm["pcg_iter_moved"], "step_gbs": step_gbs,
-                     "group_iterations": group_iters},
+                     "group_iterations": local_iters},
         "kernels": kern,
         "all_converged": conv_all,
+        "parity": par,
         "clocks": clocks.summary(),
     }
+    if load is not None:
+        gi = load["group_iterations"]
+        line["shards"] = {"groups_per_rank": load["groups"], "group_iterations_per_rank": gi,
+                          "imbalance_max_over_mean": max(gi) / (sum(gi) / len(gi)) if sum(gi)
+                          else None}
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(cfg, coords, keys)
+        line["cpu_baseline"] = cpu_baseline(
+            cfg, ids, coords, keys, gold, args.max_iters,
+            lambda k_: (it_h[k_].tolist(), q_h[k_].tolist()))
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

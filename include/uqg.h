@@ -61,7 +61,7 @@ int uqg_ctx_set_band_hint(uqg_ctx* ctx, int nbands, const int* starts_host,
 #define UQG_K_PCG_UPDATE 4 /* r update + r.r, r.z                       */
 #define UQG_K_PCG_DIR 5    /* p = z + beta p, deferred x updates         */
 #define UQG_K_DOT 6        /* lane_dot / qoi                             */
-#define UQG_K_GROUP 7      /* rank sort + chunk                          */
+#define UQG_K_GROUP 7      /* key bits + radix sort + chunk              */
 #define UQG_K_SPMV 8       /* standalone spmv                            */
 #define UQG_K_OTHER 9      /* diagonal, jacobi, finalize                 */
 #define UQG_NKERN 10
@@ -232,9 +232,17 @@ int uqg_anisotropy_indicator(uqg_ctx* ctx, const double* modes, int P, int M,
  * (group_by_key/_chunk, grouping.py:83-95,105-122).  keys NULL = natural
  * order (group_natural, grouping.py:98-102).  order [n] out (may be NULL),
  * groups [ceil(n/S)][S] out (indices into the input), pad [ceil(n/S)] out.
- * Synchronises; returns UQG_EINVAL on a non-finite key. */
+ * The sort is a stable LSD radix sort of order-preserving 64-bit key images
+ * (+0.0 and -0.0 tie).  Synchronises; returns UQG_EINVAL on a non-finite key. */
 int uqg_group_sort(uqg_ctx* ctx, const double* keys, int n, int S, int* order, int* groups,
                    int* pad, void* stream);
+/* The same without any host synchronisation (the level pipeline): a
+ * non-finite key sets status bit 1, seen by the caller's next
+ * uqg_status_sync. */
+int uqg_group_sort_async(uqg_ctx* ctx, const double* keys, int n, int S, int* order,
+                         int* groups, int* pad, void* stream);
+/* Clear the device status word, stream-ordered (no host synchronisation). */
+int uqg_status_clear(uqg_ctx* ctx, void* stream);
 
 #ifdef __cplusplus
 }

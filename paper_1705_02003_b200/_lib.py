@@ -58,6 +58,8 @@ SIGNATURES = {
                               _c_double, _c_int, _p, _p, _p, _p, _p, _p, _c_int,
                               ctypes.POINTER(_c_int), _p]),
     "uqg_group_sort": (_c_int, [_p, _p, _c_int, _c_int, _p, _p, _p, _p]),
+    "uqg_group_sort_async": (_c_int, [_p, _p, _c_int, _c_int, _p, _p, _p, _p]),
+    "uqg_status_clear": (_c_int, [_p, _p]),
     "uqg_surrogate_eval": (_c_int, [_p, _p, _c_int, _c_int, _p, _p, _p, _c_int, _p, _p]),
     "uqg_anisotropy_indicator": (_c_int, [_p, _p, _c_int, _c_int, _p, _p, _c_int, _c_double,
                                           _c_int, _c_double, _c_int, _c_double, _c_double, _p,

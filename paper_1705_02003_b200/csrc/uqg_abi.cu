@@ -1,6 +1,7 @@
 // uqg_abi.cu - the C ABI of libuqg.so (include/uqg.h): argument validation,
 // context / workspace management, launch accounting and the host side of the
 // device-resident PCG loop.
+#include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
@@ -940,26 +941,45 @@ int uqg_anisotropy_indicator(uqg_ctx* ctx, const double* modes, int P, int M,
   return UQG_OK;
 }
 
-int uqg_group_sort(uqg_ctx* ctx, const double* keys, int n, int S, int* order, int* groups,
-                   int* pad, void* stream) {
-  UQG_REQUIRE(ctx && groups && pad, "uqg_group_sort: NULL argument");
-  UQG_REQUIRE(n >= 1, "cannot group an empty sample set");
-  UQG_REQUIRE(S >= 1, "ensemble size must be >= 1");
-  cudaStream_t s = as_stream(stream);
-  int st = 0;
-  int rc = uqg_status_sync(ctx, stream, &st);
-  if (rc) return rc;
+}  // extern "C"
+
+namespace {
+
+// Stable ascending sort of the keys (LSD radix sort over the order-preserving
+// 64-bit images, cub::DeviceRadixSort - stable, so equal keys keep generation
+// order) + chunking into width-S groups.  No host synchronisation: a
+// non-finite key sets status bit 1, read by the caller's next status check.
+int group_sort_impl(uqg_ctx* ctx, const double* keys, int n, int S, int* order, int* groups,
+                    int* pad, cudaStream_t s) {
   const int K = (n + S - 1) / S;
   int* ord = order;
   if (keys) {
-    if (!ord) {
-      const size_t need = (size_t)n * sizeof(int) + 256;
-      rc = ensure_ws(ctx, need);
-      if (rc) return rc;
-      ord = (int*)ws_base(ctx, need);
-    }
+    size_t temp = 0;
+    UQG_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, (unsigned long long*)nullptr,
+                                                 (unsigned long long*)nullptr, (int*)nullptr,
+                                                 (int*)nullptr, n, 0, 64, s));
+    Carver probe{nullptr};
+    probe.take<unsigned long long>(n);
+    probe.take<unsigned long long>(n);
+    probe.take<int>(n);
+    probe.take<int>(n);
+    probe.take<char>(temp);
+    const size_t need = probe.off + 256;
+    int rc = ensure_ws(ctx, need);
+    if (rc) return rc;
+    Carver c{(char*)ws_base(ctx, need)};
+    unsigned long long* kin = c.take<unsigned long long>(n);
+    unsigned long long* kout = c.take<unsigned long long>(n);
+    int* ids = c.take<int>(n);
+    int* ord_ws = c.take<int>(n);
+    void* tmp = c.take<char>(temp);
+    if (!ord) ord = ord_ws;
     UQG_LAUNCH(UQG_K_GROUP, s,
-               rank_sort_kernel<<<(n + 255) / 256, 256, 0, s>>>(keys, n, ord, ctx->status_dev));
+               key_bits_kernel<<<(n + 255) / 256, 256, 0, s>>>(keys, n, kin, ids, ctx->status_dev));
+    cudaError_t se = cudaSuccess;  // cub launches its own kernels (counted as one)
+    UQG_LAUNCH(UQG_K_GROUP, s,
+               se = cub::DeviceRadixSort::SortPairs(tmp, temp, kin, kout, ids, ord, n, 0, 64, s));
+    UQG_TRY_CUDA(se);
   } else {
     ord = nullptr;  // natural order
   }
@@ -969,9 +989,41 @@ int uqg_group_sort(uqg_ctx* ctx, const double* keys, int n, int S, int* order, i
   if (!keys && order) {
     UQG_TRY_CUDA(cudaMemcpyAsync(order, groups, (size_t)n * sizeof(int), cudaMemcpyDeviceToDevice, s));
   }
+  return UQG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int uqg_group_sort(uqg_ctx* ctx, const double* keys, int n, int S, int* order, int* groups,
+                   int* pad, void* stream) {
+  UQG_REQUIRE(ctx && groups && pad, "uqg_group_sort: NULL argument");
+  UQG_REQUIRE(n >= 1, "cannot group an empty sample set");
+  UQG_REQUIRE(S >= 1, "ensemble size must be >= 1");
+  cudaStream_t s = as_stream(stream);
+  int st = 0;
+  int rc = uqg_status_sync(ctx, stream, &st);  // clear stale bits
+  if (rc) return rc;
+  rc = group_sort_impl(ctx, keys, n, S, order, groups, pad, s);
+  if (rc) return rc;
   rc = uqg_status_sync(ctx, stream, &st);
   if (rc) return rc;
   UQG_REQUIRE(!(st & 2), "grouping keys must be finite");
+  return UQG_OK;
+}
+
+int uqg_group_sort_async(uqg_ctx* ctx, const double* keys, int n, int S, int* order, int* groups,
+                         int* pad, void* stream) {
+  UQG_REQUIRE(ctx && groups && pad, "uqg_group_sort_async: NULL argument");
+  UQG_REQUIRE(n >= 1, "cannot group an empty sample set");
+  UQG_REQUIRE(S >= 1, "ensemble size must be >= 1");
+  return group_sort_impl(ctx, keys, n, S, order, groups, pad, as_stream(stream));
+}
+
+int uqg_status_clear(uqg_ctx* ctx, void* stream) {
+  UQG_REQUIRE(ctx, "uqg_status_clear: NULL ctx");
+  UQG_TRY_CUDA(cudaMemsetAsync(ctx->status_dev, 0, sizeof(int), as_stream(stream)));
   return UQG_OK;
 }
 

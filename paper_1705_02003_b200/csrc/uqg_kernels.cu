@@ -312,29 +312,20 @@ __global__ void assemble_fem3d_kernel(int m, int G, int S, const double* __restr
 // ===========================================================================
 // Grouping: stable rank sort + chunk/pad (grouping.py:83-122)
 
-// rank_i = #{j : k_j < k_i or (k_j == k_i and j < i)}; order[rank_i] = i.
-// IEEE comparisons already treat -0.0 == +0.0, as numpy's stable argsort does.
-__global__ void rank_sort_kernel(const double* __restrict__ keys, int n, int* __restrict__ order,
-                                 int* status) {
-  __shared__ double tile[1024];
+// Order-preserving 64-bit image of each key for the stable radix sort:
+// +0.0 and -0.0 map to the same bits (numpy's stable argsort ties them and
+// keeps generation order), negatives flip every bit, non-negatives flip the
+// sign bit; ids[i] = i is the payload.  A non-finite key sets status bit 1.
+__global__ void key_bits_kernel(const double* __restrict__ keys, int n,
+                                unsigned long long* __restrict__ bits, int* __restrict__ ids,
+                                int* status) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const double ki = i < n ? keys[i] : 0.0;
-  if (i < n && !isfinite(ki)) atomicOr(status, 2);
-  int rank = 0;
-  for (int base = 0; base < n; base += 1024) {
-    __syncthreads();
-    for (int q = threadIdx.x; q < 1024; q += blockDim.x)
-      tile[q] = base + q < n ? keys[base + q] : 0.0;
-    __syncthreads();
-    const int lim = min(1024, n - base);
-    if (i < n) {
-      for (int q = 0; q < lim; ++q) {
-        const double kj = tile[q];
-        rank += (kj < ki) || (kj == ki && base + q < i);
-      }
-    }
-  }
-  if (i < n) order[rank] = i;
+  if (i >= n) return;
+  const double k = keys[i];
+  if (!isfinite(k)) atomicOr(status, 2);
+  const unsigned long long b = k == 0.0 ? 0ull : (unsigned long long)__double_as_longlong(k);
+  bits[i] = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+  ids[i] = i;
 }
 
 __global__ void chunk_kernel(const int* __restrict__ order, int n, int S, int K,

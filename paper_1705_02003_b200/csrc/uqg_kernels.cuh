@@ -152,7 +152,8 @@ __global__ void kl_sep3d_kernel(int m, const double* qtab, const int* mode_p, co
 __global__ void assemble_fem3d_kernel(int m, int G, int S, const double* a_q, const double* dx_tab,
                                       const double* kyz_tab, const int* row_offsets, double* vals,
                                       double* dinv);
-__global__ void rank_sort_kernel(const double* keys, int n, int* order, int* status);
+__global__ void key_bits_kernel(const double* keys, int n, unsigned long long* bits, int* ids,
+                                int* status);
 __global__ void chunk_kernel(const int* order, int n, int S, int K, int* groups, int* pad);
 
 // uqg_pcg.cu: launchers of the V-templated streaming kernels

@@ -193,9 +193,10 @@ class IdentityPreconditioner:
 class JacobiPreconditioner:
     """z = D^-1 r per lane (``ensemble.py:169-176``); keeps a device copy."""
 
-    def __init__(self, inv_diag, _dev=None):
+    def __init__(self, inv_diag, _dev=None, _shape=None):
         self._host = None if inv_diag is None else np.asarray(inv_diag, dtype=np.float64)
         self._dev = _dev  # [n][S] device tensor
+        self._shape = _shape if _dev is not None else None  # (S, n) of the device copy
 
     @property
     def inv_diag(self) -> np.ndarray:
@@ -205,8 +206,15 @@ class JacobiPreconditioner:
         return self._host
 
     def device(self, width: int, n: int):
+        """The [n][S] device copy for a (width, n) solve.  A preconditioner
+        reused with another system shape raises ``EnsembleError`` (the
+        reference's numpy broadcast fails there too) instead of letting the
+        solver read past the copy."""
         if self._dev is None:
             self._dev = _lib.lanes_to_dev(_check_vector(width, n, self._host, "inv_diag"))
+            self._shape = (width, n)
+        if self._shape != (width, n):
+            raise EnsembleError(f"inv_diag has shape {self._shape}, expected {(width, n)}")
         return self._dev
 
     def apply(self, r):
@@ -222,9 +230,7 @@ def jacobi_precond(mat: EnsembleCsrMatrix) -> JacobiPreconditioner:
     d = vals.new_empty((mat.n_rows * mat.width,))
     _lib.call("uqg_jacobi_dinv", _lib.ctx(), mat.n_rows, mat.nnz, mat.width, 1, _lib.ptr(ro),
               _lib.ptr(ci), _lib.ptr(vals), _lib.ptr(d), _lib.stream())
-    pre = JacobiPreconditioner(None, d)
-    pre._shape = (mat.width, mat.n_rows)
-    return pre
+    return JacobiPreconditioner(None, d, (mat.width, mat.n_rows))
 
 
 class LaneSolveResult:

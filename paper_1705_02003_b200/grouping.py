@@ -4,12 +4,14 @@
 * ``group_natural`` <- ``grouping.py:98-102``;
 * ``group_by_key``  <- ``grouping.py:105-122``: the stable ascending key sort
   and the width-S chunking with last-group replica padding run on the device
-  (``uqg_group_sort``); sample ids may be any hashable objects, the device
+  (``uqg_group_sort``: a stable LSD radix sort of order-preserving 64-bit key
+  images, O(n) per level); sample ids may be any hashable objects, the device
   works on their generation-order indices.
 
-The post-hoc accounting (``compute_R``, ``group_oracle``,
-``predicted_speedup``) is out of scope for the device and lives
-in ``accounting.py`` as host code.
+The reference's post-hoc accounting (``compute_R``, ``group_oracle``,
+``predicted_speedup``, ``grouping.py:125-260``) is not on the hot path and is
+not rebuilt here; the reference's own functions
+accept these plans unchanged (``tests/test_ref_conformance.py``).
 """
 
 from __future__ import annotations
@@ -61,11 +63,14 @@ class GroupingPlan:
         return out
 
 
-def device_group(n: int, size: int, d_keys=None):
+def device_group(n: int, size: int, d_keys=None, sync: bool = True):
     """Device sort + chunk of n generation-order indices.
 
     Returns device int32 tensors (groups [K*size], padding [K]); ``d_keys``
-    (float64 device tensor [n]) or None for natural order.
+    (float64 device tensor [n]) or None for natural order.  ``sync=False``
+    (the level pipeline) never waits for the device: a non-finite key sets
+    status bit 1, which the caller's next status check turns into
+    ``GroupingError``.
     """
     if size < 1:
         raise GroupingError(f"ensemble size must be >= 1, got {size}")
@@ -75,8 +80,9 @@ def device_group(n: int, size: int, d_keys=None):
     K = (n + size - 1) // size
     groups = torch.empty((K * size,), dtype=torch.int32, device=_lib.device())
     pad = torch.empty((K,), dtype=torch.int32, device=_lib.device())
-    _lib.call("uqg_group_sort", _lib.ctx(), _lib.ptr(d_keys), n, size, None, _lib.ptr(groups),
-              _lib.ptr(pad), _lib.stream(), invalid=GroupingError)
+    _lib.call("uqg_group_sort" if sync else "uqg_group_sort_async", _lib.ctx(), _lib.ptr(d_keys),
+              n, size, None, _lib.ptr(groups), _lib.ptr(pad), _lib.stream(),
+              invalid=GroupingError)
     return groups, pad
 
 

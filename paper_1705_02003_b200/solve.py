@@ -150,6 +150,7 @@ class EnsembleSolver:
         self._bufs = {}
         self._pins = {}
         self._ws = None
+        self._waves = {}
 
     # -- memory planning ----------------------------------------------------
     def bytes_per_group(self, S: int) -> int:
@@ -160,14 +161,21 @@ class EnsembleSolver:
         return int(per)
 
     def wave_size(self, S: int, K: int) -> int:
-        torch = _lib._torch()
-        free, _ = torch.cuda.mem_get_info()
-        held = sum(t.numel() * t.element_size() for t in self._bufs.values())
-        held += 0 if self._ws is None else self._ws.numel()
-        budget = (free + held) * self.mem_fraction
-        g = max(1, int(budget // self.bytes_per_group(S)))
-        if self.max_groups_per_wave:
-            g = min(g, self.max_groups_per_wave)
+        """Groups per device wave: as many as fit in ``mem_fraction`` of the
+        HBM this solver can use (free + what it already holds).  Measured
+        once per ensemble width (``torch.cuda.mem_get_info`` is a device
+        query); ``release()`` forgets it."""
+        g = self._waves.get(S)
+        if g is None:
+            torch = _lib._torch()
+            free, _ = torch.cuda.mem_get_info()
+            held = sum(t.numel() * t.element_size() for t in self._bufs.values())
+            held += 0 if self._ws is None else self._ws.numel()
+            budget = (free + held) * self.mem_fraction
+            g = max(1, int(budget // self.bytes_per_group(S)))
+            if self.max_groups_per_wave:
+                g = min(g, self.max_groups_per_wave)
+            self._waves[S] = g
         return min(g, K)
 
     def _pinned(self, name, n):
@@ -207,20 +215,40 @@ class EnsembleSolver:
 
     def release(self):
         self._bufs.clear()
+        self._waves.clear()
         if self._ws is not None:
             _lib.call("uqg_ctx_set_workspace", _lib.ctx(), None, 0)
             self._ws = None
 
     # -- solve --------------------------------------------------------------
-    def solve_wave(self, d_samples, G: int, S: int, record_history: bool = False, lane_ids=None):
+    def _check_inputs(self):
+        """The one host synchronisation before a wave's PCG: the reference
+        rejects a non-positive coefficient in ``assemble`` before any solve
+        (``fem3d.py:153-154``) and a non-finite key in ``group_by_key``
+        (``grouping.py:115-120``); the device status word carries both."""
+        from .errors import GroupingError
+
+        st = _lib.status_sync()
+        if st & 2:
+            raise GroupingError("grouping keys must be finite")
+        if st & 1:
+            raise FemError("non-positive diffusion coefficient at a mesh node")
+
+    def solve_wave(self, d_samples, G: int, S: int, record_history: bool = False, lane_ids=None,
+                   clear_status: bool = True):
         """One batched launch set over G groups; samples already on the device.
 
         ``lane_ids`` (device int32 [G*S]) maps lanes to rows of ``d_samples``
         (the device grouping plan); None = rows in lane order.
+        ``clear_status=False``: the caller cleared the device status word
+        itself and queued work whose bits must reach this wave's check (the
+        level pipeline's device grouping).
         Returns device tensors (iters, conv, frozen, ens, qoi, hist, x).
         """
         torch = _lib._torch()
         o = self.op
+        if clear_status:
+            _lib.call("uqg_status_clear", _lib.ctx(), _lib.stream())
         a = self._buf("a", G * o.n_coef * S, torch.float64)
         dinv = self._buf("dinv", G * o.n_dofs * S, torch.float64)
         o.coefficients(d_samples, lane_ids, G, S, a)
@@ -229,6 +257,7 @@ class EnsembleSolver:
             tx = self._buf("vals", G * F * S, torch.float64)
             ty = self._buf("ty", G * F * S, torch.float64) if o.a2 == "same" else None
             o.assemble_faces(a, G, S, tx, ty, dinv)
+            self._check_inputs()
             with self._workspace(G, S):
                 x, iters, conv, frz, ens, hist = run_pcg_fv2d(
                     o.mesh.cells, S, G, tx, ty, o.field.a_y, None, o.rhs_const, dinv, self.tol,
@@ -236,6 +265,7 @@ class EnsembleSolver:
                 return self._finish(x, iters, conv, frz, ens, hist, G, S)
         vals = self._buf("vals", G * o.nnz * S, torch.float64)
         o.assemble(a, G, S, vals, dinv)
+        self._check_inputs()
         rowptr, col = o.graph()
         # banded-graph hint: the SpMV bulk-prefetches each tile's p bands into L2
         # (UQG_SPMV_TMA=3 stages them in shared memory instead); UQG_BAND_HINT=0
@@ -263,8 +293,6 @@ class EnsembleSolver:
         q = torch.empty((G * S,), dtype=torch.float64, device=_lib.device())
         _lib.call("uqg_lane_dot", _lib.ctx(), o.n_dofs, S, G, _lib.ptr(x), _lib.ptr(x), _lib.ptr(q),
                   _lib.stream())
-        if _lib.status_sync() & 1:
-            raise FemError("non-positive diffusion coefficient at a mesh node")
         return iters, conv, frz, ens, q, hist, x
 
     def solve_groups(self, samples, record_history: bool = False) -> LevelSolveResult:
@@ -303,35 +331,55 @@ class EnsembleSolver:
                                 cat["fz"].astype(bool), cat["en"].astype(int), cat["q"], hists,
                                 waves)
 
-    def run_level_device(self, d_coords, n: int, S: int, d_keys=None):
-        """The whole level on the device: group (sort + chunk) -> KL -> assemble
-        -> PCG -> QoI.  ``d_coords`` [n][M] and ``d_keys`` [n] (None = natural
-        order) are device tensors; returns device tensors
-        (groups [K*S], padding [K], iters [K*S], conv [K*S], ens [K], qoi [K*S]).
-        """
+    def run_groups_device(self, d_coords, lane_ids, G: int, S: int, clear_status: bool = True):
+        """Solve G groups whose lanes read rows ``lane_ids`` [G*S] of the
+        device samples ``d_coords`` [n][M], in waves that fit in HBM; returns
+        device (iters [G*S], conv [G*S], ens [G], qoi [G*S])."""
         torch = _lib._torch()
-        from .grouping import device_group
-
-        groups, pad = device_group(n, S, d_keys)
-        K = pad.numel()
-        gw = self.wave_size(S, K)
+        gw = self.wave_size(S, G)
         parts = {k: [] for k in ("it", "cv", "en", "q")}
-        for k0 in range(0, K, gw):
-            g = min(gw, K - k0)
+        for k0 in range(0, G, gw):
+            g = min(gw, G - k0)
             it, cv, _, en, q, _, _ = self.solve_wave(d_coords, g, S,
-                                                     lane_ids=groups[k0 * S:(k0 + g) * S])
+                                                     lane_ids=lane_ids[k0 * S:(k0 + g) * S],
+                                                     clear_status=clear_status and k0 == 0)
             parts["it"].append(it)
             parts["cv"].append(cv)
             parts["en"].append(en)
             parts["q"].append(q)
         cat = {k: (v[0] if len(v) == 1 else torch.cat(v)) for k, v in parts.items()}
-        return groups, pad, cat["it"], cat["cv"], cat["en"], cat["q"]
+        return cat["it"], cat["cv"], cat["en"], cat["q"]
 
-    def solve_level(self, ids, coords, size: int, keys=None, level: int = 1, tag: str = "sur"):
+    def run_level_device(self, d_coords, n: int, S: int, d_keys=None, shard=None):
+        """The whole level on the device: group (sort + chunk) -> KL -> assemble
+        -> PCG -> QoI.  ``d_coords`` [n][M] and ``d_keys`` [n] (None = natural
+        order) are device tensors; returns device tensors
+        (groups [K*S], padding [K], iters [K*S], conv [K*S], ens [K], qoi [K*S]).
+
+        ``shard`` (``dist.LevelShard``, world > 1): this rank solves its
+        round-robin share of the plan's groups and one allgather returns the
+        whole level's results on every rank.
+        """
+        from .grouping import device_group
+
+        _lib.call("uqg_status_clear", _lib.ctx(), _lib.stream())
+        groups, pad = device_group(n, S, d_keys, sync=False)
+        K = pad.numel()
+        if shard is None or shard.world == 1:
+            it, cv, en, q = self.run_groups_device(d_coords, groups, K, S, clear_status=False)
+        else:
+            it, cv, en, q = shard.solve(
+                lambda lanes, g: self.run_groups_device(d_coords, lanes, g, S, clear_status=False),
+                groups, K, S)
+        return groups, pad, it, cv, en, q
+
+    def solve_level(self, ids, coords, size: int, keys=None, level: int = 1, tag: str = "sur",
+                    shard=None):
         """Public end-to-end entry: host ids / coords (n, M) / keys (n,) in,
         grouping plan and per-sample results out - ``group_by_key`` (or
         ``group_natural`` when ``keys`` is None) fused with ``solve_plan`` on
         the device.  Returns (plan, iters dict, qois dict, notes).
+        ``shard``: ``dist.LevelShard`` for a multi-GPU level (same results).
         """
         from .grouping import GroupingPlan
 
@@ -352,7 +400,7 @@ class EnsembleSolver:
         if keys is not None:
             stage[n * M:].copy_(torch.from_numpy(np.ascontiguousarray(keys, dtype=np.float64)))
             d_k = stage[n * M:].to(dev, non_blocking=True)
-        groups, pad, it, cv, en, q = self.run_level_device(d_c, n, size, d_k)
+        groups, pad, it, cv, en, q = self.run_level_device(d_c, n, size, d_k, shard)
         d_out = torch.cat([groups.double(), pad.double(), it.double(), cv.double(), q])
         h_out = self._pinned("out", d_out.numel())
         h_out.copy_(d_out, non_blocking=True)

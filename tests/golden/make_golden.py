@@ -125,7 +125,48 @@ def eigen_cases():
     np.savez_compressed(HERE / "eigen.npz", **out)
 
 
-def reference_study(cfg, max_levels=None):
+# ---------------------------------------------------------------------------
+# parallel per-group solves (the reference's ensemble_pcg, one group per
+# process, 1 BLAS thread): the study loop itself stays sequential
+
+_POOL_STATE = {}
+
+
+def _pool_init(cfg_name):
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(limits=1)
+    cfg = CONFIGS[cfg_name]
+    fld = field2d.KL2D.select(**cfg.field_kwargs())
+    mesh = fv2d.Mesh2D(cfg.cells)
+    _POOL_STATE.update(cfg=cfg, fld=fld, mesh=mesh, table=fld.mode_table(mesh.node_points))
+
+
+def _solve_group_ref(args):
+    """One group through the reference's own ensemble_pcg on the oracle 2D
+    operator: (per-lane iterations, converged, QoI, ensemble iterations)."""
+    ys, maxit, keep = args
+    st = _POOL_STATE
+    cfg = st["cfg"]
+    sysm = fv2d.assemble(st["mesh"], st["fld"], np.asarray(ys), st["table"], cfg.a2)
+    mat = ref_ens.EnsembleCsrMatrix(sysm.row_offsets, sysm.col_indices, sysm.values)
+    res = ref_ens.ensemble_pcg(mat, sysm.rhs, tol=cfg.tol, maxit=cfg.maxit if maxit is None else maxit,
+                               record_history=keep)
+    out = {"iterations": res.iterations_per_lane.tolist(),
+           "converged": res.converged_per_lane.tolist(),
+           "qoi": [float(np.dot(u, u)) for u in res.solution],
+           "ensemble_iterations": int(res.ensemble_iterations)}
+    if keep:
+        out["history"] = np.array(res.residual_history)
+        out["solution"] = res.solution
+    return out
+
+
+def _pool(cfg_name, procs):
+    import multiprocessing as mp
+    return mp.get_context("fork").Pool(procs, initializer=_pool_init, initargs=(cfg_name,))
+
+
+def reference_study(cfg, max_levels=None, pool=None):
     """The reference's adaptive loop (harness.py:604-701, exec plan 'sur') on the 2D operator."""
     fld = field2d.KL2D.select(**{k: v for k, v in cfg.field_kwargs().items()})
     mesh = fv2d.Mesh2D(cfg.cells)
@@ -150,16 +191,26 @@ def reference_study(cfg, max_levels=None):
             plan = ref_grp.group_by_key(ids, {sid: float(predicted[i]) for i, sid in enumerate(ids)},
                                         S, level, "sur")
         iters, qois, ens_iters = {}, {}, []
-        for group in plan.ensembles:
-            ys = np.array([coords_by_id[sid] for sid in group])
-            sysm = fv2d.assemble(mesh, fld, ys, table, cfg.a2)
-            mat = ref_ens.EnsembleCsrMatrix(sysm.row_offsets, sysm.col_indices, sysm.values)
-            res = ref_ens.ensemble_pcg(mat, sysm.rhs, tol=cfg.tol, maxit=cfg.maxit)
-            ens_iters.append(int(res.ensemble_iterations))
+        if pool is None:
+            results = []
+            for group in plan.ensembles:
+                ys = np.array([coords_by_id[sid] for sid in group])
+                sysm = fv2d.assemble(mesh, fld, ys, table, cfg.a2)
+                mat = ref_ens.EnsembleCsrMatrix(sysm.row_offsets, sysm.col_indices, sysm.values)
+                res = ref_ens.ensemble_pcg(mat, sysm.rhs, tol=cfg.tol, maxit=cfg.maxit)
+                results.append({"iterations": res.iterations_per_lane.tolist(),
+                                "ensemble_iterations": int(res.ensemble_iterations),
+                                "qoi": [float(np.dot(u, u)) for u in res.solution]})
+        else:
+            results = pool.map(_solve_group_ref,
+                               [(np.array([coords_by_id[sid] for sid in g]), None, False)
+                                for g in plan.ensembles], chunksize=1)
+        for group, res in zip(plan.ensembles, results):
+            ens_iters.append(int(res["ensemble_iterations"]))
             for s, sid in enumerate(group):
                 if sid not in iters:
-                    iters[sid] = int(res.iterations_per_lane[s])
-                    qois[sid] = float(np.dot(res.solution[s], res.solution[s]))
+                    iters[sid] = int(res["iterations"][s])
+                    qois[sid] = float(res["qoi"][s])
         nodes = grid.nodes[start:]
         grid.compute_surpluses("qoi", {nd: qois[sid] for nd, sid in zip(nodes, ids)})
         grid.compute_surpluses("iterations", {nd: iters[sid] for nd, sid in zip(nodes, ids)})
@@ -311,6 +362,73 @@ def c2_group():
     (HERE / "c2_group.json").write_text(json.dumps(doc))
 
 
+def c2_study(procs=6):
+    """The full C2 adaptive study (every level, every group) through the
+    reference's own loop pieces - the bench's C2 workload is its last level."""
+    with _pool("C2", procs) as pool:
+        doc = reference_study(CONFIGS["C2"], pool=pool)
+    (HERE / "c2_adaptive.json").write_text(json.dumps(doc))
+
+
+def _workload(name):
+    z = np.load(REPO / "bench_workloads" / f"{name}.npz")
+    keys = z["keys"] if z["keys"].size else None
+    return [int(i) for i in z["ids"]], np.asarray(z["coords"]), keys
+
+
+def c3_level(procs=6):
+    """Every group of the C3 bench workload (the study's final level: samples +
+    surrogate keys, bench_workloads/C3.npz) grouped by the reference's
+    group_by_key and solved to convergence by the reference's ensemble_pcg on
+    the oracle 2D operator.  One mid-cost group also keeps its residual history."""
+    cfg = CONFIGS["C3"]
+    ids, coords, keys = _workload("C3")
+    plan = ref_grp.group_by_key(ids, {sid: float(k) for sid, k in zip(ids, keys)},
+                                cfg.ensemble_size, 5, "sur")
+    row = {sid: i for i, sid in enumerate(ids)}
+    K = len(plan.ensembles)
+    keep = K // 2
+    import time
+    t0 = time.time()
+    with _pool("C3", procs) as pool:
+        res = pool.map(_solve_group_ref,
+                       [(coords[[row[s] for s in g]], None, k == keep)
+                        for k, g in enumerate(plan.ensembles)], chunksize=1)
+    hist = res[keep].pop("history")
+    sol = res[keep].pop("solution")
+    doc = {"config": cfg.to_dict(), "workload": "bench_workloads/C3.npz",
+           "ensembles": [list(g) for g in plan.ensembles], "padding": list(plan.padding),
+           "groups": res, "history_group": keep,
+           "cpu_seconds_wall": time.time() - t0, "procs": procs}
+    (HERE / "c3_level.json").write_text(json.dumps(doc))
+    idx = np.arange(0, sol.shape[1], 997)
+    np.savez_compressed(HERE / "c3_history.npz", history=hist, group=keep, idx=idx,
+                        x_idx=sol[:, idx], x_norm2=np.einsum("ij,ij->i", sol, sol))
+
+
+def fixed_iterations(name, maxit=30):
+    """The first group of the C4 / C5 bench workload, exactly `maxit` PCG
+    iterations of the reference's ensemble_pcg: residual history, and x through
+    per-lane x.x plus x at every 997th unknown."""
+    cfg = CONFIGS[name]
+    ids, coords, keys = _workload(name)
+    S = cfg.ensemble_size
+    if keys is None:
+        plan = ref_grp.group_natural(ids, S, 1, "nat")
+    else:
+        plan = ref_grp.group_by_key(ids, {sid: float(k) for sid, k in zip(ids, keys)}, S, 2, "sur")
+    row = {sid: i for i, sid in enumerate(ids)}
+    g = plan.ensembles[0]
+    _pool_init(name)
+    out = _solve_group_ref((coords[[row[s] for s in g]], maxit, True))
+    sol = out["solution"]
+    idx = np.arange(0, sol.shape[1], 997)
+    np.savez_compressed(HERE / f"{name.lower()}_fixed.npz", group=np.array(list(g)),
+                        maxit=np.array(maxit), history=out["history"],
+                        iterations=np.array(out["iterations"]), idx=idx, x_idx=sol[:, idx],
+                        x_norm2=np.einsum("ij,ij->i", sol, sol))
+
+
 def fv2d_small():
     fld = field2d.KL2D.select(0.2, 1.0, 3, 0.0)
     mesh = fv2d.Mesh2D(8)
@@ -369,6 +487,13 @@ if __name__ == "__main__":
         (HERE / "c1_adaptive.json").write_text(json.dumps(doc))
     if "c2" in which:
         c2_group()
+    if "c2study" in which:
+        c2_study()
+    if "c3level" in which:
+        c3_level()
+    for nm in ("C4", "C5"):
+        if nm.lower() + "fixed" in which:
+            fixed_iterations(nm)
     if "refrun" in which:
         refrun_outputs()
     if "fem3d" in which:

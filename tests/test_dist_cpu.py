@@ -105,3 +105,71 @@ def test_round_robin_covers_all_groups_once():
         for W in (1, 2, 4, 8):
             seen = sorted(k for r in range(W) for k in my_groups(K, r, W))
             assert seen == list(range(K))
+
+
+# ---------------------------------------------------------------------------
+# LevelShard: the bench's strong-scaling step (device-resident plan, one
+# all_gather_into_tensor) with a deterministic stand-in for the GPU solve
+
+def _fake_solve_tensors(coords_t, S):
+    import torch
+
+    def solve(lanes, g):
+        y = coords_t[lanes.long()]                       # [g*S, M]
+        it = (y.abs().sum(dim=1) * 100).to(torch.int32) + 1
+        q = (y ** 2).sum(dim=1)
+        cv = it < 250
+        en = it.view(g, S).max(dim=1).values
+        return it, cv, en, q
+    return solve
+
+
+def _level_worker(rank, world, port, n, S, M, q):
+    import torch
+
+    from paper_1705_02003_b200.dist import LevelShard
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(1)
+        coords = torch.from_numpy(rng.uniform(-1, 1, (n, M)))
+        K = -(-n // S)
+        order = torch.from_numpy(rng.permutation(n)).to(torch.int32)
+        groups = torch.cat([order, order[-1:].repeat(K * S - n)])   # a plan with padding
+        sh = LevelShard.from_env()
+        it, cv, en, qq = sh.solve(_fake_solve_tensors(coords, S), groups, K, S)
+        q.put((rank, it.tolist(), cv.tolist(), en.tolist(), qq.tolist(), sh.last_load))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,S,world", [(37, 8, 2), (5, 4, 2), (130, 16, 3)])
+def test_level_shard_equals_single_rank(n, S, world):
+    import torch
+
+    from paper_1705_02003_b200.dist import LevelShard
+
+    M = 3
+    rng = np.random.default_rng(1)
+    coords = torch.from_numpy(rng.uniform(-1, 1, (n, M)))
+    K = -(-n // S)
+    order = torch.from_numpy(rng.permutation(n)).to(torch.int32)
+    groups = torch.cat([order, order[-1:].repeat(K * S - n)])
+    want = LevelShard(0, 1).solve(_fake_solve_tensors(coords, S), groups, K, S)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_level_worker, args=(r, world, port, n, S, M, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, it, cv, en, qq, load in got:
+        assert it == want[0].tolist() and cv == want[1].tolist()
+        assert en == want[2].tolist() and qq == want[3].tolist()   # bitwise
+        assert load["groups"] == [len(my_groups(K, r, world)) for r in range(world)]
+        assert sum(load["group_iterations"]) == int(want[2].sum())

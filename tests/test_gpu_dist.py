@@ -1,6 +1,7 @@
 """Multi-rank path on the GPU box: the C1 study with each level's groups sharded
 over 2 ranks (one allgather per level) reproduces the single-rank reference
-golden; and `bench.py` runs under torchrun with N=2.  Both ranks share cuda:0
+golden; one bench level sharded over 2 ranks (the strong-scaling bench step)
+is bit-identical to one rank; and `bench.py` runs under torchrun with N=2.  Both ranks share cuda:0
 with gloo (UQG_BENCH_SHARE_GPU=1) because the box has one GPU; no rank's
 kernels wait on another's, so this is safe."""
 
@@ -44,6 +45,34 @@ def test_sharded_study_matches_single_rank_golden(tmp_path, c1_golden):
         assert max(abs(a - b) / abs(b) for a, b in zip(got["qoi"], gold["qoi"])) <= 1e-8
 
 
+def test_sharded_level_bitwise_equals_single_rank(tmp_path):
+    """The bench's strong-scaling step (LevelShard over 2 ranks) returns the
+    whole level bit-identical to one rank's run_level_device."""
+    import numpy as np
+    import torch
+
+    from paper_1705_02003_b200.configs import get
+
+    out = tmp_path / "lvl.json"
+    r = _torchrun([str(ROOT / "tools" / "dist_level.py"), "--config", "C1", "--out", str(out)], {})
+    assert r.returncode == 0, r.stderr[-3000:]
+    doc = json.loads(out.read_text())
+    assert doc["world"] == 2
+    cfg = get("C1")
+    z = np.load(ROOT / "bench_workloads" / "C1.npz")
+    solver = cfg.make_solver()
+    dev = torch.device("cuda", 0)
+    groups, pad, it, cv, en, q = solver.run_level_device(
+        torch.from_numpy(z["coords"]).to(dev), len(z["coords"]), cfg.ensemble_size,
+        torch.from_numpy(z["keys"]).to(dev))
+    assert doc["groups"] == groups.tolist()
+    assert doc["iters"] == it.tolist() and doc["conv"] == cv.tolist()
+    assert doc["ens"] == en.tolist()
+    assert doc["qoi"] == q.tolist()  # bitwise
+    K = pad.numel()
+    assert doc["load"]["groups"] == [len(range(0, K, 2)), len(range(1, K, 2))]
+
+
 def test_bench_runs_with_two_ranks():
     r = _torchrun([str(ROOT / "bench.py"), "--gpus", "2", "--config", "C1", "--steps", "2",
                    "--warmup", "3"], {})
@@ -51,4 +80,14 @@ def test_bench_runs_with_two_ranks():
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1
     d = json.loads(lines[0])
-    assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "strong"
+    assert sum(d["shards"]["groups_per_rank"]) == 22  # the C1 level's groups, split over 2
+    assert d["parity"]["ok"], d["parity"]
+
+
+def test_bench_weak_scaling_opt_in():
+    r = _torchrun([str(ROOT / "bench.py"), "--gpus", "2", "--config", "C1", "--steps", "2",
+                   "--warmup", "3", "--scaling", "weak"], {})
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
+    assert d["scaling"] == "weak" and d["value"] > 0
