@@ -104,6 +104,11 @@ def bytes_model(cfg, op=None, kx=1):
     else:
         direction = 6 * 8 * S * N   # read x, p, r, dinv; write x, p (x += alpha p deferred here)
     return {"spmv": spmv, "update": update, "dir": direction,
+            # kx > 1, per kernel: pcg_dir_kernel reads p, r, dinv and writes p
+            # every iteration; pcg_flush_kernel reads each iteration's p once and
+            # reads + writes x once per flush launch
+            "dir_only": (4 if kx > 1 else 6) * 8 * S * N,
+            "flush_p": 8 * S * N, "flush_x": 16 * S * N,
             # SURVEY 8d's algorithmic bytes per PCG iteration (13 vector passes) and
             # the bytes this implementation actually moves (12 passes)
             "pcg_iter": 8 * S * (n_op + 13 * N) + graph,
@@ -586,7 +591,7 @@ def main():
     torch.cuda.synchronize()
 
     import ctypes
-    NK = 10
+    NK = 11  # UQG_NKERN
 
     def timed(profile: bool, steps: int):
         """`steps` timed steps; per-launch CUDA-event kernel timing when `profile`."""
@@ -595,7 +600,8 @@ def main():
         lib.uqg_ctx_profile_read(ctx, ms, cnt, 1)
         lib.uqg_ctx_profile(ctx, int(profile))
         launches0 = lib.uqg_ctx_launch_count(ctx)
-        times, local_iters, last = [], 0, None
+        times, local_iters, local_flush, last = [], 0, 0, None
+        kx = max(1, int(lib.uqg_pcg_x_defer()))
         with ClockSampler(torch.cuda.current_device()) as clocks:
             for _ in range(steps):
                 barrier()
@@ -612,23 +618,25 @@ def main():
                     t = float(tt.item())
                 times.append(t)
                 # this rank's group-iterations (its own kernels' work)
-                local_iters += int(last[4][mine].sum().item())
+                en_mine = last[4][mine].long()
+                local_iters += int(en_mine.sum().item())
+                local_flush += int(((en_mine + kx - 1) // kx).sum().item())
                 barrier()
         launches = lib.uqg_ctx_launch_count(ctx) - launches0
         lib.uqg_ctx_profile_read(ctx, ms, cnt, 1)
         lib.uqg_ctx_profile(ctx, 0)
-        return times, local_iters, launches, ms, cnt, clocks, last
+        return times, local_iters, local_flush, launches, ms, cnt, clocks, last
 
     # value from un-instrumented steps (the library solves a level's groups as
     # concurrent parts on several streams); the per-kernel times for the
     # roofline from an identical profiled pass on ONE stream, so each launch's
     # duration is that kernel's alone (UQG_SOLVE_STREAMS=1; same results).
-    times, local_iters, launches, _, _, clocks, last = timed(False, args.steps)
+    times, local_iters, _, launches, _, _, clocks, last = timed(False, args.steps)
     prev = os.environ.get("UQG_SOLVE_STREAMS")
     os.environ["UQG_SOLVE_STREAMS"] = "1"
     try:
         prof_steps = max(1, min(args.prof_steps, args.steps))
-        _, prof_iters, _, ms, cnt, _, _ = timed(True, prof_steps)
+        _, prof_iters, prof_flush, _, ms, cnt, _, _ = timed(True, prof_steps)
     finally:
         if prev is None:
             os.environ.pop("UQG_SOLVE_STREAMS", None)
@@ -685,15 +693,20 @@ def main():
     # kernel with the largest measured time share (the dominant kernel)
     spmv_name = "pcg_spmv_fv2d_kernel" if bm["operator"] != "csr" else "pcg_spmv_tma_kernel"
     per = {}
-    for key, idx, kname in (("spmv", 3, spmv_name), ("update", 4, "pcg_update_kernel"),
-                            ("dir", 5, "pcg_dir_kernel + pcg_flush_kernel" if "flush" in bm
-                             else "pcg_dir_kernel")):
+    kernels = [("spmv", 3, spmv_name, prof_iters, prof_iters * bm["spmv"]),
+               ("update", 4, "pcg_update_kernel", prof_iters, prof_iters * bm["update"]),
+               ("dir", 5, "pcg_dir_kernel", prof_iters, prof_iters * bm["dir_only"])]
+    if "flush" in bm:
+        kernels.append(("flush", 10, "pcg_flush_kernel", prof_flush,
+                        prof_iters * bm["flush_p"] + prof_flush * bm["flush_x"]))
+    for key, idx, kname, glaunch, nbytes in kernels:
         t_ms = ms[idx]
-        gbs = prof_iters * bm[key] / (t_ms / 1e3) / 1e9 if t_ms else None
+        gbs = nbytes / (t_ms / 1e3) / 1e9 if t_ms else None
         tr = traffic_all.get(f"{cfg.name}:{kname}", {})
         per[key] = {"kernel": kname, "ms": t_ms, "achieved": gbs,
                     "frac": gbs / peak if gbs else None,
-                    "bytes_per_group_launch": bm[key],
+                    "group_launches": glaunch,
+                    "bytes_per_group_launch": nbytes / glaunch if glaunch else None,
                     "traffic": tr.get("dram_bytes_per_launch"),
                     "traffic_algorithmic_same_launch": tr.get("algorithmic_bytes_per_launch"),
                     "traffic_source": tr.get("source")}
@@ -714,12 +727,12 @@ def main():
             "traffic_algorithmic_same_launch": tr.get("algorithmic_bytes_per_launch"),
             "traffic_source": tr.get("source")}}
     dom = max(per, key=lambda k: per[k]["ms"] or 0.0)
-    loop_ms = ms[3] + ms[4] + ms[5]
+    loop_ms = ms[3] + ms[4] + ms[5] + ms[10]
     loop_gbs = prof_iters * bm["pcg_iter"] / (loop_ms / 1e3) / 1e9 if loop_ms else None
     step_gbs = local_iters * bm["pcg_iter"] / (total_ms / 1e3) / 1e9
     kern = {name: {"ms": ms[k], "launches": int(cnt[k])} for k, name in enumerate(
         ["kl", "assemble", "pcg_init", "pcg_spmv", "pcg_update", "pcg_dir", "dot_qoi", "group",
-         "spmv", "other"]) if cnt[k]}
+         "spmv", "other", "pcg_flush"]) if cnt[k]}
     all_ms = sum(ms[k] for k in range(NK))
 
     # ---- parity of this run's level against the reference's results ----------
@@ -766,7 +779,7 @@ def main():
                      "peak_spec": 8000.0,
                      "frac_spec": (per[dom]["achieved"] / 8000.0) if per[dom]["achieved"] else None,
                      "bytes_per_group_launch": per[dom]["bytes_per_group_launch"],
-                     "group_launches": prof_iters,
+                     "group_launches": per[dom].get("group_launches", prof_iters),
                      "timing": f"per-launch CUDA events on the launching stream, {prof_steps} "
                                "profiled step(s) with the level on one stream "
                                "(UQG_SOLVE_STREAMS=1)",

@@ -59,12 +59,13 @@ int uqg_ctx_set_band_hint(uqg_ctx* ctx, int nbands, const int* starts_host,
 #define UQG_K_PCG_INIT 2
 #define UQG_K_PCG_SPMV 3   /* Ap = A p + p.Ap                           */
 #define UQG_K_PCG_UPDATE 4 /* r update + r.r, r.z                       */
-#define UQG_K_PCG_DIR 5    /* p = z + beta p, deferred x updates         */
+#define UQG_K_PCG_DIR 5    /* p = z + beta p (x += alpha p when kx = 1)  */
 #define UQG_K_DOT 6        /* lane_dot / qoi                             */
 #define UQG_K_GROUP 7      /* key bits + radix sort + chunk              */
 #define UQG_K_SPMV 8       /* standalone spmv                            */
 #define UQG_K_OTHER 9      /* diagonal, jacobi, finalize                 */
-#define UQG_NKERN 10
+#define UQG_K_PCG_FLUSH 10 /* deferred x += sum_j alpha_j p_j (every kx) */
+#define UQG_NKERN 11
 
 /* Per-launch CUDA-event timing on the launching stream (off by default).
  * uqg_ctx_profile_read returns accumulated milliseconds and launch counts per

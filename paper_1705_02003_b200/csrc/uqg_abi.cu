@@ -690,7 +690,7 @@ int pcg_impl(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const 
                  launch_pcg_spmv(gl, q.G, qs, N, nnz, q.st, q.op.ro, q.op.ci, q.op.vals, q.p,
                                  q.ap, ctx->bands.nb ? &ctx->bands : nullptr));
     UQG_LAUNCH(UQG_K_PCG_UPDATE, qs, launch_pcg_update(gl, q.G, qs, N, q.st, dq, maxit, q.r, q.ap));
-    if (flush) UQG_LAUNCH(UQG_K_PCG_DIR, qs, launch_pcg_flush(gl, q.G, qs, N, q.st, xq, q.p, true));
+    if (flush) UQG_LAUNCH(UQG_K_PCG_FLUSH, qs, launch_pcg_flush(gl, q.G, qs, N, q.st, xq, q.p, true));
     UQG_LAUNCH(UQG_K_PCG_DIR, qs, launch_pcg_dir(gl, q.G, qs, N, q.st, dq, q.r, xq, q.p));
     return UQG_OK;
   };
@@ -779,7 +779,7 @@ int pcg_impl(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const 
       return UQG_ECUDA;
     }
     if (kx > 1)  // deferred x updates still pending at termination
-      UQG_LAUNCH(UQG_K_PCG_DIR, s, launch_pcg_flush(gl, G, s, N, st, x, p, false));
+      UQG_LAUNCH(UQG_K_PCG_FLUSH, s, launch_pcg_flush(gl, G, s, N, st, x, p, false));
     UQG_TRY_CUDA(cudaMemcpyAsync(ctx->loops_host, ctx->loops_dev, sizeof(int),
                                  cudaMemcpyDeviceToHost, s));
     UQG_TRY_CUDA(cudaMemcpyAsync(ctx->loops_host + 1, st.ndone, sizeof(int),
@@ -794,7 +794,8 @@ int pcg_impl(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const 
     ctx->launches += per_pass * (passes - 1);
     ctx->kind_launches[UQG_K_PCG_SPMV] += (long long)kx * (passes - 1);
     ctx->kind_launches[UQG_K_PCG_UPDATE] += (long long)kx * (passes - 1);
-    ctx->kind_launches[UQG_K_PCG_DIR] += (long long)(kx + (kx > 1)) * (passes - 1);
+    ctx->kind_launches[UQG_K_PCG_DIR] += (long long)kx * (passes - 1);
+    ctx->kind_launches[UQG_K_PCG_FLUSH] += (long long)(kx > 1) * (passes - 1);
     ctx->kind_launches[UQG_K_OTHER] += passes - 1;
   } else {
     // Launch loop: the host polls each part's device done-counter between
@@ -853,7 +854,7 @@ int pcg_impl(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const 
     for (int i = 0; i < P; ++i) {
       Part& q = parts[i];
       if (kx > 1)  // deferred x updates still pending at termination
-        UQG_LAUNCH(UQG_K_PCG_DIR, q.s,
+        UQG_LAUNCH(UQG_K_PCG_FLUSH, q.s,
                    launch_pcg_flush(with_groups(geo, q.G), q.G, q.s, N, q.st, vecw(q, x), q.p,
                                     false));
       if (i > 0) UQG_LAUNCH(UQG_K_OTHER, q.s, launch_pcg_finalize(q.G, S, q.s, q.st, ens_iters + q.g0));

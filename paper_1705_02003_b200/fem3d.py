@@ -27,7 +27,7 @@ from . import _lib
 from .errors import FemError
 from .field import GAUSS
 
-__all__ = ["StructuredMesh3D", "shape_data"]
+__all__ = ["StructuredMesh3D", "StructuredMesh", "assemble", "shape_data"]
 
 
 def shape_data():
@@ -51,9 +51,12 @@ def shape_data():
 class StructuredMesh3D:
     """Uniform hex mesh of the unit cube: graph, element tables, load."""
 
-    def __init__(self, cells: int):
+    def __init__(self, cells: int, quadrature: str = "gauss2"):
         if cells < 2:
             raise FemError(f"need at least 2 cells per direction, got {cells}")
+        if quadrature != "gauss2":
+            raise FemError(f"unsupported quadrature {quadrature!r}")
+        self.quadrature = quadrature
         m = self.cells = int(cells)
         self.h = 1.0 / m
         k = m - 1
@@ -88,8 +91,14 @@ class StructuredMesh3D:
         """Constant second/third-direction element matrix (``fem3d.py:160``)."""
         return a_y * self.elem_mats[1].sum(axis=0) + a_z * self.elem_mats[2].sum(axis=0)
 
+    @property
     def quad_points(self) -> np.ndarray:
         """(E*8, 3) Gauss points, element-major, q bit-ordered (``fem3d.py:93-95``)."""
+        if getattr(self, "_qp", None) is None:
+            self._qp = self._quad_points()
+        return self._qp
+
+    def _quad_points(self) -> np.ndarray:
         m = self.cells
         ex, ey, ez = np.meshgrid(np.arange(m), np.arange(m), np.arange(m), indexing="ij")
         elems = np.stack([ex.ravel(), ey.ravel(), ez.ravel()], axis=1)
@@ -112,3 +121,44 @@ class StructuredMesh3D:
             self._dev = (_lib.to_dev(self.row_offsets), _lib.to_dev(self.col_indices),
                          _lib.to_dev(np.ascontiguousarray(self.elem_mats[0])))
         return self._dev
+
+
+StructuredMesh = StructuredMesh3D  # the reference's name (fem3d.py:57)
+
+
+def assemble(mesh: StructuredMesh3D, field, samples, mode_vals=None):
+    """Drop-in for the reference's ``assemble`` (``fem3d.py:138-175``) on its
+    own 3D operator: the width-S ensemble system assembled on the GPU
+    (``uqg_kl_eval_sep3d`` + ``uqg_assemble_fem3d``), the matrix kept
+    device-resident as ``[nnz][S]`` (host values materialise lazily).
+
+    ``mode_vals`` is accepted for signature parity; the device rebuilds the
+    mode values at the Gauss points from separable 1D tables (bit-identical
+    to ``field.mode_values(mesh.quad_points)``).  Raises ``FemError`` on a
+    non-positive coefficient (``:153-154``) before returning.
+    """
+    from .ensemble import EnsembleCsrMatrix
+    from .fv2d import AssembledEnsembleSystem
+    from .solve import FEM3DOperator
+
+    ys = np.atleast_2d(np.asarray(samples, dtype=np.float64))
+    S = len(ys)
+    if getattr(field, "dim", 3) != 3:
+        raise FemError("the 3D operator needs a 3D field (build_field(..., dim=3))")
+    if ys.shape[1] != field.n_modes:
+        raise FemError(f"samples must have {field.n_modes} columns, got {ys.shape[1]}")
+    if field.a_y <= 0 or field.a_z <= 0:
+        raise FemError("non-positive diffusion coefficient at a quadrature point")
+    torch = _lib._torch()
+    op = FEM3DOperator(field, mesh.cells, mesh=mesh)
+    _lib.call("uqg_status_clear", _lib.ctx(), _lib.stream())
+    a = torch.empty((mesh.n_quad * S,), dtype=torch.float64, device=_lib.device())
+    op.coefficients(_lib.to_dev(ys), None, 1, S, a)
+    if _lib.status_sync() & 1:
+        raise FemError("non-positive diffusion coefficient at a quadrature point")
+    vals = torch.empty((mesh.nnz * S,), dtype=torch.float64, device=_lib.device())
+    op.assemble(a, 1, S, vals, None)
+    rowptr, col, _ = mesh.device()
+    mat = EnsembleCsrMatrix.from_device(mesh.row_offsets, mesh.col_indices, rowptr, col, vals, S)
+    rhs = np.full((S, mesh.n_dofs), mesh.load)
+    return AssembledEnsembleSystem(matrix=mat, rhs=rhs, samples=ys.copy())

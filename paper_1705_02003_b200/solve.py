@@ -104,13 +104,13 @@ class FEM3DOperator:
 
     max_row_len = 27
 
-    def __init__(self, field, cells: int):
+    def __init__(self, field, cells: int, mesh: StructuredMesh3D | None = None):
         if field.dim != 3:
             raise FemError("the 3D operator needs a 3D field")
         if field.a_y <= 0 or field.a_z <= 0:
             raise FemError("non-positive diffusion coefficient a_y / a_z")
         self.field = field
-        self.mesh = m = StructuredMesh3D(cells)
+        self.mesh = m = mesh if mesh is not None else StructuredMesh3D(cells)
         self.n_dofs, self.nnz, self.n_coef = m.n_dofs, m.nnz, m.n_quad
         self.rhs_const = m.load
         self.qtab = _lib.to_dev(field.quad_tables(cells))

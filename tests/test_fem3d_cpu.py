@@ -63,7 +63,7 @@ def test_quad_tables_rebuild_dense_mode_table():
     f = build_field(0.25, np.sqrt(300.0), 4, 0.1, sigma0_convention="kernel", dim=3)
     m = 5
     mesh = StructuredMesh3D(m)
-    dense = f.mode_values(mesh.quad_points())
+    dense = f.mode_values(mesh.quad_points)
     qt = f.quad_tables(m)
     e = np.arange(m ** 3)
     ex, ey, ez = e // (m * m), (e // m) % m, e % m

@@ -51,7 +51,7 @@ def test_device_keys_bit_identical_to_host(study, dim, init, tau, nmax):
 def test_anisotropy_indicator_matches_reference_formula():
     f = uq.build_field(0.25, np.sqrt(300.0), 4, 0.1, sigma0_convention="kernel", dim=3)
     mesh = uq.StructuredMesh3D(8)
-    probes = mesh.quad_points()
+    probes = mesh.quad_points
     mv = f.mode_values(probes)
     ys = np.random.default_rng(4).uniform(-1, 1, (7, 4))
     got = anisotropy_indicators(f, ys, probes, mv)

@@ -21,6 +21,8 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--wave", type=int, default=None)
     ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--maxit", type=int, default=None,
+                    help="cap PCG iterations per group (KL / assembly captures at C4/C5)")
     a = ap.parse_args()
     import torch
 
@@ -33,6 +35,8 @@ def main():
     solver = uq.EnsembleSolver2D(f, cfg.cells, cfg.tol, cfg.maxit, cfg.a2,
                                  max_groups_per_wave=a.wave)
     ids, coords, keys, _ = bench.make_workload(cfg, solver)
+    if a.maxit:
+        solver.maxit, solver.tol = a.maxit, 1e-300
     dev = torch.device("cuda", 0)
     d_c = torch.from_numpy(coords).to(dev)
     d_k = None if keys is None else torch.from_numpy(keys).to(dev)
