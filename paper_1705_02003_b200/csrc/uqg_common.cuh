@@ -82,21 +82,11 @@ struct Geo {
   int tstride;    // tickets per group: 1 (+ nsc super-chunk tickets when sc > 1)
 };
 
-// UQG_LANES_PER_THREAD=1 forces V = 1 (tuning experiments only; V changes the
-// reduction tree, so results are reproducible per setting, not across them).
-inline int forced_v() {
-  static const int v = [] {
-    const char* e = getenv("UQG_LANES_PER_THREAD");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
 inline Geo make_geo(long long N, int S, int maxrow = 0) {
   Geo g;
   g.S = S;
   g.maxrow = maxrow;
-  g.V = (S % 2 == 0 && forced_v() != 1) ? 2 : 1;
+  g.V = S % 2 == 0 ? 2 : 1;
   g.L = S / g.V;
   g.Lp = 1;
   while (g.Lp < g.L) g.Lp <<= 1;
@@ -113,10 +103,7 @@ inline Geo make_geo(long long N, int S, int maxrow = 0) {
   // Then consecutive chunks form super-chunks whose partials are summed (in
   // chunk order) by the block completing the super-chunk, and the final stage
   // sums the <= kMaxChunks super-partials.
-  static const int ct_max = [] {  // UQG_CHUNK_TILES (tuning only: changes the trees)
-    const char* e = getenv("UQG_CHUNK_TILES");
-    return e ? atoi(e) : 8;
-  }();
+  constexpr int ct_max = 8;
   long long ct = g.tiles / 64;
   ct = ct < 1 ? 1 : (ct > ct_max ? ct_max : ct);
   if ((g.tiles + ct - 1) / ct > kMaxChunks) {

@@ -402,16 +402,6 @@ __global__ void __launch_bounds__(256, UQG_FACE_MINB) pcg_spmv_fv2d_kernel(
   face_spmv_body<V, TY>(N, geo, st, op, p, ap);
 }
 
-// 4 lanes per thread (32-byte LDG/STG.256) at half the block size: the same
-// rows per tile (R), chunks and per-lane reduction trees as the 2-lane kernel
-// (identical bits), half the address arithmetic and more bytes in flight per
-// register.  geo: the 2-lane geometry with V = 4, L and Lp halved, T = 128.
-__global__ void __launch_bounds__(128, 5) pcg_spmv_fv2d4_kernel(
-    long long N, Geo geo, PcgState st, Fv2dOp op, const double* __restrict__ p,
-    double* __restrict__ ap) {
-  face_spmv_body<4>(N, geo, st, op, p, ap);
-}
-
 template <int V>
 __global__ void __launch_bounds__(256) spmv_fv2d_kernel(long long N, Geo geo, Fv2dOp op,
                                                         const double* __restrict__ x,
@@ -754,157 +744,6 @@ __device__ __forceinline__ int block_tile_count(const Geo& geo) {
   return (int)((nb - 1) * geo.chunk_tiles + last_tiles);
 }
 
-// ---------------------------------------------------------------------------
-// Shared helpers of the staged face SpMV.
-
-template <int V>
-__device__ __forceinline__ void lds_v(const double* p, double (&o)[V]) {
-  if constexpr (V == 2) {
-    const double2 t = *reinterpret_cast<const double2*>(p);
-    o[0] = t.x;
-    o[1] = t.y;
-  } else {
-    o[0] = *p;
-  }
-}
-
-// 0-based cell (i0, j0) of a row: float quotient, corrected (row < m*m).
-__device__ __forceinline__ void cell_of(int row, int m, float inv_m, int& i0, int& j0) {
-  i0 = (int)((float)row * inv_m);
-  j0 = row - i0 * m;
-  if (j0 < 0) {
-    --i0;
-    j0 += m;
-  } else if (j0 >= m) {
-    ++i0;
-    j0 -= m;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Face-form SpMV with TMA-staged first-touch bands.  Of a tile's loads, only
-// the east faces Te = tx[row + m] and the east neighbours p[row + m] are
-// first touches (DRAM); every other operand was streamed in by an earlier tile
-// (L1/L2 hits).  One elected thread bulk-copies those two R-row bands of the
-// next NST tiles into shared memory (cp.async.bulk + mbarrier), which keeps
-// NST x 2 x R x S x 8 bytes of DRAM reads in flight per CTA without holding
-// registers; the L2-resident operands are plain loads.  Same arithmetic,
-// chunks and batched reduction as pcg_spmv_fv2d_kernel: identical bits.
-// Needs S even (16-byte rows) and 16-byte aligned tx / p.
-template <int NST>
-__global__ void __launch_bounds__(256, 4) pcg_spmv_fv2d_tma_kernel(long long N, Geo geo,
-                                                                   PcgState st, Fv2dOp op,
-                                                                   const double* __restrict__ p,
-                                                                   double* __restrict__ ap) {
-  constexpr int V = 2;
-  extern __shared__ __align__(128) double red[];
-  const int g = blockIdx.y, t = threadIdx.x;
-  if (st.done[g] != kRunning) return;
-  const int xs = xslot(st, st.it[g]);  // buffer of p_k / alpha_k
-  p += (size_t)xs * st.pstride;
-  const int S = geo.S, R = geo.R, T = geo.T, m = op.m, n = (int)N, B = gridDim.x;
-  const int sl = t % geo.Lp, rr = t / geo.Lp;
-  const bool lane_ok = sl < geo.L;
-  const double* pg_all = p + (size_t)g * N * S;
-  const double* txg_all = op.tx + (size_t)g * (N + m) * S;
-  const double* pg = pg_all + V * sl;
-  const double* txg = txg_all + V * sl;
-  const double* tyg = op.ty ? op.ty + (size_t)g * (N + m) * S + V * sl : nullptr;
-  double* apg = ap + (size_t)g * N * S + V * sl;
-  const int band = R * S;  // doubles per staged band
-  double* stage = red + (size_t)kFaceBatch * V * T;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stage + (size_t)NST * 2 * band);
-  const int n_tiles = block_tile_count(geo);
-  const float inv_m = 1.0f / (float)m;
-
-  if (t == 0) {
-    for (int s = 0; s < NST; ++s) mbar_init(&bars[s], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  auto issue = [&](int i) {
-    int chunk;
-    const int r0 = (int)block_tile(geo, i, chunk) * R + m;  // first row of the +m bands
-    int tx1 = r0 + R, p1 = r0 + R;
-    if (tx1 > n + m) tx1 = n + m;
-    if (p1 > n) p1 = n;
-    const uint32_t tb = (uint32_t)(tx1 > r0 ? tx1 - r0 : 0) * (uint32_t)S * 8u;
-    const uint32_t pb = (uint32_t)(p1 > r0 ? p1 - r0 : 0) * (uint32_t)S * 8u;
-    uint64_t* bar = &bars[i % NST];
-    double* st0 = stage + (size_t)(i % NST) * 2 * band;
-    fence_proxy_async();
-    mbar_expect_tx(bar, tb + pb);
-    if (tb) bulk_g2s(st0, txg_all + (size_t)r0 * S, tb, bar);
-    if (pb) bulk_g2s(st0 + band, pg_all + (size_t)r0 * S, pb, bar);
-  };
-  if (t == 0) {
-    for (int i = 0; i < NST && i < n_tiles; ++i) issue(i);
-  }
-
-  const int ct = (int)geo.chunk_tiles;
-  double acc[V] = {};
-  int k = 0, c0 = blockIdx.x;  // chunk slot in the current batch, its first chunk
-  for (int i = 0; i < n_tiles; ++i) {
-    int chunk;
-    const long long tile = block_tile(geo, i, chunk);
-    mbar_wait(&bars[i % NST], (uint32_t)((i / NST) & 1));
-    const int row = (int)tile * R + rr;
-    if (lane_ok && row < n) {
-      int i0, j0;
-      cell_of(row, m, inv_m, i0, j0);
-      const double* st0 = stage + (size_t)(i % NST) * 2 * band + rr * S + V * sl;
-      FaceRow<V> f;
-      f.w = i0 > 0;
-      f.s = j0 > 0;
-      f.n = j0 < m - 1;
-      f.e = i0 < m - 1;
-      ldgv<V>(txg + row * S, f.tw);
-      lds_v<V>(st0, f.te);
-      if (tyg) {
-        ldgv<V>(tyg + (row + i0) * S, f.ts);
-        ldgv<V>(tyg + (row + i0 + 1) * S, f.tn);
-      } else {
-#pragma unroll
-        for (int j = 0; j < V; ++j) f.ts[j] = f.tn[j] = op.a_y;
-      }
-      if (f.w) ldgv<V>(pg + (row - m) * S, f.pw);
-      if (f.s) ldgv<V>(pg + (row - 1) * S, f.ps);
-      ldgv<V>(pg + row * S, f.pc);
-      if (f.n) ldgv<V>(pg + (row + 1) * S, f.pn);
-      if (f.e) lds_v<V>(st0 + band, f.pe);
-      double y[V];
-      f.apply(y, acc);
-      stv<V>(apg + row * S, y);
-    }
-    __syncthreads();  // stage (i % NST) consumed by every thread
-    if (t == 0 && i + NST < n_tiles) issue(i + NST);
-    const bool chunk_end = ((i + 1) % ct == 0) || (tile == geo.tiles - 1);
-    if (!chunk_end) continue;
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-      red[(k * V + j) * T + t] = acc[j];
-      acc[j] = 0.0;
-    }
-    ++k;
-    if (k < kFaceBatch && i + 1 < n_tiles) continue;
-    const bool last = reduce_lanes_batch<1, V>(red, st.part, st.ticket, g, c0, B, k, geo);
-    c0 += k * B;
-    k = 0;
-    if (!last) continue;
-    if (t < geo.L) {
-#pragma unroll
-      for (int j = 0; j < V; ++j) {
-        const size_t l = (size_t)g * S + V * t + j;
-        const double pap = red[j * T + t];
-        const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
-        st.frozen[l] = fr;
-        st.alpha[(size_t)xs * st.G * S + l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
-      }
-    }
-    if (t == 0) st.it[g] += 1;
-  }
-}
-
 template <int ML, int NST = kStages, int MINB = 3>
 __global__ void __launch_bounds__(256, MINB) pcg_spmv_tma_kernel(long long N, long long nnz, Geo geo,
                                                            PcgState st,
@@ -1022,208 +861,6 @@ __global__ void __launch_bounds__(256, MINB) pcg_spmv_tma_kernel(long long N, lo
   }
 }
 
-// ---------------------------------------------------------------------------
-// Warp-specialized variant: one producer warp streams the tiles' values into a
-// 4-stage ring (full/empty mbarrier pair per stage) while 8 consumer warps
-// compute; a consumer warp releases a stage with one mbarrier arrive, so there
-// is no CTA-wide barrier per tile and warps drift independently.  Chunk-end
-// reductions synchronise the consumers only (named barrier 1, 256 threads).
-
-constexpr int kWsStages = 4;
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
-
-template <int NS>
-__device__ __forceinline__ void tree_rows_c(double* red, int T, int Lp, int R, int t) {
-  for (int st = R >> 1; st > 0; st >>= 1) {
-    if ((t / Lp) < st) {
-#pragma unroll
-      for (int v = 0; v < NS; ++v) red[v * T + t] += red[v * T + t + st * Lp];
-    }
-    consumer_sync();
-  }
-}
-
-// reduce_lanes with consumer-only barriers (same arithmetic and order)
-template <int NV, int V>
-__device__ bool reduce_lanes_c(const double (&val)[NV][V], double* red, double* part,
-                               unsigned int* ticket, int g, int chunk, const Geo& geo,
-                               int* s_last) {
-  constexpr int NS = NV * V;
-  const int t = threadIdx.x;
-  const int T = geo.T, Lp = geo.Lp, R = geo.R, L = geo.L, S = geo.S, C = geo.chunks;
-  consumer_sync();
-#pragma unroll
-  for (int v = 0; v < NV; ++v)
-#pragma unroll
-    for (int j = 0; j < V; ++j) red[(v * V + j) * T + t] = val[v][j];
-  consumer_sync();
-  tree_rows_c<NS>(red, T, Lp, R, t);
-  if (t < L) {
-#pragma unroll
-    for (int v = 0; v < NV; ++v)
-#pragma unroll
-      for (int j = 0; j < V; ++j)
-        part[(((size_t)g * geo.pstride + chunk) * NV + v) * S + V * t + j] =
-            red[(v * V + j) * T + t];
-  }
-  __threadfence();
-  consumer_sync();
-  if (t == 0) {  // (no super-chunks: the host selects this kernel only when geo.sc == 1)
-    unsigned int tk = atomicAdd(&ticket[(size_t)g * geo.tstride], 1u);
-    *s_last = (tk == (unsigned)(C - 1));
-  }
-  consumer_sync();
-  if (!*s_last) return false;
-  __threadfence();
-  const int sl = t % Lp, jr = t / Lp;
-  double acc[NS];
-#pragma unroll
-  for (int v = 0; v < NS; ++v) acc[v] = 0.0;
-  if (sl < L) {
-#pragma unroll 4
-    for (int cc = jr; cc < C; cc += R) {
-#pragma unroll
-      for (int v = 0; v < NV; ++v)
-#pragma unroll
-        for (int j = 0; j < V; ++j)
-          acc[v * V + j] +=
-              __ldcg(&part[(((size_t)g * geo.pstride + cc) * NV + v) * S + V * sl + j]);
-    }
-  }
-#pragma unroll
-  for (int v = 0; v < NS; ++v) red[v * T + t] = acc[v];
-  consumer_sync();
-  tree_rows_c<NS>(red, T, Lp, R, t);
-  if (t == 0) ticket[(size_t)g * geo.tstride] = 0u;
-  return true;
-}
-
-template <int ML>
-__global__ void __launch_bounds__(288, 2) pcg_spmv_ws_kernel(
-    long long N, long long nnz, Geo geo, PcgState st, const int* __restrict__ ro,
-    const int* __restrict__ ci, const double* __restrict__ vals, const double* __restrict__ p,
-    double* __restrict__ ap, BandHint bh) {
-  constexpr int V = 2;
-  extern __shared__ __align__(128) double red[];
-  __shared__ int s_last;
-  const int g = blockIdx.y, t = threadIdx.x;
-  if (st.done[g] != kRunning) return;
-  const int xs = xslot(st, st.it[g]);  // buffer of p_k / alpha_k
-  p += (size_t)xs * st.pstride;
-  const int S = geo.S, R = geo.R, T = geo.T;  // T = 256 consumer threads
-  const int stage_doubles = R * ML * S;
-  double* stage = red + V * T;
-  uint64_t* full = reinterpret_cast<uint64_t*>(stage + kWsStages * stage_doubles);
-  uint64_t* empty = full + kWsStages;
-  const double* vg = vals + (size_t)g * nnz * S;
-  const double* pg_all = p + (size_t)g * N * S;
-  const int n_tiles = block_tile_count(geo);
-  const int ct = (int)geo.chunk_tiles;
-  auto tile_of = [&](int i) -> long long {
-    const int j = i / ct;
-    return ((long long)blockIdx.x + (long long)j * gridDim.x) * ct + (i - j * ct);
-  };
-  if (t == 0) {
-    for (int s = 0; s < kWsStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 8);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  if (t >= 256) {  // ---- producer warp
-    if (t == 256) {
-      for (int i = 0; i < n_tiles; ++i) {
-        const int s = i % kWsStages;
-        if (i >= kWsStages) mbar_wait(&empty[s], (uint32_t)(((i / kWsStages) - 1) & 1));
-        const long long r0 = tile_of(i) * R;
-        const long long r1 = r0 + R < N ? r0 + R : N;
-        const int k0 = __ldg(&ro[r0]), k1 = __ldg(&ro[r1]);
-        const uint32_t bytes = (uint32_t)(k1 - k0) * (uint32_t)S * 8u;
-        fence_proxy_async();
-        mbar_expect_tx(&full[s], bytes);
-        if (bytes) bulk_g2s(stage + s * stage_doubles, vg + (size_t)k0 * S, bytes, &full[s]);
-#pragma unroll
-        for (int b = 0; b < kMaxBands; ++b) {
-          if (b < bh.nb) {
-            long long lo = r0 + bh.start[b], hi = lo + R + bh.extra[b];
-            lo = lo < 0 ? 0 : lo;
-            hi = hi > N ? N : hi;
-            if (hi > lo) bulk_prefetch_l2(pg_all + lo * S, (uint32_t)(hi - lo) * S * 8u);
-          }
-        }
-      }
-    }
-    return;
-  }
-
-  // ---- consumer warps
-  const int sl = t % geo.Lp, rr = t / geo.Lp, lane = t & 31;
-  const size_t base = (size_t)g * N * S + V * sl;
-  const double* pg = p + base;
-  double acc[1][V] = {};
-  for (int i = 0; i < n_tiles; ++i) {
-    const long long tile = tile_of(i);
-    const int s = i % kWsStages;
-    mbar_wait(&full[s], (uint32_t)((i / kWsStages) & 1));
-    if (sl < geo.L) {
-      const long long row = tile * R + rr;
-      if (row < N) {
-        const int kt0 = __ldg(&ro[tile * R]);
-        const int k0 = __ldg(&ro[row]), k1 = __ldg(&ro[row + 1]);
-        const double* sv = stage + s * stage_doubles + (size_t)(k0 - kt0) * S + V * sl;
-        const int len = k1 - k0;
-        int c[ML];
-#pragma unroll
-        for (int e = 0; e < ML; ++e) c[e] = e < len ? __ldg(&ci[k0 + e]) : 0;
-        double b[ML][V];
-#pragma unroll
-        for (int e = 0; e < ML; ++e)
-          if (e < len) ldgv<V>(pg + (size_t)c[e] * S, b[e]);
-        double y[V] = {0.0, 0.0};
-#pragma unroll
-        for (int e = 0; e < ML; ++e) {
-          if (e < len) {
-            const double2 a = *reinterpret_cast<const double2*>(sv + (size_t)e * S);
-            y[0] = __dadd_rn(y[0], __dmul_rn(a.x, b[e][0]));
-            y[1] = __dadd_rn(y[1], __dmul_rn(a.y, b[e][1]));
-          }
-        }
-        stv<V>(ap + base + row * S, y);
-        double pv[V];
-        ldgv<V>(pg + row * S, pv);
-#pragma unroll
-        for (int j = 0; j < V; ++j) acc[0][j] = __fma_rn(pv[j], y[j], acc[0][j]);
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
-    const bool chunk_end = ((i + 1) % ct == 0) || (tile == geo.tiles - 1);
-    if (chunk_end) {
-      const int chunk = (int)(tile / ct);
-      if (reduce_lanes_c<1, V>(acc, red, st.part, st.ticket, g, chunk, geo, &s_last)) {
-        if (t < geo.L) {
-#pragma unroll
-          for (int j = 0; j < V; ++j) {
-            const size_t l = (size_t)g * S + V * t + j;
-            const double pap = red[j * geo.T + t];
-            const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
-            st.frozen[l] = fr;
-            st.alpha[(size_t)xs * st.G * S + l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
-          }
-        }
-        if (t == 0) st.it[g] += 1;
-      }
-      acc[0][0] = acc[0][1] = 0.0;
-    }
-  }
-}
-
 // ensemble_iterations = max over lanes (ensemble.py:277)
 __global__ void pcg_finalize_kernel(PcgState st, int G, int S, int* ens_iters) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1259,19 +896,11 @@ __global__ void pcg_finalize_kernel(PcgState st, int G, int S, int* ens_iters) {
 static size_t red_bytes(const Geo& geo, int nv) { return (size_t)nv * geo.V * geo.T * sizeof(double); }
 
 // Blocks per group sized to the kernel's residency (pick_blocks) for the
-// geo.gact running groups; UQG_OCC_BLOCKS=0 keeps with_groups' fixed target.
-static bool occ_blocks() {
-  static const bool on = [] {
-    const char* e = getenv("UQG_OCC_BLOCKS");
-    return !e || atoi(e) != 0;
-  }();
-  return on;
-}
-
+// geo.gact running groups.
 template <class F>
 static Geo sized(const Geo& geo, SlotCache& c, F fn, int T, size_t smem) {
   Geo gl = geo;
-  if (occ_blocks()) gl.B = pick_blocks(geo.gact, geo.chunks, kernel_slots(c, fn, T, smem));
+  gl.B = pick_blocks(geo.gact, geo.chunks, kernel_slots(c, fn, T, smem));
   return gl;
 }
 
@@ -1315,37 +944,6 @@ static void launch_spmv_tma(const Geo& gl, int G, cudaStream_t s, long long N, l
                                                                        vals, p, ap, bh);
 }
 
-template <int ML>
-static void launch_spmv_ws(const Geo& gl, int G, cudaStream_t s, long long N, long long nnz,
-                           const PcgState& st, const int* ro, const int* ci, const double* vals,
-                           const double* p, double* ap, const BandHint* bands) {
-  const size_t smem = (size_t)2 * gl.T * sizeof(double) +
-                      (size_t)kWsStages * gl.R * ML * gl.S * sizeof(double) + 2 * kWsStages * 8;
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaFuncSetAttribute(pcg_spmv_ws_kernel<ML>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    configured = smem;
-  }
-  BandHint bh{};
-  if (bands && (reinterpret_cast<uintptr_t>(p) & 15) == 0) bh = *bands;
-  pcg_spmv_ws_kernel<ML><<<dim3(gl.B, G), 288, smem, s>>>(N, nnz, gl, st, ro, ci, vals, p, ap, bh);
-}
-
-// UQG_SPMV_TMA (CSR SpMV): 0 = register-gather kernel, 1 = TMA-staged values
-// (default; C2 4.73 TB/s with the band hint's L2 prefetch of the p bands),
-// 4 = warp-specialized producer/consumer ring (4.04 TB/s), 6 / 7 = mode 1 with
-// 2 stages x 4 CTAs/SM / 4 stages x 2 CTAs/SM (both slower).  All give
-// identical bits.  (Metadata-staged, fully band-staged and paired-tile
-// variants were measured slower still and removed.)
-int spmv_tma_mode() {
-  static const int mode = [] {
-    const char* e = getenv("UQG_SPMV_TMA");
-    return e ? atoi(e) : 1;
-  }();
-  return mode;
-}
-
 void launch_spmv_fv2d(const Geo& geo, int G, cudaStream_t s, long long N, const Fv2dOp& op,
                       const double* x, double* y) {
   const Geo gl = with_groups(geo, G);
@@ -1361,59 +959,10 @@ void launch_pcg_spmv_fv2d(const Geo& geo, int G, cudaStream_t s, long long N, co
                      : sized(geo, cf1, pcg_spmv_fv2d_kernel<1>, geo.T,
                              red_bytes(geo, kFaceBatch));
   const size_t smem = red_bytes(gl, kFaceBatch);
-  // UQG_FACE_V4=1: 4-lanes-per-thread kernel (off by default: measured slower)
-  static const bool v4 = [] {
-    const char* e = getenv("UQG_FACE_V4");
-    return e && atoi(e) != 0;
-  }();
-  const bool al32 = ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(op.tx) |
-                      reinterpret_cast<uintptr_t>(ap)) & 31) == 0;
-  if (v4 && gl.V == 2 && gl.S % 4 == 0 && gl.Lp >= 2 && gl.T == 256 && al32 && !op.ty) {
-    Geo g4 = gl;
-    g4.V = 4;
-    g4.L = gl.L / 2;
-    g4.Lp = gl.Lp / 2;
-    g4.T = gl.T / 2;  // rows per tile R unchanged
-    pcg_spmv_fv2d4_kernel<<<dim3(g4.B, G), g4.T, smem, s>>>(N, g4, st, op, p, ap);
-    return;
-  }
-  // UQG_FACE_TMA: stages of the TMA-banded kernel (0 = off, default)
-  static const int tma = [] {
-    const char* e = getenv("UQG_FACE_TMA");
-    return e ? atoi(e) : 0;
-  }();
-  const bool aligned = ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(op.tx)) &
-                        15) == 0;
-  if (tma >= 2 && tma <= 6 && gl.V == 2 && aligned) {
-    const size_t sm = smem + (size_t)tma * 2 * gl.R * gl.S * sizeof(double) + tma * 8;
-#define UQG_FACE_TMA_LAUNCH(NS)                                                               \
-  do {                                                                                        \
-    static size_t configured = 0;                                                             \
-    if (sm > configured) {                                                                    \
-      cudaFuncSetAttribute(pcg_spmv_fv2d_tma_kernel<NS>,                                      \
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);             \
-      configured = sm;                                                                        \
-    }                                                                                         \
-    pcg_spmv_fv2d_tma_kernel<NS><<<dim3(gl.B, G), gl.T, sm, s>>>(N, gl, st, op, p, ap);       \
-  } while (0)
-    switch (tma) {
-      case 2: UQG_FACE_TMA_LAUNCH(2); break;
-      case 3: UQG_FACE_TMA_LAUNCH(3); break;
-      case 4: UQG_FACE_TMA_LAUNCH(4); break;
-      case 5: UQG_FACE_TMA_LAUNCH(5); break;
-      default: UQG_FACE_TMA_LAUNCH(6); break;
-    }
-#undef UQG_FACE_TMA_LAUNCH
-    return;
-  }
   // constant y-faces (a2 const, the BASELINE configs) compiled in: fewer live
-  // registers, no spill of the y-face branch (C2 face SpMV 2,345 -> 2,277 ms).
-  // UQG_FACE_SPEC=0: the run-time branch kernel (same bits).
-  static const bool spec = [] {
-    const char* e = getenv("UQG_FACE_SPEC");
-    return !e || atoi(e) != 0;
-  }();
-  if (spec && gl.V == 2 && !op.ty)
+  // registers, no spill of the y-face branch (C2 face SpMV 2,345 -> 2,277 ms);
+  // a y-face array (a2 = "same") takes the run-time branch kernel (same bits).
+  if (gl.V == 2 && !op.ty)
     pcg_spmv_fv2d_kernel<2, 0><<<dim3(gl.B, G), gl.T, smem, s>>>(N, gl, st, op, p, ap);
   else if (gl.V == 2)
     pcg_spmv_fv2d_kernel<2><<<dim3(gl.B, G), gl.T, smem, s>>>(N, gl, st, op, p, ap);
@@ -1425,29 +974,17 @@ void launch_pcg_spmv(const Geo& geo, int G, cudaStream_t s, long long N, long lo
                      const PcgState& st, const int* ro, const int* ci, const double* vals,
                      const double* p, double* ap, const BandHint* bands) {
   const Geo& gl = geo;  // B preset by the caller (blocks per ACTIVE group)
+  // TMA-staged values (C2 4.73 TB/s with the band hint's L2 prefetch of the p
+  // bands) when S is even, rows are short and the values 16-byte aligned;
+  // else the register-gather kernel - identical bits.  (Warp-specialized,
+  // 2/4-stage, metadata-staged, band-staged and paired-tile variants were
+  // measured slower and removed.)
   const bool aligned = (reinterpret_cast<uintptr_t>(vals) & 15) == 0;
-  const int mode = spmv_tma_mode();
-  if (mode && gl.V == 2 && aligned && gl.maxrow >= 1 && gl.maxrow <= 8) {
-    if (mode == 4 && gl.T == 256 && gl.sc == 1) {
-      if (gl.maxrow <= 5)
-        launch_spmv_ws<5>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
-      else
-        launch_spmv_ws<8>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
-    } else if (mode == 6) {  // 2 stages, 4 CTAs per SM
-      if (gl.maxrow <= 5)
-        launch_spmv_tma<5, 2, 4>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
-      else
-        launch_spmv_tma<8, 2, 4>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
-    } else if (mode == 7) {  // 4 stages, 2 CTAs per SM
-      if (gl.maxrow <= 5)
-        launch_spmv_tma<5, 4, 2>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
-      else
-        launch_spmv_tma<8, 4, 2>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
-    } else if (gl.maxrow <= 5) {
+  if (gl.V == 2 && aligned && gl.maxrow >= 1 && gl.maxrow <= 8) {
+    if (gl.maxrow <= 5)
       launch_spmv_tma<5>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
-    } else {
+    else
       launch_spmv_tma<8>(gl, G, s, N, nnz, st, ro, ci, vals, p, ap, bands);
-    }
     return;
   }
   UQG_DISPATCH_VML(gl, pcg_spmv_kernel, dim3(gl.B, G), red_bytes(gl, 1), s, N, nnz, gl, st, ro,
@@ -1468,12 +1005,9 @@ void launch_pcg_update(const Geo& geo, int G, cudaStream_t s, long long N, const
                          (int)smem);
     opted = smem;
   }
-  // UQG_UPDATE_SPEC=0: the run-time dinv branch kernel for Jacobi solves too (same bits)
-  static const bool spec = [] {
-    const char* e = getenv("UQG_UPDATE_SPEC");
-    return !e || atoi(e) != 0;
-  }();
-  if (spec && geo.V == 2 && dinv) {
+  // Jacobi scaling compiled in (the solver's case); identity preconditioning
+  // and V = 1 take the run-time branch kernel (same arithmetic)
+  if (geo.V == 2 && dinv) {
     static SlotCache cj;
     const Geo gl = sized(geo, cj, pcg_update_kernel<2, 1>, geo.T, smem);
     pcg_update_kernel<2, 1><<<dim3(gl.B, G), gl.T, smem, s>>>(N, gl, st, dinv, maxit, r, ap);

@@ -474,10 +474,6 @@ int persistent_cluster_size(const Geo& geo) {
   }
   int c = cached[vi];
   if (c > 16) c = 16;
-  if (const char* e = getenv("UQG_CLUSTER_SIZE")) {  // tuning: cap the cluster size
-    const int cap = atoi(e);
-    if (cap >= 2 && cap < c) c = cap;
-  }
   if (c > geo.chunks) c = geo.chunks;
   return c;
 }

@@ -82,14 +82,9 @@ np.save(sys.argv[2], np.array(out, dtype=object), allow_pickle=True)
 """
 
 
-_VARIANTS = {  # face SpMV variants (all must give the CSR bits)
-    "reg": {},                                            # default: 2 lanes / thread
-    "v4": {"UQG_FACE_V4": "1"},                           # 4 lanes / thread (LDG.256)
-    "tma2": {"UQG_FACE_TMA": "2"},                        # TMA-banded
-    "tma4": {"UQG_FACE_TMA": "4"},
-    "fixed": {"UQG_OCC_BLOCKS": "0"},                     # with_groups block sizing
+_VARIANTS = {  # solve-loop variants (all must give the CSR bits)
+    "reg": {},                                            # default launch loop
     "graph": {"UQG_PCG_GRAPH": "1"},                      # launch loop as one graph launch
-    "nospec": {"UQG_FACE_SPEC": "0", "UQG_UPDATE_SPEC": "0"},  # run-time branch kernels
 }
 
 
@@ -98,7 +93,7 @@ _VARIANTS = {  # face SpMV variants (all must give the CSR bits)
 def test_face_pcg_bitwise_equal_csr_pcg(tmp_path, persistent, variant):
     """Whole batched solves (iterations, QoIs, residual histories) through the
     launch loop (0), the cooperative (1) and the cluster (2) persistent kernel,
-    with every face SpMV variant."""
+    and the graph launch loop."""
     env = dict(os.environ, UQG_PCG_PERSISTENT=persistent, **_VARIANTS[variant])
     dst = tmp_path / "r.npy"
     subprocess.run([sys.executable, "-c", _SCRIPT, str(ROOT), str(dst)], env=env, check=True)

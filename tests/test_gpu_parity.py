@@ -402,40 +402,39 @@ def test_launch_accounting_and_profiling():
     assert cnt[3] >= r.ensemble_iterations and ms[3] > 0.0
 
 
-_TMA_SCRIPT = r"""
+_CSR_SCRIPT = r"""
 import sys, numpy as np
 sys.path.insert(0, sys.argv[1])
 import paper_1705_02003_b200 as uq
 cfg = uq.CONFIGS["C1"]
+S = int(sys.argv[3])
 f = uq.build_field(**cfg.field_kwargs())
 s = uq.EnsembleSolver2D(f, cfg.cells, cfg.tol, cfg.maxit)
-ys = np.random.default_rng(3).uniform(-1, 1, (4, cfg.ensemble_size, cfg.n_modes))
+ys = np.random.default_rng(3).uniform(-1, 1, (4, S, cfg.n_modes))
 r = s.solve_groups(ys)
 np.save(sys.argv[2], np.concatenate([r.iterations.ravel().astype(float), r.qoi.ravel()]))
 """
 
 
-@pytest.mark.parametrize("lanes", ["2", "1"])
-def test_tma_staged_spmv_bitwise_equals_register_path(tmp_path, lanes):
-    """The TMA-staged SpMV (default for the stencil) and the register-gather
-    SpMV produce identical bits through a whole batched solve."""
+@pytest.mark.parametrize("S", ["8", "7"])
+def test_csr_spmv_kernels_bitwise_equal_face_form(tmp_path, S):
+    """Whole batched launch-loop solves through the CSR operator - TMA-staged
+    values with and without the L2 band prefetch (S even), the register-gather
+    kernel (S odd: 1 lane per thread) - and through the face-form operator
+    produce identical bits."""
     import os
     import subprocess
     import sys
     from pathlib import Path
     root = str(Path(__file__).resolve().parents[1])
     out = {}
-    for tma, band in (("1", "1"), ("1", "0"), ("4", "1"), ("6", "1"), ("7", "1"), ("0", "0"),
-                      ("F", "F")):
-        env = dict(os.environ, UQG_SPMV_TMA=tma, UQG_BAND_HINT=band, UQG_LANES_PER_THREAD=lanes,
-                   UQG_PCG_PERSISTENT="0", UQG_FV2D_FACES="1" if tma == "F" else "0")
-        dst = tmp_path / f"r{tma}{band}.npy"
-        subprocess.run([sys.executable, "-c", _TMA_SCRIPT, root, str(dst)], env=env, check=True)
-        out[tma + band] = np.load(dst)
-    # value-staged (+L2 band prefetch), value-staged, warp-specialized, 2/4-stage TMA,
-    # face-form FV2D operator
-    for k in ("11", "10", "41", "61", "71", "FF"):
-        assert np.array_equal(out[k], out["00"]), k
+    for tag, faces, band in (("csr_band", "0", "1"), ("csr", "0", "0"), ("faces", "1", "1")):
+        env = dict(os.environ, UQG_BAND_HINT=band, UQG_PCG_PERSISTENT="0", UQG_FV2D_FACES=faces)
+        dst = tmp_path / f"{tag}.npy"
+        subprocess.run([sys.executable, "-c", _CSR_SCRIPT, root, str(dst), S], env=env, check=True)
+        out[tag] = np.load(dst)
+    assert np.array_equal(out["csr_band"], out["faces"])
+    assert np.array_equal(out["csr"], out["faces"])
 
 
 def test_empty_plan_and_level():
