@@ -703,12 +703,19 @@ def main():
         t_ms = ms[idx]
         gbs = nbytes / (t_ms / 1e3) / 1e9 if t_ms else None
         tr = traffic_all.get(f"{cfg.name}:{kname}", {})
+        gpl = tr.get("groups_per_launch") or 1
         per[key] = {"kernel": kname, "ms": t_ms, "achieved": gbs,
                     "frac": gbs / peak if gbs else None,
                     "group_launches": glaunch,
                     "bytes_per_group_launch": nbytes / glaunch if glaunch else None,
-                    "traffic": tr.get("dram_bytes_per_launch"),
-                    "traffic_algorithmic_same_launch": tr.get("algorithmic_bytes_per_launch"),
+                    # ncu DRAM bytes of one launch over `groups_per_launch` groups,
+                    # per group-launch like bytes_per_group_launch
+                    "traffic": (tr["dram_bytes_per_launch"] / gpl
+                                if tr.get("dram_bytes_per_launch") else None),
+                    "traffic_algorithmic_same_launch": (
+                        tr["algorithmic_bytes_per_launch"] / gpl
+                        if tr.get("algorithmic_bytes_per_launch") else None),
+                    "traffic_unit": "bytes per group-launch",
                     "traffic_source": tr.get("source")}
     if cnt[3] and not cnt[4] and not cnt[5]:
         # small batches: the whole solve is ONE persistent launch (cluster or
@@ -773,6 +780,8 @@ def main():
                      "achieved": per[dom]["achieved"], "peak": peak, "unit": "GB/s",
                      "frac": per[dom]["frac"], "traffic": per[dom]["traffic"],
                      "traffic_algorithmic_same_launch": per[dom]["traffic_algorithmic_same_launch"],
+                     "traffic_unit": "bytes per group-launch (ncu DRAM bytes of one launch / "
+                                     "its groups)",
                      "traffic_source": per[dom]["traffic_source"],
                      "peak_source": peak_src,
                      # also against the 8 TB/s HBM3e specification

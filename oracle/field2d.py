@@ -20,6 +20,7 @@ from dataclasses import dataclass
 
 import numpy as np
 import scipy.linalg
+from threadpoolctl import threadpool_limits
 
 
 @dataclass(frozen=True)
@@ -47,7 +48,8 @@ def nystrom_1d(delta: float, count: int, grid_points: int = 513) -> list[Mode1D]
     wts[[0, -1]] = step / 2.0
     root = np.sqrt(wts)
     kern = np.exp(-np.abs(xs[:, None] - xs[None, :]) / delta)
-    lam, vec = scipy.linalg.eigh(root[:, None] * kern * root[None, :])
+    with threadpool_limits(limits=1):  # as paper_1705_02003_b200.field: thread-independent bits
+        lam, vec = scipy.linalg.eigh(root[:, None] * kern * root[None, :])
     picked = np.argsort(lam)[::-1][:count]
     modes = []
     for col in picked:

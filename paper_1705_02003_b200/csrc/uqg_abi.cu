@@ -353,12 +353,30 @@ int uqg_kl_eval_sep2d(uqg_ctx* ctx, int n_cells, const double* table1d, int n_fa
   UQG_REQUIRE(a_hat_mode == 0 || a_hat_mode == 1, "unknown a_hat mode");
   UQG_REQUIRE(expansion == 0 || expansion == 1, "unknown expansion");
   const int n1 = n_cells + 1;
+  UQG_REQUIRE((long long)n1 * n1 < 0x7fffffffLL, "uqg_kl_eval_sep2d: too many nodes");
   const long long total = (long long)G * n1 * n1 * S;
   cudaStream_t s = as_stream(stream);
-  UQG_LAUNCH(UQG_K_KL, s,
-             kl_sep2d_kernel<<<grid_for(total, 256), 256, 0, s>>>(
-                 n1, table1d, mode_p, mode_q, sqrt_lam, M, samples, lane_ids, G, S, a_min,
-                 a_hat_mode, a_hat_value, expansion, a_out, ctx->status_dev));
+  // tiled contraction with the lane coefficients and the tile's mode values
+  // staged in shared memory; M x S too large to stage: per-element kernel
+  const size_t smem = ((size_t)M * S + S + (size_t)M * kKlTile) * sizeof(double);
+  static size_t opted = 48 * 1024;
+  if (smem > opted && smem <= 200 * 1024) {
+    UQG_TRY_CUDA(cudaFuncSetAttribute(kl_sep2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+    opted = smem;
+  }
+  if (smem <= opted) {
+    const dim3 grid((unsigned)((n1 * n1 + kKlTile - 1) / kKlTile), (unsigned)G);
+    UQG_LAUNCH(UQG_K_KL, s,
+               kl_sep2d_kernel<<<grid, 256, smem, s>>>(
+                   n1, table1d, mode_p, mode_q, sqrt_lam, M, samples, lane_ids, G, S, a_min,
+                   a_hat_mode, a_hat_value, expansion, a_out, ctx->status_dev));
+  } else {
+    UQG_LAUNCH(UQG_K_KL, s,
+               kl_sep2d_elem_kernel<<<grid_for(total, 256), 256, 0, s>>>(
+                   n1, table1d, mode_p, mode_q, sqrt_lam, M, samples, lane_ids, G, S, a_min,
+                   a_hat_mode, a_hat_value, expansion, a_out, ctx->status_dev));
+  }
   return UQG_OK;
 }
 

@@ -34,11 +34,68 @@ __device__ __forceinline__ double kl_finish(double e, int expansion, double a_mi
   return __dadd_rn(a_min, __dmul_rn(ahat, e));
 }
 
-// One thread per (group, node, lane); lanes fastest so the a_out store is
-// coalesced.  Mode values are rebuilt on the fly from the separable 1D tables
-// (one rounded product each, bit-identical to the host mode table), so the
-// (M x P) table never has to be streamed from HBM.
-__global__ void kl_sep2d_kernel(int n1, const double* __restrict__ table1d,
+// The KL contraction fluct(node, lane) = sum_m (y_m sqrt(lam_m)) * mv_m(node)
+// is a dense (P x M)(M x S) product per group followed by exp.  One CTA takes
+// one group and a tile of kKlTile consecutive nodes: the lane coefficients
+// c[m][s] = y_s[m] * sqrt(lam_m) and the tile's mode values mv[m][k] (rebuilt
+// from the separable 1D tables, one rounded product each - bit-identical to
+// the host mode table, so the (M x P) table is never streamed from HBM) are
+// staged in shared memory once; every (node, lane) element then runs the
+// M-term FMA chain in mode order from shared memory (mv broadcast across the
+// warp's lanes) and the exp, and the store of a[g][node][lane] is coalesced.
+// Same arithmetic, in the same order, as one thread per element recomputing
+// everything (kl_sep2d_elem_kernel, kept for M x S too large to stage): same
+// bits.  FP64-pipe bound (exp), not HBM bound: ncu in profiles/.
+__global__ void __launch_bounds__(256) kl_sep2d_kernel(
+    int n1, const double* __restrict__ table1d, const int* __restrict__ mode_p,
+    const int* __restrict__ mode_q, const double* __restrict__ sqrt_lam, int M,
+    const double* __restrict__ samples, const int* __restrict__ lane_ids, int G, int S,
+    double a_min, int a_hat_mode, double a_hat_value, int expansion, double* __restrict__ a_out,
+    int* status) {
+  extern __shared__ double kl_sm[];
+  double* c = kl_sm;             // [M][S]
+  double* ah = c + M * S;        // [S]
+  double* mv = ah + S;           // [M][kKlTile]
+  const int g = blockIdx.y, t = threadIdx.x, T = blockDim.x;
+  const int P = n1 * n1;
+  const int p0 = blockIdx.x * kKlTile;
+  const int tn = P - p0 < kKlTile ? P - p0 : kKlTile;
+  for (int e = t; e < M * S; e += T) {
+    const int m = e / S, s = e - m * S;
+    const size_t lane = (size_t)g * S + s;
+    const double* y = samples + (lane_ids ? (size_t)__ldg(&lane_ids[lane]) : lane) * M;
+    c[e] = __dmul_rn(y[m], __ldg(&sqrt_lam[m]));
+  }
+  for (int s = t; s < S; s += T) {
+    const size_t lane = (size_t)g * S + s;
+    const double* y = samples + (lane_ids ? (size_t)__ldg(&lane_ids[lane]) : lane) * M;
+    ah[s] = a_hat_of(y, M, a_hat_mode, a_hat_value);
+  }
+  for (int e = t; e < M * kKlTile; e += T) {
+    const int m = e / kKlTile, k = e - m * kKlTile;
+    if (k < tn) {
+      const int p = p0 + k, i = p / n1, j = p - i * n1;
+      mv[e] = __dmul_rn(__ldg(&table1d[(size_t)__ldg(&mode_p[m]) * n1 + i]),
+                        __ldg(&table1d[(size_t)__ldg(&mode_q[m]) * n1 + j]));
+    }
+  }
+  __syncthreads();
+  double* out = a_out + ((size_t)g * P + p0) * S;
+  bool bad = false;
+  for (int e = t; e < tn * S; e += T) {
+    const int k = e / S, s = e - k * S;
+    double acc = 0.0;
+    for (int m = 0; m < M; ++m) acc = __fma_rn(c[m * S + s], mv[m * kKlTile + k], acc);
+    const double a = kl_finish(acc, expansion, a_min, ah[s]);
+    bad |= a <= 0.0;
+    out[e] = a;
+  }
+  if (bad) atomicOr(status, 1);
+}
+
+// One thread per (group, node, lane), everything recomputed per element (for
+// M x S beyond the shared-memory staging of kl_sep2d_kernel; same bits).
+__global__ void kl_sep2d_elem_kernel(int n1, const double* __restrict__ table1d,
                                 const int* __restrict__ mode_p, const int* __restrict__ mode_q,
                                 const double* __restrict__ sqrt_lam, int M,
                                 const double* __restrict__ samples,

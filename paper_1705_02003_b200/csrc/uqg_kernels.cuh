@@ -119,7 +119,7 @@ struct PcgState {
   size_t pstride;
 };
 
-constexpr int kMaxKx = 4;  // deepest supported deferral
+constexpr int kMaxKx = 8;  // deepest supported deferral
 
 // Buffer slot of iteration `it`'s p / alpha.
 __device__ __forceinline__ int xslot(const PcgState& st, int it) {
@@ -132,6 +132,12 @@ __global__ void kl_sep2d_kernel(int n1, const double* table1d, const int* mode_p
                                 const double* samples, const int* lane_ids, int G, int S,
                                 double a_min, int a_hat_mode, double a_hat_value, int expansion,
                                 double* a_out, int* status);
+__global__ void kl_sep2d_elem_kernel(int n1, const double* table1d, const int* mode_p,
+                                const int* mode_q, const double* sqrt_lam, int M,
+                                const double* samples, const int* lane_ids, int G, int S,
+                                double a_min, int a_hat_mode, double a_hat_value, int expansion,
+                                double* a_out, int* status);
+constexpr int kKlTile = 64;  // nodes per CTA of kl_sep2d_kernel
 __global__ void kl_table_kernel(const double* modes, int P, int M, const double* sqrt_lam,
                                 const double* samples, int L, double a_min, int a_hat_mode,
                                 double a_hat_value, int expansion, double* a_out, int* status);

@@ -621,10 +621,14 @@ __global__ void __launch_bounds__(256, 3) pcg_dir_kernel(long long N, Geo geo, P
 // iterations of every group not yet DONE - before pcg_dir overwrites the
 // oldest p buffer.  Otherwise (after the loop): the it % kx updates still
 // pending for each group.
-template <int V>
+// KX: the deepest window this instantiation handles (4 or 8 p buffers); the
+// 4-deep kernel streams two tiles per step, the 8-deep one a single tile (the
+// window's p values already keep 8 loads per thread in flight).
+template <int V, int KX>
 __global__ void __launch_bounds__(256, 2) pcg_flush_kernel(long long N, Geo geo, PcgState st,
                                                      double* __restrict__ x,
                                                      const double* __restrict__ p, int in_loop) {
+  constexpr int U = KX <= 4 ? 2 : 1;  // tiles per step
   const int g = blockIdx.y, t = threadIdx.x;
   const int it = st.it[g], kx = st.kx;
   const int n = in_loop ? ((st.done[g] != kDone && it % kx == 0) ? kx : 0) : it % kx;
@@ -632,10 +636,10 @@ __global__ void __launch_bounds__(256, 2) pcg_flush_kernel(long long N, Geo geo,
   if (n == 0 || sl >= geo.L) return;
   const size_t base = (size_t)g * N * S + V * sl, GS = (size_t)st.G * S;
   const size_t l0 = (size_t)g * S + V * sl;
-  double aj[kMaxKx][V];
-  const double* pj[kMaxKx];
+  double aj[KX][V];
+  const double* pj[KX];
 #pragma unroll
-  for (int q = 0; q < kMaxKx; ++q) {  // oldest first: j = it - n + q
+  for (int q = 0; q < KX; ++q) {  // oldest first: j = it - n + q
     const int sj = q < n ? xslot(st, it - n + q) : 0;
     pj[q] = p + (size_t)sj * st.pstride;
 #pragma unroll
@@ -643,28 +647,28 @@ __global__ void __launch_bounds__(256, 2) pcg_flush_kernel(long long N, Geo geo,
   }
   for (int chunk = blockIdx.x; chunk < geo.chunks; chunk += gridDim.x) {
     const ChunkRows cr = chunk_tiles(geo, chunk);
-    // two tiles per step: all loads of both are issued before any store
-    for (long long tile = cr.t0; tile < cr.t1; tile += 2) {
-      double xv[2][V], pv[2][kMaxKx][V];
-      bool ok[2];
-      size_t o[2];
+    // U tiles per step: all loads of the step are issued before any store
+    for (long long tile = cr.t0; tile < cr.t1; tile += U) {
+      double xv[U][V], pv[U][KX][V];
+      bool ok[U];
+      size_t o[U];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < U; ++u) {
         const long long row = (tile + u) * geo.R + rr;
         ok[u] = tile + u < cr.t1 && row < N;
         o[u] = base + (ok[u] ? row : 0) * S;
         if (ok[u]) {
           ldv<V>(x + o[u], xv[u]);
 #pragma unroll
-          for (int q = 0; q < kMaxKx; ++q)
+          for (int q = 0; q < KX; ++q)
             if (q < n) ldv<V>(pj[q] + o[u], pv[u][q]);
         }
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < U; ++u) {
         if (!ok[u]) continue;
 #pragma unroll
-        for (int q = 0; q < kMaxKx; ++q)
+        for (int q = 0; q < KX; ++q)
           if (q < n)
 #pragma unroll
             for (int j = 0; j < V; ++j)
@@ -1021,7 +1025,17 @@ void launch_pcg_update(const Geo& geo, int G, cudaStream_t s, long long N, const
 void launch_pcg_flush(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,
                       double* x, const double* p, bool in_loop) {
   const Geo& gl = geo;  // B preset by the caller
-  UQG_DISPATCH_V(gl, pcg_flush_kernel, dim3(gl.B, G), 0, s, N, gl, st, x, p, in_loop ? 1 : 0);
+  const int il = in_loop ? 1 : 0;
+  if (st.kx <= 4) {
+    if (gl.V == 2)
+      pcg_flush_kernel<2, 4><<<dim3(gl.B, G), gl.T, 0, s>>>(N, gl, st, x, p, il);
+    else
+      pcg_flush_kernel<1, 4><<<dim3(gl.B, G), gl.T, 0, s>>>(N, gl, st, x, p, il);
+  } else if (gl.V == 2) {
+    pcg_flush_kernel<2, 8><<<dim3(gl.B, G), gl.T, 0, s>>>(N, gl, st, x, p, il);
+  } else {
+    pcg_flush_kernel<1, 8><<<dim3(gl.B, G), gl.T, 0, s>>>(N, gl, st, x, p, il);
+  }
 }
 
 void launch_pcg_dir(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,

@@ -23,6 +23,7 @@ from dataclasses import dataclass
 
 import numpy as np
 import scipy.linalg
+from threadpoolctl import threadpool_limits
 
 from . import _lib
 from .errors import FieldError
@@ -56,7 +57,14 @@ def eigenpairs_1d(delta: float, count: int, grid_points: int = 513) -> list[Eige
     w[0] = w[-1] = h / 2.0
     sw = np.sqrt(w)
     kmat = sw[:, None] * np.exp(-np.abs(grid[:, None] - grid[None, :]) / delta) * sw[None, :]
-    evals, evecs = scipy.linalg.eigh(kmat)
+    # LAPACK's eigh rounds differently with the BLAS thread count (OpenBLAS
+    # blocks by thread): pinned to one thread, the field - and every bit
+    # downstream of it - is the same on every host and under torchrun (which
+    # sets OMP_NUM_THREADS=1), so N-GPU results equal 1-GPU results bitwise.
+    # The reference's eigenpairs equal these bits when it runs single-threaded
+    # too (tests/golden/eigen.npz is generated that way).
+    with threadpool_limits(limits=1):
+        evals, evecs = scipy.linalg.eigh(kmat)
     out = []
     for k in np.argsort(evals)[::-1][:count]:
         v = evecs[:, k] / sw

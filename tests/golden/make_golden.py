@@ -117,9 +117,14 @@ def grouping_cases():
 
 
 def eigen_cases():
+    """The reference's eigenpairs, computed single-threaded (LAPACK's eigh
+    rounds differently with the BLAS thread count; the drop-in pins one)."""
+    from threadpoolctl import threadpool_limits
+
     out = {}
     for delta in (0.2, 0.1, 0.05, 0.25):
-        pairs = ref_rf.eigenpairs_1d(delta, 12, 513)
+        with threadpool_limits(limits=1):
+            pairs = ref_rf.eigenpairs_1d(delta, 12, 513)
         out[f"lam_{delta}"] = np.array([p.eigenvalue for p in pairs])
         out[f"vec_{delta}"] = np.stack([p.values for p in pairs])
     np.savez_compressed(HERE / "eigen.npz", **out)

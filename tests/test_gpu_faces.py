@@ -109,7 +109,7 @@ def test_deferred_x_update_bitwise(tmp_path):
     FLUSH iterations + pcg_flush) rounds in the same order as the per-iteration
     update: every kx gives the bits of kx = 1, CSR and face operator, launch loop."""
     outs = {}
-    for kx in ("1", "2", "3", "4"):
+    for kx in ("1", "2", "3", "4", "8"):
         for graph in ("0", "1"):  # host-polled / graph launch loop
             env = dict(os.environ, UQG_PCG_PERSISTENT="0", UQG_X_DEFER=kx, UQG_PCG_GRAPH=graph)
             dst = tmp_path / f"x{kx}{graph}.npy"

@@ -242,6 +242,24 @@ def test_kl_nodes_match_oracle(cells, M, delta, sigma, S):
     np.testing.assert_allclose(f.eval_a_batch(None, ys[:S], tab), want[:S], rtol=1e-14)
 
 
+def test_kl_tiled_contraction_bitwise_equals_per_element_kernel():
+    """kl_sep2d_kernel (lane coefficients + tile mode values staged in shared
+    memory) and kl_sep2d_elem_kernel (per-element recompute; taken when
+    M x S is too large to stage) run the same FMA chain: bit-identical lanes.
+    S = 8 takes the tiled kernel, S = 512 with M = 56 the per-element one;
+    lanes 0..7 of both carry the same samples."""
+    M, cells = 56, 6
+    f = uq.build_field(0.1, 1.0, M, 0.0)
+    mesh = uq.StructuredMesh2D(cells)
+    P = mesh.n_nodes
+    ys = np.random.default_rng(4).uniform(-1, 1, (512, M))
+    small = kl_nodes(FieldTables(f, mesh), _lib.to_dev(ys[:8]), 1, 8)
+    big = kl_nodes(FieldTables(f, mesh), _lib.to_dev(ys), 1, 512)
+    a = small.reshape(P, 8).cpu().numpy()
+    b = big.reshape(P, 512).cpu().numpy()[:, :8]
+    assert np.array_equal(a, b)
+
+
 def test_assembly_bitwise_given_nodal_coefficients(fv2d_golden):
     g = fv2d_golden
     mesh = uq.StructuredMesh2D(8)
