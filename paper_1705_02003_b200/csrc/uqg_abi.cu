@@ -167,7 +167,7 @@ int persistent_mode() {
 int x_defer() {
   static const int k = [] {
     const char* e = getenv("UQG_X_DEFER");
-    const int v = e ? atoi(e) : 4;
+    const int v = e ? atoi(e) : 8;
     return v < 1 ? 1 : (v > kMaxKx ? kMaxKx : v);
   }();
   return k;
@@ -358,7 +358,7 @@ int uqg_kl_eval_sep2d(uqg_ctx* ctx, int n_cells, const double* table1d, int n_fa
   cudaStream_t s = as_stream(stream);
   // tiled contraction with the lane coefficients and the tile's mode values
   // staged in shared memory; M x S too large to stage: per-element kernel
-  const size_t smem = ((size_t)M * S + S + (size_t)M * kKlTile) * sizeof(double);
+  const size_t smem = ((size_t)M * S + S + 1 + (size_t)M * kKlTile) * sizeof(double);
   static size_t opted = 48 * 1024;
   if (smem > opted && smem <= 200 * 1024) {
     UQG_TRY_CUDA(cudaFuncSetAttribute(kl_sep2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

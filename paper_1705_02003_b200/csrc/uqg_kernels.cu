@@ -53,9 +53,9 @@ __global__ void __launch_bounds__(256) kl_sep2d_kernel(
     double a_min, int a_hat_mode, double a_hat_value, int expansion, double* __restrict__ a_out,
     int* status) {
   extern __shared__ double kl_sm[];
-  double* c = kl_sm;             // [M][S]
-  double* ah = c + M * S;        // [S]
-  double* mv = ah + S;           // [M][kKlTile]
+  double* c = kl_sm;                          // [M][S]
+  double* ah = c + M * S;                     // [S]
+  double* mv = ah + S + ((M * S + S) & 1);    // [M][kKlTile], 16-byte aligned
   const int g = blockIdx.y, t = threadIdx.x, T = blockDim.x;
   const int P = n1 * n1;
   const int p0 = blockIdx.x * kKlTile;
@@ -82,13 +82,41 @@ __global__ void __launch_bounds__(256) kl_sep2d_kernel(
   __syncthreads();
   double* out = a_out + ((size_t)g * P + p0) * S;
   bool bad = false;
-  for (int e = t; e < tn * S; e += T) {
-    const int k = e / S, s = e - k * S;
-    double acc = 0.0;
-    for (int m = 0; m < M; ++m) acc = __fma_rn(c[m * S + s], mv[m * kKlTile + k], acc);
-    const double a = kl_finish(acc, expansion, a_min, ah[s]);
-    bad |= a <= 0.0;
-    out[e] = a;
+  if (S <= T && T % S == 0) {
+    // register blocking: a thread owns lane s and 4 consecutive nodes, so each
+    // mode step is one c load (per lane) and two 16-byte mv loads (broadcast
+    // across the lanes) for 4 FMAs - the chain per element is unchanged
+    const int s = t % S, kr = t / S, RP = T / S;
+    const double cs_ah = ah[s];
+    for (int k0 = 4 * kr; k0 < tn; k0 += 4 * RP) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int m = 0; m < M; ++m) {
+        const double cm = c[m * S + s];
+        const double2 v01 = *reinterpret_cast<const double2*>(&mv[m * kKlTile + k0]);
+        const double2 v23 = *reinterpret_cast<const double2*>(&mv[m * kKlTile + k0 + 2]);
+        acc[0] = __fma_rn(cm, v01.x, acc[0]);
+        acc[1] = __fma_rn(cm, v01.y, acc[1]);
+        acc[2] = __fma_rn(cm, v23.x, acc[2]);
+        acc[3] = __fma_rn(cm, v23.y, acc[3]);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (k0 + q < tn) {
+          const double a = kl_finish(acc[q], expansion, a_min, cs_ah);
+          bad |= a <= 0.0;
+          out[(size_t)(k0 + q) * S + s] = a;
+        }
+      }
+    }
+  } else {
+    for (int e = t; e < tn * S; e += T) {
+      const int k = e / S, s = e - k * S;
+      double acc = 0.0;
+      for (int m = 0; m < M; ++m) acc = __fma_rn(c[m * S + s], mv[m * kKlTile + k], acc);
+      const double a = kl_finish(acc, expansion, a_min, ah[s]);
+      bad |= a <= 0.0;
+      out[e] = a;
+    }
   }
   if (bad) atomicOr(status, 1);
 }

@@ -137,7 +137,7 @@ __global__ void kl_sep2d_elem_kernel(int n1, const double* table1d, const int* m
                                 const double* samples, const int* lane_ids, int G, int S,
                                 double a_min, int a_hat_mode, double a_hat_value, int expansion,
                                 double* a_out, int* status);
-constexpr int kKlTile = 64;  // nodes per CTA of kl_sep2d_kernel
+constexpr int kKlTile = 128;  // nodes per CTA of kl_sep2d_kernel (multiple of 4)
 __global__ void kl_table_kernel(const double* modes, int P, int M, const double* sqrt_lam,
                                 const double* samples, int L, double a_min, int a_hat_mode,
                                 double a_hat_value, int expansion, double* a_out, int* status);
