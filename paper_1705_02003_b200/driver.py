@@ -34,6 +34,12 @@ class LevelRecord:
     iterations: dict
     qois: dict
     notes: list = dc_field(default_factory=list)
+    # run-report fields (harness.py:439-524): QoI-channel error indicator after
+    # the level's fit, the budget flag of the refinement that made the level,
+    # and the per-sample anisotropy indicator (adaptive_run(indicators=True))
+    error_indicator: float | None = None
+    budget_truncated: bool = False
+    indicator: np.ndarray | None = None
 
 
 def sample_set(cfg: StudyConfig) -> np.ndarray:
@@ -43,7 +49,7 @@ def sample_set(cfg: StudyConfig) -> np.ndarray:
 
 def adaptive_run(cfg: StudyConfig, solver: EnsembleSolver | None = None, shard=None,
                  max_levels: int | None = None, device_keys: bool = False,
-                 residual_sink=None):
+                 residual_sink=None, indicators: bool = False):
     """Run the grouped adaptive loop; returns (records, stop_reason, grid).
 
     ``shard``: optional callable(plan, coords_by_id) -> (iters, qois, notes)
@@ -55,6 +61,11 @@ def adaptive_run(cfg: StudyConfig, solver: EnsembleSolver | None = None, shard=N
     ``residual_sink(level, ensemble, history)``: per-ensemble lane residual
     histories, as the reference's ``adaptive_run(residual_sink=...)``
     (``report.residual_sink`` writes the reference's CSVs).
+    ``indicators``: record each sample's anisotropy indicator on the device
+    (``harness.py:616``; the run report's ``indicator`` column).  The
+    reference's budget notes ("level L truncated to the n_max=... sample
+    budget") are appended to the notes of the level whose refinement
+    truncated the next one, so concatenated notes keep the reference's order.
     """
     if solver is None and shard is None:
         solver = cfg.make_solver()
@@ -70,7 +81,14 @@ def adaptive_run(cfg: StudyConfig, solver: EnsembleSolver | None = None, shard=N
     if len(batch) > cfg.n_max:
         raise ValueError(f"n_max={cfg.n_max} is smaller than the {len(batch)}-point initial grid")
     cap = cfg.max_levels if max_levels is None else max_levels
-    records, level, stop = [], 0, None
+    records, level, stop, truncated = [], 0, None, False
+    probe = None
+    if indicators:
+        from .field import anisotropy_indicators
+
+        op = solver.op
+        probe = (op.field, op.indicator_points())
+        probe = probe + (op.field.mode_values(probe[1]),)
     while True:
         level += 1
         start = len(grid) - len(batch)
@@ -85,11 +103,14 @@ def adaptive_run(cfg: StudyConfig, solver: EnsembleSolver | None = None, shard=N
                 ITER, coords, n_nodes=start)
             plan = group_by_key(ids, {sid: float(predicted[i]) for i, sid in enumerate(ids)}, S,
                                 level, "sur")
+        ind = None if probe is None else anisotropy_indicators(probe[0], coords, probe[1],
+                                                                probe[2])
         iters, qois, notes = solve(plan, coords_by_id)
         grid.fit(QOI, {sid: qois[sid] for sid in ids})
         (grid.fit_device if device_keys else grid.fit)(ITER, {sid: iters[sid] for sid in ids})
         records.append(LevelRecord(level, ids, coords, predicted, plan.ensembles, plan.padding,
-                                   iters, qois, notes))
+                                   iters, qois, list(notes), grid.error_indicator(QOI),
+                                   truncated, ind))
         if level >= cap:
             stop = "level_cap"
             break
@@ -97,5 +118,9 @@ def adaptive_run(cfg: StudyConfig, solver: EnsembleSolver | None = None, shard=N
         if not new:
             stop = "budget_exhausted" if exhausted else "tolerance_met"
             break
+        truncated = exhausted
+        if truncated:
+            records[-1].notes.append(
+                f"level {level + 1} truncated to the n_max={cfg.n_max} sample budget")
         batch = new
     return records, stop, grid

@@ -92,6 +92,10 @@ class FV2DOperator:
     def band_hint(self):
         return self.mesh.band_hint()
 
+    def indicator_points(self):
+        """Probe points of the anisotropy indicator: the KL nodes."""
+        return self.mesh.node_coords()
+
     def coefficients(self, d_samples, lane_ids, G, S, out):
         kl_nodes(self.tables, d_samples, G, S, out=out, lane_ids=lane_ids)
 
@@ -121,6 +125,11 @@ class FEM3DOperator:
     def graph(self):
         rowptr, col, _ = self.mesh.device()
         return rowptr, col
+
+    def indicator_points(self):
+        """Probe points of the anisotropy indicator: the Gauss points
+        (``harness.py:393-397``)."""
+        return self.mesh.quad_points
 
     def coefficients(self, d_samples, lane_ids, G, S, out):
         f, c = self.field, self.consts

@@ -464,8 +464,9 @@ def refrun_outputs():
                        "--n-max", "60", "--mesh-cells", "6", "--dump-residuals",
                        "--out-dir", tmp])
         assert rc in (0, 2)  # 2: stopped on the budget, outputs complete
-        for name in ("iterations_by_level.csv", "residuals_level1_ens0.csv",
-                     "residuals_level1_ens11.csv", "residuals_level2_ens0.csv"):
+        for name in ("iterations_by_level.csv", "r_table.csv", "manifest.json",
+                     "residuals_level1_ens0.csv", "residuals_level1_ens11.csv",
+                     "residuals_level2_ens0.csv"):
             shutil.copy(Path(tmp) / name, dst / name)
         n = len(list(Path(tmp).glob("residuals_level*_ens*.csv")))
         (dst / "README").write_text(

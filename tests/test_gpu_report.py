@@ -19,9 +19,9 @@ import pytest
 
 import paper_1705_02003_b200 as uq
 from paper_1705_02003_b200.driver import adaptive_run
-from paper_1705_02003_b200.report import residual_sink, write_iterations_by_level
+from paper_1705_02003_b200.report import emit_reports, residual_sink
 
-from conftest import GOLDEN
+from conftest import GOLDEN, ROOT
 
 pytestmark = pytest.mark.gpu
 REF = GOLDEN / "refrun_pde_test1"
@@ -29,8 +29,10 @@ REF = GOLDEN / "refrun_pde_test1"
 
 def _run(out):
     cfg = dataclasses.replace(uq.PRESETS_3D["pde_test1"], cells=6, n_max=60)
-    records, stop, _ = adaptive_run(cfg, residual_sink=residual_sink(out, cfg.ensemble_size))
-    write_iterations_by_level(records, out)
+    records, stop, grid = adaptive_run(cfg, residual_sink=residual_sink(out, cfg.ensemble_size),
+                                       indicators=True)
+    notes = [n for r in records for n in r.notes]
+    emit_reports(cfg, records, stop, grid, out, notes, dump_residuals=True)
     return stop
 
 
@@ -62,3 +64,56 @@ def test_device_study_emits_reference_files(tmp_path):
     assert files == sorted(p.name for p in b.iterdir()) and len(files) > 10
     for name in files:
         assert (a / name).read_bytes() == (b / name).read_bytes(), name
+
+
+def test_device_run_report_matches_reference(tmp_path):
+    """r_table.csv and manifest.json of the device study (harness.py:741-782)
+    against the reference CLI's: same levels, sample ids, coordinates, plans
+    on level 1, counts in the envelope, anisotropy indicators to 1e-12, QoI-
+    channel error indicators and surpluses to rounding; the manifest parses
+    with the reference's own parse_manifest."""
+    import json
+    import sys
+
+    out = tmp_path / "run"
+    _run(out)
+    mine = list(csv.reader((out / "r_table.csv").read_text().splitlines()))
+    ref = list(csv.reader((REF / "r_table.csv").read_text().splitlines()))
+    assert len(mine) == len(ref) and mine[0] == ref[0]
+    for m, r in zip(mine[1:], ref[1:]):
+        assert m[:5] == r[:5]
+        for a, b in ((m[5], r[5]), (m[6], r[6])):
+            assert (a == "") == (b == "")
+            if b:
+                assert abs(float(a) - float(b)) <= 0.05 * float(b)
+    doc = json.loads((out / "manifest.json").read_text())["reports"][0]
+    rep = json.loads((REF / "manifest.json").read_text())["reports"][0]
+    assert doc["config"] == rep["config"]
+    assert doc["stop_reason"] == rep["stop_reason"] and doc["notes"] == rep["notes"]
+    assert len(doc["levels"]) == len(rep["levels"])
+    for a, b in zip(doc["levels"], rep["levels"]):
+        assert a["level"] == b["level"] and a["budget_truncated"] == b["budget_truncated"]
+        assert [s["sample_id"] for s in a["samples"]] == [s["sample_id"] for s in b["samples"]]
+        for sa, sb in zip(a["samples"], b["samples"]):
+            assert sa["coords"] == sb["coords"]
+            assert abs(sa["iterations"] - sb["iterations"]) <= 1
+            assert abs(sa["indicator"] - sb["indicator"]) <= 1e-12 * abs(sb["indicator"])
+        np.testing.assert_allclose(a["error_indicator"], b["error_indicator"], rtol=1e-5)
+    pa, pb = doc["levels"][0]["plans"][0], rep["levels"][0]["plans"][0]
+    assert (pa["ensembles"], pa["padding"]) == (pb["ensembles"], pb["padding"])
+    assert abs(pa["R_l"] - pb["R_l"]) <= 0.05 * pb["R_l"]   # counts within the envelope
+    na, nb = doc["grid"]["nodes"], rep["grid"]["nodes"]
+    assert [(n["level"], n["index"], n["coords"]) for n in na] == \
+        [(n["level"], n["index"], n["coords"]) for n in nb]
+    qa = np.array([n["surpluses"]["qoi"] for n in na], dtype=float)
+    qb = np.array([n["surpluses"]["qoi"] for n in nb], dtype=float)
+    np.testing.assert_allclose(qa, qb, rtol=1e-6, atol=1e-9 * np.nanmax(np.abs(qb)))
+    ref_pkg = ROOT / "baseline" / "_ref"
+    if (ref_pkg / "uqgroup").exists():
+        sys.path.insert(0, str(ref_pkg))
+        try:
+            from uqgroup.harness import parse_manifest
+            (parsed,) = parse_manifest(out / "manifest.json")
+        finally:
+            sys.path.remove(str(ref_pkg))
+        assert parsed.stop_reason == "budget_exhausted" and len(parsed.levels) == len(rep["levels"])
