@@ -151,8 +151,8 @@ struct PersistBufs {
 };
 thread_local PersistBufs g_persist;
 
-// UQG_PCG_PERSISTENT: 3 = smem-resident cluster kernel, 2 = cluster kernel,
-// 1 = cooperative kernel (when co-resident), 0 = never, unset = auto
+// UQG_PCG_PERSISTENT: 2 = cluster kernel, 1 = cooperative kernel (when
+// co-resident), 0 = never, unset = auto
 // (small batches: the launch-per-phase loop would be latency-bound).
 int persistent_mode() {
   static const int m = [] {
@@ -612,11 +612,9 @@ int pcg_impl(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const 
   cudaStream_t s = as_stream(stream);
   Geo geo = make_geo(N, S, max_row_len);
   // Small batches: one cooperative launch runs the whole solve (uqg_persistent.cu).
-  // UQG_PCG_PERSISTENT: 3 = shared-memory-resident cluster kernel (face form),
-  // 2 = cluster-barrier kernel, 1 = cooperative kernel, 0 = launch loop;
-  // auto = cluster kernel for small batches (< 512 MB per iteration) - the
-  // shared-memory-resident one when the group fits its cluster - and the
-  // launch loop otherwise.
+  // UQG_PCG_PERSISTENT: 2 = cluster-barrier kernel, 1 = cooperative kernel,
+  // 0 = launch loop; auto = cluster kernel for small batches (< 512 MB per
+  // iteration), launch loop otherwise.
   const int pmode = persistent_mode();
   const double op_elems = op.fv.tx ? (double)(N + op.fv.m) * (op.fv.ty ? 2 : 1) : (double)nnz;
   const double iter_bytes = 8.0 * S * (op_elems + 12.0 * N) * G;
@@ -633,14 +631,6 @@ int pcg_impl(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const 
   }
   if (!use_cluster && geo.sc == 1 && (pmode == 1 || (pmode < 0 && small)))
     pblocks = persistent_blocks(geo, G);
-  // the group's whole state in its cluster's shared memory (face form with
-  // constant y-faces): mode 3, or auto whenever the cluster kernel is chosen
-  int smem_nb = 0;
-  size_t smem_bytes = 0;
-  if (op.fv.tx && !op.fv.ty && geo.sc == 1 &&
-      (pmode == 3 || (pmode < 0 && use_cluster)))
-    smem_nb = cluster_smem_size(geo, N, op.fv.m, &smem_bytes);
-  if (smem_nb > 0 && pblocks == 0) pblocks = smem_nb;
   // workspace: the persistent kernel updates x in place (kx = 1)
   const int kx = pblocks > 0 ? 1 : x_defer();
   int P = 1;  // concurrent parts of the launch loop
@@ -732,14 +722,10 @@ int pcg_impl(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const 
     UQG_TRY_CUDA(cudaMemsetAsync(pb.bar, 0, (2 * (size_t)G + 1) * sizeof(unsigned), s));
     cudaError_t le = cudaSuccess;
     UQG_LAUNCH(UQG_K_PCG_SPMV, s, {
-      if (smem_nb > 0)
-        le = launch_pcg_cluster_smem(geo, G, smem_nb, smem_bytes, s, N, st, op.fv, rhs,
-                                     rhs_const, dinv, tol, maxit, x);
-      else
-        le = launch_pcg_persistent(geo, G, pblocks, use_cluster, s, N, nnz, st, op.ro, op.ci,
-                                   op.vals, op.fv, rhs, rhs_const, dinv, tol, maxit, x, r, p,
-                                   ap, pb.partA, st.part, pb.bar, pb.bar + G,
-                                   reinterpret_cast<int*>(pb.bar + 2 * G));
+      le = launch_pcg_persistent(geo, G, pblocks, use_cluster, s, N, nnz, st, op.ro, op.ci,
+                                 op.vals, op.fv, rhs, rhs_const, dinv, tol, maxit, x, r, p, ap,
+                                 pb.partA, st.part, pb.bar, pb.bar + G,
+                                 reinterpret_cast<int*>(pb.bar + 2 * G));
     });
     if (le != cudaSuccess) {
       cudaGetLastError();

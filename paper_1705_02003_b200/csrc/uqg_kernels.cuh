@@ -202,13 +202,6 @@ void launch_anisotropy(cudaStream_t s, const double* modes, int P, int M, const 
 // uqg_persistent.cu: whole-solve cooperative kernel for small batches
 int persistent_blocks(const Geo& geo, int G);
 int persistent_cluster_size(const Geo& geo);
-// smem-resident cluster kernel (face form, constant y-faces): CTAs per group
-// and shared-memory bytes, 0 if the group does not fit
-int cluster_smem_size(const Geo& geo, long long N, int m, size_t* smem_out);
-cudaError_t launch_pcg_cluster_smem(const Geo& geo, int G, int nb, size_t smem, cudaStream_t s,
-                                    long long N, const PcgState& st, const Fv2dOp& fv,
-                                    const double* rhs, double rhs_const, const double* dinv,
-                                    double tol, int maxit, double* x);
 cudaError_t launch_pcg_persistent(const Geo& geo, int G, int blocks, bool cluster, cudaStream_t s,
                                   long long N, long long nnz, const PcgState& st, const int* ro,
                                   const int* ci, const double* vals, const Fv2dOp& fv,

@@ -20,8 +20,6 @@
 #include <float.h>
 #include <math.h>
 
-#include <cooperative_groups.h>
-
 #include "uqg_common.cuh"
 #include "uqg_kernels.cuh"
 
@@ -416,525 +414,6 @@ __global__ void __launch_bounds__(256, 4) pcg_persistent_kernel(
       atomicAdd(st.ndone, 1);
     }
   }
-}
-
-// ---------------------------------------------------------------------------
-// Shared-memory-resident cluster PCG (face-form FV2D operator, small groups:
-// the C1 oracle case).  A group is one thread-block cluster of NB CTAs and
-// each CTA OWNS a contiguous run of reduction chunks: its rows of x, r, p (two
-// buffers), Ap and dinv and the x-faces they touch live in its shared memory
-// for the whole solve.  Cross-CTA traffic goes through distributed shared
-// memory (DSMEM, ld.shared::cluster via map_shared_rank):
-//   * chunk partials: each CTA keeps its chunks' partials; after the cluster
-//     barrier every CTA sums all partials in the canonical order (same trees
-//     as finish_chunks / final_partials), so every CTA holds the same lane
-//     state without a broadcast;
-//   * the SpMV's p halo (rows within m of the CTA's range): the direction
-//     step forms p_{k+1} for the halo rows itself from the owner's r and p_k
-//     (read over DSMEM; dinv's halo is a local copy), so the next SpMV needs
-//     no barrier: two cluster barriers per iteration (after the SpMV partials
-//     and after the update partials) instead of three.
-// Hazards: p is double-buffered (a neighbour still reads p_k while p_{k+1} is
-// written); r of iteration k+1 is written after barrier 1 of k+1, which every
-// CTA reaches only after its halo reads of r_k; partial buffers are rewritten
-// one barrier after their last remote read.
-// Arithmetic and reduction order are those of the launch loop (x += alpha p
-// moves into the update phase: the same values, so the same bits).
-
-namespace cg = cooperative_groups;
-
-struct SmemPlan {  // per-CTA shared-memory layout (doubles unless noted)
-  int ncl;         // max chunks per CTA
-  int nr;          // max rows per CTA
-  int hm;          // halo rows on each side (min(m, N))
-  size_t bytes;
-};
-
-__host__ __device__ inline SmemPlan smem_plan(const Geo& geo, int m, long long N, int nb) {
-  SmemPlan sp;
-  sp.ncl = (geo.chunks + nb - 1) / nb;
-  sp.nr = (int)(sp.ncl * geo.chunk_tiles * geo.R);
-  sp.hm = (int)(m < N ? m : N);
-  const size_t S = geo.S;
-  size_t d = 0;
-  d += 6 * (size_t)sp.nr * S;             // x, r, p0, p1, ap, dinv
-  d += (size_t)(sp.nr + m) * S;           // x-faces of the CTA's rows (w: row, e: row + m)
-  d += 4 * (size_t)sp.hm * S;             // p halo (west, east) + dinv halo (west, east)
-  d += 3 * (size_t)sp.ncl * S;            // partials: p.Ap, (r.r, r.z)
-  d += (size_t)sp.ncl * 2 * geo.V * geo.T;  // batched in-block trees
-  d += 4 * S;                             // alpha, beta, rz, thr
-  sp.bytes = d * sizeof(double) + S * (sizeof(int) + 2) + 64;
-  return sp;
-}
-
-__device__ __forceinline__ int chunk_lo(int C, int nb, int b) {
-  return C * b / nb;  // C <= kMaxChunks, nb <= 16: no overflow
-}
-__device__ __forceinline__ int chunk_owner(int C, int nb, int c) {
-  int b = c * nb / C;
-  while (b + 1 < nb && chunk_lo(C, nb, b + 1) <= c) ++b;
-  while (b > 0 && chunk_lo(C, nb, b) > c) --b;
-  return b;
-}
-
-template <int V>
-__global__ void __launch_bounds__(256, 1) pcg_cluster_smem_kernel(
-    long long N_ll, Geo geo, PcgState st, Fv2dOp fv, const double* __restrict__ rhs,
-    double rhs_const, const double* __restrict__ dinv_g, double tol, int maxit,
-    double* __restrict__ x_g) {
-  extern __shared__ __align__(16) double sm[];
-  cg::cluster_group cluster = cg::this_cluster();
-  const int N = (int)N_ll, m = fv.m;
-  const int g = blockIdx.y, t = threadIdx.x, b = (int)cluster.block_rank();
-  const int nb = (int)cluster.num_blocks();
-  const int S = geo.S, T = geo.T, L = geo.L, Lp = geo.Lp, R = geo.R, C = geo.chunks;
-  const int CR = (int)(geo.chunk_tiles * R);  // rows per chunk
-  const int sl = t % Lp, rr = t / Lp;
-  const SmemPlan sp = smem_plan(geo, m, N, nb);
-  const int c0 = chunk_lo(C, nb, b), c1 = chunk_lo(C, nb, b + 1), ncl = c1 - c0;
-  const int row0 = c0 * CR;
-  int row1 = c1 * CR;
-  if (row1 > N) row1 = N;
-  const int hm = sp.hm;
-  // layout (identical in every CTA, so DSMEM offsets are the owner's local ones)
-  double* xs = sm;
-  double* rs = xs + (size_t)sp.nr * S;
-  double* pb[2] = {rs + (size_t)sp.nr * S, rs + 2 * (size_t)sp.nr * S};
-  double* aps = pb[1] + (size_t)sp.nr * S;
-  double* ds = aps + (size_t)sp.nr * S;
-  double* txs = ds + (size_t)sp.nr * S;
-  double* hw = txs + (size_t)(sp.nr + m) * S;   // p halo rows [row0 - hm, row0)
-  double* he = hw + (size_t)hm * S;             // p halo rows [row1, row1 + hm)
-  double* hdw = he + (size_t)hm * S;
-  double* hde = hdw + (size_t)hm * S;
-  double* pA = hde + (size_t)hm * S;            // [ncl][S]
-  double* pB = pA + (size_t)sp.ncl * S;         // [ncl][2][S]
-  double* red = pB + 2 * (size_t)sp.ncl * S;    // [ncl * 2 * V][T]
-  double* la = red + (size_t)sp.ncl * 2 * V * T;
-  double* lb = la + S;
-  double* lrz = lb + S;
-  double* lthr = lrz + S;
-  int* lit = reinterpret_cast<int*>(lthr + S);
-  unsigned char* lconv = reinterpret_cast<unsigned char*>(lit + S);
-  unsigned char* lfr = lconv + S;
-  __shared__ int s_flags[2];
-  const size_t gb = (size_t)g * N * S;
-  const size_t fo = (size_t)g * (N + m) * S;
-
-  // ---- load the CTA's slice: dinv, x-faces, dinv halo; x = 0, r = b, p0 = z
-  for (int e = t; e < (row1 - row0) * L; e += T) {
-    const int q = row0 + e / L, l = V * (e % L);
-    const size_t o = gb + (size_t)q * S + l, lo = (size_t)(q - row0) * S + l;
-    double bv[V], dv[V], z[V], zero[V];
-    if (rhs) {
-      ldgv<V>(rhs + o, bv);
-    } else {
-#pragma unroll
-      for (int j = 0; j < V; ++j) bv[j] = rhs_const;
-    }
-    if (dinv_g) ldgv<V>(dinv_g + o, dv);
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-      if (!dinv_g) dv[j] = 1.0;
-      z[j] = dinv_g ? __dmul_rn(bv[j], dv[j]) : bv[j];
-      zero[j] = 0.0;
-      xs[lo + j] = zero[j];
-      rs[lo + j] = bv[j];
-      ds[lo + j] = dv[j];
-      pb[0][lo + j] = z[j];
-    }
-  }
-  for (int e = t; e < (row1 - row0 + m) * L; e += T) {
-    const int q = row0 + e / L, l = V * (e % L);
-    double tv[V];
-    ldgv<V>(fv.tx + fo + (size_t)q * S + l, tv);
-#pragma unroll
-    for (int j = 0; j < V; ++j) txs[(size_t)(q - row0) * S + l + j] = tv[j];
-  }
-  for (int e = t; e < 2 * hm * L; e += T) {
-    const int h = e / L, l = V * (e % L);
-    const int q = h < hm ? row0 - hm + h : row1 + (h - hm);
-    double* dst = h < hm ? hdw + (size_t)h * S : hde + (size_t)(h - hm) * S;
-#pragma unroll
-    for (int j = 0; j < V; ++j)
-      dst[l + j] = (q >= 0 && q < N) ? (dinv_g ? __ldg(dinv_g + gb + (size_t)q * S + l + j) : 1.0)
-                                     : 0.0;
-  }
-  __syncthreads();
-
-  // p of global row q from the current buffer (own rows or the local halo)
-  auto p_at = [&](const double* pown, int q) -> const double* {
-    if (q >= row0 && q < row1) return pown + (size_t)(q - row0) * S;
-    if (q < row0) return hw + (size_t)(q - (row0 - hm)) * S;
-    return he + (size_t)(q - row1) * S;
-  };
-  // halo p_{k+1} = r * dinv + beta * p_k from the owners' r and p_k (DSMEM);
-  // init: beta = 0 and r = b gives p_0 = z.  A thread's halo items and their
-  // owners' addresses are fixed for the solve: resolved once (kHaloItems per
-  // thread cached, any further ones resolved per call).
-  constexpr int kHaloItems = 2;
-  const double* h_r[kHaloItems];
-  const double* h_p[kHaloItems][2];
-  auto halo_src = [&](int e, const double*& ro_, const double*& p0_, const double*& p1_) {
-    const int h = e / L, l = V * (e % L);
-    const int q = h < hm ? row0 - hm + h : row1 + (h - hm);
-    if (q < 0 || q >= N) {
-      ro_ = nullptr;
-      return;
-    }
-    const int ob = chunk_owner(C, nb, q / CR);
-    const size_t off = (size_t)(q - chunk_lo(C, nb, ob) * CR) * S + l;
-    ro_ = cluster.map_shared_rank(rs, ob) + off;
-    p0_ = cluster.map_shared_rank(pb[0], ob) + off;
-    p1_ = cluster.map_shared_rank(pb[1], ob) + off;
-  };
-#pragma unroll
-  for (int i = 0; i < kHaloItems; ++i) {
-    h_r[i] = nullptr;
-    const int e = t + i * T;
-    if (e < 2 * hm * L) halo_src(e, h_r[i], h_p[i][0], h_p[i][1]);
-  }
-  auto form_item = [&](int e, const double* rr_o, const double* p0_, const double* p1_, int kb,
-                       bool init) {
-    {
-      if (!rr_o) return;
-      const int h = e / L, l = V * (e % L);
-      const double* dh = (h < hm ? hdw + (size_t)h * S : hde + (size_t)(h - hm) * S) + l;
-      double* dst = (h < hm ? hw + (size_t)h * S : he + (size_t)(h - hm) * S) + l;
-      double rv[V];
-#pragma unroll
-      for (int j = 0; j < V; ++j) rv[j] = rr_o[j];
-      if (init) {
-#pragma unroll
-        for (int j = 0; j < V; ++j) dst[j] = dinv_g ? __dmul_rn(rv[j], dh[j]) : rv[j];
-      } else {
-        const double* pk_o = kb ? p1_ : p0_;
-        double pv[V];
-#pragma unroll
-        for (int j = 0; j < V; ++j) pv[j] = pk_o[j];
-#pragma unroll
-        for (int j = 0; j < V; ++j) {
-          const double z = dinv_g ? __dmul_rn(rv[j], dh[j]) : rv[j];
-          dst[j] = __dadd_rn(z, __dmul_rn(lb[l + j], pv[j]));
-        }
-      }
-    }
-  };
-  auto form_halo = [&](int kb, bool init) {
-#pragma unroll
-    for (int i = 0; i < kHaloItems; ++i)
-      if (t + i * T < 2 * hm * L) form_item(t + i * T, h_r[i], h_p[i][0], h_p[i][1], kb, init);
-    for (int e = t + kHaloItems * T; e < 2 * hm * L; e += T) {
-      const double *rr_o, *p0_ = nullptr, *p1_ = nullptr;
-      halo_src(e, rr_o, p0_, p1_);
-      form_item(e, rr_o, p0_, p1_, kb, init);
-    }
-  };
-  // canonical chunk partials of this CTA's chunks: per-thread values already
-  // in red[((k*NV + v)*V + j)*T + t]; one tree pass for all chunks
-  auto chunk_trees = [&](int NVv, double* part) {
-    const int ns = ncl * NVv * V;
-    __syncthreads();
-    for (int s2 = R >> 1; s2 > 0; s2 >>= 1) {
-      if ((t / Lp) < s2)
-        for (int v = 0; v < ns; ++v) red[v * T + t] += red[v * T + t + s2 * Lp];
-      __syncthreads();
-    }
-    if (t < L)
-      for (int k = 0; k < ncl; ++k)
-        for (int v = 0; v < NVv; ++v)
-#pragma unroll
-          for (int j = 0; j < V; ++j)
-            part[((size_t)k * NVv + v) * S + V * t + j] = red[((k * NVv + v) * V + j) * T + t];
-  };
-  // all C partials in the canonical final order (finish_chunks' last stage):
-  // totals of value v, lane V*sl+j in red[(v*V + j)*T + sl]
-  auto final_sum = [&](int NVv, double* part) {
-    double acc[2 * V];
-#pragma unroll
-    for (int v = 0; v < 2 * V; ++v) acc[v] = 0.0;
-    if (sl < L) {
-      for (int cc = rr; cc < C; cc += R) {
-        const int ob = chunk_owner(C, nb, cc);
-        const double* pr = cluster.map_shared_rank(part, ob) +
-                           (size_t)(cc - chunk_lo(C, nb, ob)) * NVv * S;
-        for (int v = 0; v < NVv; ++v)
-#pragma unroll
-          for (int j = 0; j < V; ++j) acc[v * V + j] += pr[(size_t)v * S + V * sl + j];
-      }
-    }
-    __syncthreads();
-    for (int v = 0; v < NVv * V; ++v) red[v * T + t] = acc[v];
-    __syncthreads();
-    for (int s2 = R >> 1; s2 > 0; s2 >>= 1) {
-      if ((t / Lp) < s2)
-        for (int v = 0; v < NVv * V; ++v) red[v * T + t] += red[v * T + t + s2 * Lp];
-      __syncthreads();
-    }
-  };
-
-  // ---- init partials b.b and r.z (r = b, z = p0)
-  for (int k = 0; k < ncl; ++k) {
-    double acc[2][V] = {};
-    if (sl < L) {
-      for (int q = (c0 + k) * CR + rr; q < (c0 + k + 1) * CR && q < N; q += R) {
-        const size_t lo = (size_t)(q - row0) * S + V * sl;
-#pragma unroll
-        for (int j = 0; j < V; ++j) {
-          acc[0][j] = __fma_rn(rs[lo + j], rs[lo + j], acc[0][j]);
-          acc[1][j] = __fma_rn(rs[lo + j], pb[0][lo + j], acc[1][j]);
-        }
-      }
-    }
-#pragma unroll
-    for (int v = 0; v < 2; ++v)
-#pragma unroll
-      for (int j = 0; j < V; ++j) red[((k * 2 + v) * V + j) * T + t] = acc[v][j];
-  }
-  chunk_trees(2, pB);
-  cluster.sync();
-  form_halo(0, true);
-  final_sum(2, pB);
-  if (t == 0) s_flags[0] = 1;
-  __syncthreads();
-  if (t < L) {
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-      const int s = V * t + j;
-      const double bn = sqrt(red[j * T + t]);
-      const double thr = tol * bn;
-      lthr[s] = thr;
-      lrz[s] = red[(V + j) * T + t];
-      lconv[s] = bn <= thr;
-      lfr[s] = 0;
-      lit[s] = 0;
-      if (b == 0 && st.hist) st.hist[(size_t)g * S + s] = bn;
-      if (!(bn <= thr)) s_flags[0] = 0;
-    }
-  }
-  __syncthreads();
-  int it = 0, kb = 0;  // kb: buffer of p_k
-  bool finish = s_flags[0] || maxit == 0;
-  bool bad = false;
-  while (!finish) {
-    ++it;
-    // ---- phase A: Ap = A p_k (shared memory + halo), partial p.Ap
-    const double* pk = pb[kb];
-    for (int k = 0; k < ncl; ++k) {
-      double acc[V] = {};
-      if (sl < L) {
-        for (int q = (c0 + k) * CR + rr; q < (c0 + k + 1) * CR && q < N; q += R) {
-          const int i0 = q / m, j0 = q - i0 * m;
-          const size_t lo = (size_t)(q - row0) * S + V * sl;
-          const double* tw = txs + lo;
-          const double* te = txs + lo + (size_t)m * S;
-          const double ay = fv.a_y;
-          const bool w = i0 > 0, s_ = j0 > 0, n_ = j0 < m - 1, e_ = i0 < m - 1;
-          const double* pc = pk + lo;
-          const double* pw = p_at(pk, q - m) + V * sl;
-          const double* ps = p_at(pk, q - 1) + V * sl;
-          const double* pn = p_at(pk, q + 1) + V * sl;
-          const double* pe = p_at(pk, q + m) + V * sl;
-#pragma unroll
-          for (int j = 0; j < V; ++j) {
-            const double d = __dadd_rn(__dadd_rn(__dadd_rn(tw[j], te[j]), ay), ay);
-            double y = 0.0;
-            if (w) y = __dadd_rn(y, __dmul_rn(-tw[j], pw[j]));
-            if (s_) y = __dadd_rn(y, __dmul_rn(-ay, ps[j]));
-            y = __dadd_rn(y, __dmul_rn(d, pc[j]));
-            if (n_) y = __dadd_rn(y, __dmul_rn(-ay, pn[j]));
-            if (e_) y = __dadd_rn(y, __dmul_rn(-te[j], pe[j]));
-            aps[lo + j] = y;
-            acc[j] = __fma_rn(pc[j], y, acc[j]);
-          }
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < V; ++j) red[(k * V + j) * T + t] = acc[j];
-    }
-    chunk_trees(1, pA);
-    cluster.sync();  // barrier 1: p.Ap partials visible
-    final_sum(1, pA);
-    if (t < L) {
-#pragma unroll
-      for (int j = 0; j < V; ++j) {
-        const int s = V * t + j;
-        const double pap = red[j * T + t];
-        const unsigned char fr = lfr[s] | (unsigned char)(pap <= DBL_MIN);
-        lfr[s] = fr;
-        la[s] = fr ? 0.0 : __ddiv_rn(lrz[s], pap);
-      }
-    }
-    __syncthreads();
-    // ---- phase B: x += alpha p_k; r -= alpha Ap; partials r.r, r.z
-    double alpha[V];
-#pragma unroll
-    for (int j = 0; j < V; ++j) alpha[j] = sl < L ? la[V * sl + j] : 0.0;
-    for (int k = 0; k < ncl; ++k) {
-      double acc[2][V] = {};
-      if (sl < L) {
-        for (int q = (c0 + k) * CR + rr; q < (c0 + k + 1) * CR && q < N; q += R) {
-          const size_t lo = (size_t)(q - row0) * S + V * sl;
-#pragma unroll
-          for (int j = 0; j < V; ++j) {
-            xs[lo + j] = __dadd_rn(xs[lo + j], __dmul_rn(alpha[j], pk[lo + j]));
-            const double rv = __dsub_rn(rs[lo + j], __dmul_rn(alpha[j], aps[lo + j]));
-            rs[lo + j] = rv;
-            const double zv = dinv_g ? __dmul_rn(rv, ds[lo + j]) : rv;
-            acc[0][j] = __fma_rn(rv, rv, acc[0][j]);
-            acc[1][j] = __fma_rn(rv, zv, acc[1][j]);
-          }
-        }
-      }
-#pragma unroll
-      for (int v = 0; v < 2; ++v)
-#pragma unroll
-        for (int j = 0; j < V; ++j) red[((k * 2 + v) * V + j) * T + t] = acc[v][j];
-    }
-    chunk_trees(2, pB);
-    cluster.sync();  // barrier 2: update partials (and every CTA's r) visible
-    final_sum(2, pB);
-    if (t == 0) {
-      s_flags[0] = 1;
-      s_flags[1] = 0;
-    }
-    __syncthreads();
-    if (t < L) {
-#pragma unroll
-      for (int j = 0; j < V; ++j) {
-        const int s = V * t + j;
-        const double rn = sqrt(red[j * T + t]);
-        const double rz_new = red[(V + j) * T + t];
-        if (b == 0 && st.hist) {
-          if (it <= st.hist_cap) st.hist[((size_t)it * st.G + g) * S + s] = rn;
-          else atomicOr(st.overflow, 1);
-        }
-        const bool live = !lfr[s];
-        if (live && !isfinite(rn)) atomicOr(&s_flags[1], 1);
-        if (live && !lconv[s] && rn <= lthr[s]) {
-          lit[s] = it;
-          lconv[s] = 1;
-        }
-        if (live && !lconv[s]) atomicAnd(&s_flags[0], 0);
-        const double rz_old = lrz[s];
-        lb[s] = (live && rz_old > 0.0) ? __ddiv_rn(rz_new, rz_old) : 0.0;
-        lrz[s] = rz_new;
-      }
-    }
-    __syncthreads();
-    bad = s_flags[1] != 0;
-    finish = bad || s_flags[0] || it >= maxit;
-    if (finish) break;
-    // ---- phase C: p_{k+1} = z + beta p_k into the other buffer, own rows + halo
-    double* pn = pb[kb ^ 1];
-    for (int e = t; e < (row1 - row0) * L; e += T) {
-      const size_t lo = (size_t)(e / L) * S + V * (e % L);
-#pragma unroll
-      for (int j = 0; j < V; ++j) {
-        const double zv = dinv_g ? __dmul_rn(rs[lo + j], ds[lo + j]) : rs[lo + j];
-        pn[lo + j] = __dadd_rn(zv, __dmul_rn(lb[V * (e % L) + j], pk[lo + j]));
-      }
-    }
-    form_halo(kb, false);
-    kb ^= 1;
-    __syncthreads();
-  }
-  // ---- outputs: x rows, lane results (CTA 0 of the group)
-  for (int e = t; e < (row1 - row0) * L; e += T) {
-    const int q = row0 + e / L, l = V * (e % L);
-    double xv[V];
-#pragma unroll
-    for (int j = 0; j < V; ++j) xv[j] = xs[(size_t)(q - row0) * S + l + j];
-    stv<V>(x_g + gb + (size_t)q * S + l, xv);
-  }
-  if (b == 0) {
-    if (t < L) {
-#pragma unroll
-      for (int j = 0; j < V; ++j) {
-        const int s = V * t + j;
-        const size_t l = (size_t)g * S + s;
-        st.iters[l] = lconv[s] ? lit[s] : it;
-        st.conv[l] = lconv[s];
-        st.frozen[l] = lfr[s];
-        st.alpha[l] = la[s];
-      }
-    }
-    if (t == 0) {
-      st.it[g] = it;
-      st.status[g] = bad ? 2 : 0;
-      st.done[g] = kDone;
-      atomicAdd(st.ndone, 1);
-    }
-  }
-  cluster.sync();  // no CTA leaves while another may still read its shared memory
-}
-
-// Cluster size and shared-memory bytes for the smem-resident kernel, or 0
-// when the group does not fit (face form with constant y-faces only).
-int cluster_smem_size(const Geo& geo, long long N, int m, size_t* smem_out) {
-  int dev = 0, optin = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  if (geo.sc != 1 || geo.T > 256) return 0;
-  for (int nb = geo.chunks < 16 ? geo.chunks : 16; nb >= 1; --nb) {
-    // every CTA must own at least one chunk and the smem plan must fit
-    const SmemPlan sp = smem_plan(geo, m, N, nb);
-    if ((long long)sp.bytes > optin) {
-      if (nb == (geo.chunks < 16 ? geo.chunks : 16)) continue;
-      return 0;  // fewer CTAs only makes each slice bigger
-    }
-    const void* fn = geo.V == 2 ? (const void*)pcg_cluster_smem_kernel<2>
-                                : (const void*)pcg_cluster_smem_kernel<1>;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.bytes);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(nb, 1, 1);
-    cfg.blockDim = dim3(geo.T, 1, 1);
-    cfg.dynamicSmemBytes = sp.bytes;
-    cudaLaunchAttribute attr;
-    attr.id = cudaLaunchAttributeClusterDimension;
-    attr.val.clusterDim.x = nb;
-    attr.val.clusterDim.y = 1;
-    attr.val.clusterDim.z = 1;
-    cfg.attrs = &attr;
-    cfg.numAttrs = 1;
-    int nclusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg) != cudaSuccess) {
-      cudaGetLastError();
-      continue;
-    }
-    if (nclusters >= 1) {
-      if (smem_out) *smem_out = sp.bytes;
-      return nb;
-    }
-  }
-  return 0;
-}
-
-cudaError_t launch_pcg_cluster_smem(const Geo& geo, int G, int nb, size_t smem, cudaStream_t s,
-                                    long long N, const PcgState& st, const Fv2dOp& fv,
-                                    const double* rhs, double rhs_const, const double* dinv,
-                                    double tol, int maxit, double* x) {
-  Geo gl = geo;
-  gl.B = nb;
-  Fv2dOp op = fv;
-  PcgState sc = st;
-  void* args[] = {&N, &gl, &sc, &op, (void*)&rhs, &rhs_const, (void*)&dinv, &tol, &maxit, &x};
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(nb, G, 1);
-  cfg.blockDim = dim3(gl.T, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr;
-  attr.id = cudaLaunchAttributeClusterDimension;
-  attr.val.clusterDim.x = nb;
-  attr.val.clusterDim.y = 1;
-  attr.val.clusterDim.z = 1;
-  cfg.attrs = &attr;
-  cfg.numAttrs = 1;
-  const void* fn = gl.V == 2 ? (const void*)pcg_cluster_smem_kernel<2>
-                             : (const void*)pcg_cluster_smem_kernel<1>;
-  return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 // Lets every persistent instantiation take `smem` bytes of dynamic shared

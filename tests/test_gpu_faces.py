@@ -89,8 +89,7 @@ _VARIANTS = {  # solve-loop variants (all must give the CSR bits)
 
 
 @pytest.mark.parametrize("persistent,variant", [
-    ("0", "reg"), ("1", "reg"), ("2", "reg"), ("3", "reg")] +
-    [("0", v) for v in _VARIANTS if v != "reg"])
+    ("0", "reg"), ("1", "reg"), ("2", "reg")] + [("0", v) for v in _VARIANTS if v != "reg"])
 def test_face_pcg_bitwise_equal_csr_pcg(tmp_path, persistent, variant):
     """Whole batched solves (iterations, QoIs, residual histories) through the
     launch loop (0), the cooperative (1) and the cluster (2) persistent kernel,

@@ -42,9 +42,8 @@ np.save(sys.argv[2], np.concatenate(out))
 
 def test_persistent_bitwise_equals_launch_loop(tmp_path):
     got = {}
-    # smem-resident cluster kernel, cluster barriers, cooperative barriers,
-    # host-polled launch loop, graph launch loop
-    for mode in ("3", "2", "1", "0", "0g"):
+    # cluster barriers, cooperative barriers, host-polled launch loop, graph launch loop
+    for mode in ("2", "1", "0", "0g"):
         env = dict(os.environ, UQG_PCG_PERSISTENT=mode[0], UQG_PCG_GRAPH=str(int(mode == "0g")))
         dst = tmp_path / f"p{mode}.npy"
         subprocess.run([sys.executable, "-c", _SCRIPT, str(ROOT), str(dst)], env=env, check=True,
@@ -53,7 +52,6 @@ def test_persistent_bitwise_equals_launch_loop(tmp_path):
     assert got["1"].shape == got["0"].shape
     assert np.array_equal(got["1"], got["0"])
     assert np.array_equal(got["2"], got["0"])
-    assert np.array_equal(got["3"], got["0"])
     assert np.array_equal(got["0g"], got["0"])
 
 
