@@ -33,6 +33,7 @@ import sys
 import threading
 import time
 from pathlib import Path
+from types import SimpleNamespace
 
 import numpy as np
 
@@ -321,17 +322,53 @@ def _cpu_warm(cfg_name):
     return os.getpid()
 
 
+REF_PKG = ROOT / "baseline" / "_ref"
+
+
+def _reference_solver():
+    """The reference's own ``EnsembleCsrMatrix`` / ``ensemble_pcg``
+    (``ensemble.py:52-281``, unmodified, installed in baseline/_ref by
+    tools/stage_reference.py; it travels to the GPU box), or None when it is
+    not staged - then the oracle's restatement (oracle/pcg.py) is timed."""
+    if not (REF_PKG / "uqgroup").exists():
+        return None
+    if str(REF_PKG) not in sys.path:
+        sys.path.append(str(REF_PKG))
+    try:
+        from uqgroup import ensemble as ref_ens
+    except Exception:  # noqa: BLE001 - fall back to the port
+        return None
+    return ref_ens
+
+
+def cpu_path_kind() -> str:
+    return "reference" if _reference_solver() is not None else "port"
+
+
 def _cpu_group_worker(args):
-    """One group through the CPU path, 1 thread.  ``maxit`` None: full solve.
-    Otherwise the PCG runs ``maxit`` iterations, and its initialisation
-    (Jacobi inverse, r = b, norms) is timed separately by a maxit=0 run, so
-    the per-iteration time excludes it."""
+    """One group through the CPU path, 1 thread: the 2D assembly restated in
+    oracle/ (the reference has no 2D operator) and the reference's own
+    ``ensemble_pcg`` (baseline/_ref; else oracle/pcg.py).  ``maxit`` None:
+    full solve.  Otherwise the PCG runs ``maxit`` iterations, and its
+    initialisation (Jacobi inverse, r = b, norms) is timed separately by a
+    maxit=0 run, so the per-iteration time excludes it."""
     cfg_name, samples, maxit = args
     from threadpoolctl import threadpool_limits
 
     from oracle import fv2d as ofv, pcg as opcg
 
     cfg, fld, mesh, table = _cpu_setup(cfg_name)
+    ref = _reference_solver()
+
+    def solve(sysm, k):
+        if ref is None:
+            return opcg.pcg(sysm.row_offsets, sysm.col_indices, sysm.values, sysm.rhs,
+                            tol=cfg.tol, maxit=k)
+        mat = ref.EnsembleCsrMatrix(sysm.row_offsets, sysm.col_indices, sysm.values)
+        r = ref.ensemble_pcg(mat, sysm.rhs, tol=cfg.tol, maxit=k)
+        return SimpleNamespace(ensemble_iterations=r.ensemble_iterations,
+                               iterations=r.iterations_per_lane, solution=r.solution)
+
     with threadpool_limits(limits=1):
         t0 = time.perf_counter()
         sysm = ofv.assemble(mesh, fld, samples, table, cfg.a2)
@@ -339,12 +376,10 @@ def _cpu_group_worker(args):
         t_init = 0.0
         if maxit is not None:
             t0 = time.perf_counter()
-            opcg.pcg(sysm.row_offsets, sysm.col_indices, sysm.values, sysm.rhs, tol=cfg.tol,
-                     maxit=0)
+            solve(sysm, 0)
             t_init = time.perf_counter() - t0
         t0 = time.perf_counter()
-        res = opcg.pcg(sysm.row_offsets, sysm.col_indices, sysm.values, sysm.rhs, tol=cfg.tol,
-                       maxit=cfg.maxit if maxit is None else maxit)
+        res = solve(sysm, cfg.maxit if maxit is None else maxit)
         t_pcg = time.perf_counter() - t0
         t0 = time.perf_counter()
         q = [ofv.qoi(u) for u in res.solution]
@@ -400,7 +435,7 @@ def cpu_baseline(cfg, ids, coords, keys, gold, max_iters, gpu_rows=None):
     full, src = full_iterations(cfg, ens, gold, keys, max_iters)
     S = cfg.ensemble_size
     out = {"unit": "sample-solves/s" if not max_iters else "sample-iterations/s", "cores": 1,
-           "kind": "port" if r["full"] else "port (projected)", **host_info()}
+           "kind": cpu_path_kind() + ("" if r["full"] else " (projected)"), **host_info()}
     if full is None and not r["full"]:
         out.update(value=None, sample="no iteration counts to project a full solve")
         return out
@@ -410,8 +445,9 @@ def cpu_baseline(cfg, ids, coords, keys, gold, max_iters, gpu_rows=None):
            f"{r['iters_run']} PCG iterations timed ({r['pcg']:.1f}s) + setup {r['setup']:.1f}s, "
            f"projected to {full[k]} iterations ({src})")
     out["sample"] = (f"group {k} of {len(ens)} (S={S}, median in surrogate order) of the {cfg.name} "
-                     f"final level: 2D KL + assembly + Jacobi-PCG + QoI, oracle/ numpy+scipy, "
-                     f"1 thread; {how}")
+                     f"final level: 2D KL + assembly (oracle/) + Jacobi-PCG ("
+                     + ("uqgroup ensemble_pcg, baseline/_ref" if cpu_path_kind() == "reference"
+                        else "oracle/pcg.py") + f") + QoI, 1 thread; {how}")
     if r["full"] and gpu_rows is not None:
         it_g, q_g = gpu_rows(k)
         out["parity_vs_gpu"] = {
@@ -496,11 +532,15 @@ def run_reference(args, cfg):
         "config": config_dict(cfg, n, K, world, args.scaling, meta),
         "cpu_baseline": {
             "value": value, "unit": unit, "cores": P,
-            "kind": "port" if maxit is None else "port (projected)",
+            "kind": cpu_path_kind() + ("" if maxit is None else " (projected)"),
             "sample": f"per step {len(samples[0]) if samples else 0} of {K} groups (stratified: "
                       f"every {K / P:.1f}th in surrogate order, offset = step), one per process, "
-                      f"1 BLAS thread each; {how}; oracle/ restatement of uqgroup's path (the "
-                      "reference is pure Python; its 2D operator does not exist, DESIGN.md)",
+                      f"1 BLAS thread each; {how}; " + (
+                          "uqgroup's own EnsembleCsrMatrix/ensemble_pcg from baseline/_ref "
+                          "(unmodified) on the 2D assembly restated in oracle/ (the reference "
+                          "has no 2D operator, DESIGN.md)" if cpu_path_kind() == "reference"
+                          else "oracle/ restatement of uqgroup's path (baseline/_ref not "
+                          "staged)"),
             "step_values": times, **host_info()},
         "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

@@ -20,7 +20,8 @@ def test_reference_arm_runs_on_cpu():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["metric"].startswith("ensemble sample-solves/s")
-    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "port"
+    assert d["e2e"]["h2d_bytes_per_step"] == 0
+    assert d["cpu_baseline"]["kind"] in ("reference", "port")  # reference: baseline/_ref staged
 
 
 def test_byte_model_matches_survey():
