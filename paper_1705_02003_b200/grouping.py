@@ -8,10 +8,12 @@
   images, O(n) per level); sample ids may be any hashable objects, the device
   works on their generation-order indices.
 
-The reference's post-hoc accounting (``compute_R``, ``group_oracle``,
-``predicted_speedup``, ``grouping.py:125-260``) is not on the hot path and is
-not rebuilt here; the reference's own functions
-accept these plans unchanged (``tests/test_ref_conformance.py``).
+The reference's post-hoc accounting is not on the hot path: ``compute_R``
+(``grouping.py:156-193``) is restated in ``report.py`` for the run files
+(``r_table.csv``); ``group_oracle`` and ``predicted_speedup``
+(``grouping.py:125-154,196-204``) are not rebuilt (DESIGN.md "Out of scope").
+The reference's own functions accept these plans unchanged
+(``tests/test_ref_conformance.py``).
 """
 
 from __future__ import annotations
