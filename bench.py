@@ -574,6 +574,9 @@ def main():
         if share:
             dist.init_process_group("gloo")
         else:
+            # NCCL's init log (ranks, transports, NVLS) goes to stderr for the record
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_1705_02003_b200 as uq
