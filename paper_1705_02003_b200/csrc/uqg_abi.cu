@@ -1,7 +1,6 @@
 // uqg_abi.cu - the C ABI of libuqg.so (include/uqg.h): argument validation,
 // context / workspace management, launch accounting and the host side of the
 // device-resident PCG loop.
-#include <nvtx3/nvToolsExt.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -151,15 +150,6 @@ struct PersistBufs {
   unsigned* bar;  // [G] counts, [G] generations, [1] abort flag
 };
 thread_local PersistBufs g_persist;
-
-// NVTX range over a host entry point (header-only NVTX v3: a no-op unless a
-// profiler is attached), so nsys / ncu timelines show the library's phases.
-struct NvtxRange {
-  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
-  ~NvtxRange() { nvtxRangePop(); }
-  NvtxRange(const NvtxRange&) = delete;
-  NvtxRange& operator=(const NvtxRange&) = delete;
-};
 
 // UQG_PCG_PERSISTENT: 2 = cluster kernel, 1 = cooperative kernel (when
 // co-resident), 0 = never, unset = auto
@@ -357,7 +347,6 @@ int uqg_kl_eval_sep2d(uqg_ctx* ctx, int n_cells, const double* table1d, int n_fa
                       const double* samples, const int* lane_ids, int G, int S, double a_min,
                       int a_hat_mode, double a_hat_value, int expansion, double* a_out,
                       void* stream) {
-  NvtxRange nvtx_("uqg_kl_eval_sep2d");
   UQG_REQUIRE(ctx && table1d && mode_p && mode_q && sqrt_lam && samples && a_out,
               "uqg_kl_eval_sep2d: NULL argument");
   UQG_REQUIRE(n_cells >= 2 && n_factors >= 1 && M >= 1 && G >= 1 && S >= 1,
@@ -506,7 +495,6 @@ int uqg_spmv(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G,
 
 int uqg_lane_dot(uqg_ctx* ctx, int N, int S, int G, const double* a, const double* b,
                  double* out, void* stream) {
-  NvtxRange nvtx_("uqg_lane_dot");
   UQG_REQUIRE(ctx && a && b && out, "uqg_lane_dot: NULL argument");
   UQG_REQUIRE(N >= 0 && S >= 1 && S <= kMaxLanes && G >= 1, "uqg_lane_dot: bad sizes");
   cudaStream_t s = as_stream(stream);
@@ -571,7 +559,6 @@ int uqg_pcg(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const i
 int uqg_assemble_fv2d_faces(uqg_ctx* ctx, int n_cells, int G, int S, const double* a_nodes,
                             double a_y, int a2_same, double* tx, double* ty, double* dinv,
                             void* stream) {
-  NvtxRange nvtx_("uqg_assemble_fv2d_faces");
   UQG_REQUIRE(ctx && a_nodes && tx && (!a2_same || ty), "uqg_assemble_fv2d_faces: NULL argument");
   UQG_REQUIRE(n_cells >= 2 && G >= 1 && S >= 1, "uqg_assemble_fv2d_faces: bad sizes");
   const long long m = n_cells - 1;
@@ -619,7 +606,6 @@ int pcg_impl(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const 
              const double* rhs, double rhs_const, const double* dinv, double tol, int maxit,
              double* x, int* iters, unsigned char* converged, unsigned char* frozen,
              int* ens_iters, double* hist_host, int hist_cap, int* hist_rows_host, void* stream) {
-  NvtxRange nvtx_("uqg_pcg");
   UQG_REQUIRE(tol > 0.0 && tol <= 1.7976931348623157e308, "tol must be positive and finite");
   UQG_REQUIRE(maxit >= 0, "maxit must be >= 0");
   UQG_REQUIRE(!hist_host || (hist_cap >= 0 && hist_rows_host), "uqg_pcg: bad history buffer");
@@ -1032,7 +1018,6 @@ extern "C" {
 
 int uqg_group_sort(uqg_ctx* ctx, const double* keys, int n, int S, int* order, int* groups,
                    int* pad, void* stream) {
-  NvtxRange nvtx_("uqg_group_sort");
   UQG_REQUIRE(ctx && groups && pad, "uqg_group_sort: NULL argument");
   UQG_REQUIRE(n >= 1, "cannot group an empty sample set");
   UQG_REQUIRE(S >= 1, "ensemble size must be >= 1");
@@ -1050,7 +1035,6 @@ int uqg_group_sort(uqg_ctx* ctx, const double* keys, int n, int S, int* order, i
 
 int uqg_group_sort_async(uqg_ctx* ctx, const double* keys, int n, int S, int* order, int* groups,
                          int* pad, void* stream) {
-  NvtxRange nvtx_("uqg_group_sort");
   UQG_REQUIRE(ctx && groups && pad, "uqg_group_sort_async: NULL argument");
   UQG_REQUIRE(n >= 1, "cannot group an empty sample set");
   UQG_REQUIRE(S >= 1, "ensemble size must be >= 1");
