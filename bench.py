@@ -634,7 +634,7 @@ def main():
     torch.cuda.synchronize()
 
     import ctypes
-    NK = 11  # UQG_NKERN
+    NK = _lib.NKERN  # UQG_NKERN
 
     def timed(profile: bool, steps: int):
         """`steps` timed steps; per-launch CUDA-event kernel timing when `profile`."""

@@ -21,6 +21,10 @@ UQG_OK, UQG_EINVAL, UQG_EBREAKDOWN, UQG_ECUDA, UQG_ENOMEM, UQG_ECAPACITY = range
 _c_int, _c_double, _c_ll = ctypes.c_int, ctypes.c_double, ctypes.c_longlong
 _p = ctypes.c_void_p
 
+# UQG_NKERN (include/uqg.h): length of the per-kernel-class arrays that
+# uqg_ctx_profile_read fills
+NKERN = 11
+
 # name -> (restype, argtypes); the exact list include/uqg.h declares
 SIGNATURES = {
     "uqg_version": (_c_int, []),

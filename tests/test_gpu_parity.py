@@ -408,8 +408,9 @@ def test_solve_level_equals_group_by_key_plus_solve_plan():
 def test_launch_accounting_and_profiling():
     lib, ctx = _lib.load(), _lib.ctx()
     import ctypes
-    ms = (ctypes.c_double * 10)()
-    cnt = (ctypes.c_longlong * 10)()
+    # arrays of UQG_NKERN (include/uqg.h) entries: the library fills all of them
+    ms = (ctypes.c_double * _lib.NKERN)()
+    cnt = (ctypes.c_longlong * _lib.NKERN)()
     lib.uqg_ctx_profile_read(ctx, ms, cnt, 1)
     lib.uqg_ctx_profile(ctx, 1)
     before = lib.uqg_ctx_launch_count(ctx)

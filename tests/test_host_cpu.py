@@ -124,3 +124,14 @@ def test_device_entry_points_fail_loudly_without_gpu():
     from paper_1705_02003_b200 import DeviceError, group_natural
     with pytest.raises(DeviceError):
         group_natural([1, 2, 3], 2)
+
+
+def test_nkern_matches_header():
+    """The profile arrays the bindings allocate are UQG_NKERN long: the library
+    writes every entry (a shorter array corrupted the host heap)."""
+    import re
+
+    from paper_1705_02003_b200 import _lib
+
+    h = (ROOT / "include" / "uqg.h").read_text()
+    assert int(re.search(r"#define UQG_NKERN (\d+)", h).group(1)) == _lib.NKERN
