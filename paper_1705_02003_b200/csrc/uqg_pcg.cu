@@ -424,8 +424,26 @@ __global__ void __launch_bounds__(256) spmv_fv2d_kernel(long long N, Geo geo, Fv
 }
 
 // chunks per batched reduction in pcg_update (reduce_lanes_batch)
+// Tiles per step of the streaming update / direction kernels (all loads of a
+// step issued before any store) and their CTAs per SM: 4 tiles at 2 CTAs/SM
+// (128 registers) keep 192 B per thread in flight - C3 level 10.64 -> 10.48 s,
+// C2 1.455 -> 1.436 s against 2 tiles at 3 CTAs/SM (tools/runs/sweep_tiles*.sh;
+// tools/stream_probe.cu: 7.17 TB/s for this 3-read / 1-write pattern at 4 rows
+// per thread vs 6.99 at 2).  Per-thread rows are accumulated in tile order
+// either way: same bits.
+#ifndef UQG_UPDATE_TILES
+#define UQG_UPDATE_TILES 4
+#endif
+constexpr int kUpdTiles = UQG_UPDATE_TILES;  // tiles per step in pcg_update
+#ifndef UQG_DIR_TILES
+#define UQG_DIR_TILES 4
+#endif
+constexpr int kDirTiles = UQG_DIR_TILES;  // tiles per step in pcg_dir
+#ifndef UQG_DIR_MINB
+#define UQG_DIR_MINB 2
+#endif
 #ifndef UQG_UPDATE_MINB
-#define UQG_UPDATE_MINB 3
+#define UQG_UPDATE_MINB 2
 #endif
 #ifndef UQG_UPDATE_BATCH
 #define UQG_UPDATE_BATCH 4
@@ -459,13 +477,13 @@ __global__ void __launch_bounds__(256, UQG_UPDATE_MINB) pcg_update_kernel(long l
       double acc[2][V] = {};
       if (sl < geo.L) {
         const ChunkRows cr = chunk_tiles(geo, chunk);
-        // two tiles per step: all loads of both are issued before any store
-        for (long long tile = cr.t0; tile < cr.t1; tile += 2) {
-          double rv[2][V], av[2][V], dv[2][V];
-          bool ok[2];
-          size_t o[2];
+        // kUpdTiles tiles per step: all loads of the step are issued before any store
+        for (long long tile = cr.t0; tile < cr.t1; tile += kUpdTiles) {
+          double rv[kUpdTiles][V], av[kUpdTiles][V], dv[kUpdTiles][V];
+          bool ok[kUpdTiles];
+          size_t o[kUpdTiles];
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
+          for (int u = 0; u < kUpdTiles; ++u) {
             const long long row = (tile + u) * geo.R + rr;
             ok[u] = tile + u < cr.t1 && row < N;
             o[u] = base + (ok[u] ? row : 0) * S;
@@ -476,7 +494,7 @@ __global__ void __launch_bounds__(256, UQG_UPDATE_MINB) pcg_update_kernel(long l
             }
           }
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
+          for (int u = 0; u < kUpdTiles; ++u) {
             if (!ok[u]) continue;
             double zv[V];
 #pragma unroll
@@ -547,7 +565,7 @@ __global__ void __launch_bounds__(256, UQG_UPDATE_MINB) pcg_update_kernel(long l
 // place.  kx > 1 (deferred solution update): only p_{k+1} = z + beta p_k, into
 // the next buffer; x is updated by pcg_update's FLUSH iterations and pcg_flush.
 template <int V>
-__global__ void __launch_bounds__(256, 3) pcg_dir_kernel(long long N, Geo geo, PcgState st,
+__global__ void __launch_bounds__(256, UQG_DIR_MINB) pcg_dir_kernel(long long N, Geo geo, PcgState st,
                                                       const double* __restrict__ dinv,
                                                       const double* __restrict__ r,
                                                       double* __restrict__ x,
@@ -570,13 +588,13 @@ __global__ void __launch_bounds__(256, 3) pcg_dir_kernel(long long N, Geo geo, P
     double* pn = p + (size_t)xslot(st, it) * st.pstride;  // == pk when kx = 1
     for (int chunk = blockIdx.x; chunk < geo.chunks; chunk += gridDim.x) {
       const ChunkRows cr = chunk_tiles(geo, chunk);
-      // two tiles per step: all loads of both are issued before any store
-      for (long long tile = cr.t0; tile < cr.t1; tile += 2) {
-        double xv[2][V], pv[2][V], rv[2][V], dv[2][V];
-        bool ok[2];
-        size_t o[2];
+      // kDirTiles tiles per step: all loads of the step are issued before any store
+      for (long long tile = cr.t0; tile < cr.t1; tile += kDirTiles) {
+        double xv[kDirTiles][V], pv[kDirTiles][V], rv[kDirTiles][V], dv[kDirTiles][V];
+        bool ok[kDirTiles];
+        size_t o[kDirTiles];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < kDirTiles; ++u) {
           const long long row = (tile + u) * geo.R + rr;
           ok[u] = tile + u < cr.t1 && row < N;
           o[u] = base + (ok[u] ? row : 0) * S;
@@ -590,7 +608,7 @@ __global__ void __launch_bounds__(256, 3) pcg_dir_kernel(long long N, Geo geo, P
           }
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < kDirTiles; ++u) {
           if (!ok[u]) continue;
           if (inplace) {
 #pragma unroll
