@@ -16,6 +16,12 @@
 // one another, GPU suite green) the C3 level went 10.53 -> 10.66 s, so the
 // cyclic map stays.
 //
+// Also here: probe_il<KI>, KI ADJACENT chunks per block interleaved tile by tile
+// (cyclic map, one accumulator per chunk; the east band of chunk c is the
+// centre band of chunk c+1 and the west band of c+2, so those re-reads could be
+// L1 hits).  C3 shape, 14 blocks per group: cyclic 4,805, KI = 1 4,768, 2 4,902,
+// 4 3,827, 8 4,212 GB/s; C2 shape: slower for every KI > 1.  Not adopted.
+//
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 --fmad=false -o /tmp/frp tools/face_run_probe.cu
 //   /tmp/frp [cells=512] [S=32] [G=42] [random=1] [x] [ncu-mode]
 #include <cuda_runtime.h>
@@ -231,6 +237,114 @@ __global__ void fill(double* a, size_t n, unsigned seed) {
   }
 }
 
+
+// KI adjacent chunks per block, interleaved tile by tile (cyclic map, per-chunk
+// accumulators): the east band of chunk c is the centre band of chunk c+1 and
+// the west band of chunk c+2, so with the chunks on one SM those re-reads can
+// be L1 hits instead of L2 sectors.  Same chunk partials as MAP 0.
+template <int KI>
+__global__ void __launch_bounds__(256, 4) probe_il(Args a, int CT, double* part,
+                                                   unsigned* ticket) {
+  extern __shared__ double red[];
+  const int S = a.S, m = a.m, N = a.N, L = S / 2, Lp = L, T = 256, R = T / Lp;
+  const int tiles = (N + R - 1) / R, chunks = (tiles + CT - 1) / CT;
+  const int units = (chunks + KI - 1) / KI;
+  constexpr int UB = 8 / KI;  // units per batched tree (8 chunks)
+  const int g = blockIdx.y, B = gridDim.x, t = threadIdx.x;
+  const int sl = t % Lp, rr = t / Lp;
+  const double* txg = a.tx + (size_t)g * (N + m) * S + 2 * sl;
+  const double* pg = a.p + (size_t)g * N * S + 2 * sl;
+  double* apg = a.ap + (size_t)g * N * S + 2 * sl;
+  const int crows = CT * R;
+  for (int u0 = blockIdx.x; u0 < units; u0 += UB * B) {
+    int nu = (units - 1 - u0) / B + 1;
+    if (nu > UB) nu = UB;
+    for (int j = 0; j < nu; ++j) {
+      const int c_first = (u0 + j * B) * KI;
+      double2 acc[KI];
+#pragma unroll
+      for (int kk = 0; kk < KI; ++kk) acc[kk] = make_double2(0.0, 0.0);
+      int row0 = c_first * crows + rr;
+      int i0 = row0 / m, j0 = row0 - i0 * m;
+      for (int tl = 0; tl < CT; ++tl) {
+        int ik = i0, jk = j0;
+#pragma unroll
+        for (int kk = 0; kk < KI; ++kk) {
+          const int row = row0 + kk * crows;
+          int cend = (c_first + kk + 1) * crows;
+          if (cend > N) cend = N;
+          if (row < cend) {
+            const bool w = ik > 0, s = jk > 0, n = jk < m - 1, e = ik < m - 1;
+            const double2 z = make_double2(0, 0);
+            const double2 tw = ld2(txg + row * S), te = ld2(txg + (row + m) * S);
+            double2 pw = z, ps = z, pn = z, pe = z;
+            if (w) pw = ld2(pg + (row - m) * S);
+            if (s) ps = ld2(pg + (row - 1) * S);
+            const double2 pc = ld2(pg + row * S);
+            if (n) pn = ld2(pg + (row + 1) * S);
+            if (e) pe = ld2(pg + (row + m) * S);
+            double2 y;
+            y.x = row1(tw.x, te.x, pw.x, ps.x, pc.x, pn.x, pe.x, w, s, n, e);
+            y.y = row1(tw.y, te.y, pw.y, ps.y, pc.y, pn.y, pe.y, w, s, n, e);
+            *reinterpret_cast<double2*>(apg + row * S) = y;
+            acc[kk].x = fma(pc.x, y.x, acc[kk].x);
+            acc[kk].y = fma(pc.y, y.y, acc[kk].y);
+          }
+          jk += crows;
+          while (jk >= m) {
+            jk -= m;
+            ++ik;
+          }
+        }
+        row0 += R;
+        j0 += R;
+        while (j0 >= m) {
+          j0 -= m;
+          ++i0;
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < KI; ++kk) {
+        red[(2 * (j * KI + kk)) * T + t] = acc[kk].x;
+        red[(2 * (j * KI + kk) + 1) * T + t] = acc[kk].y;
+      }
+    }
+    __syncthreads();
+    for (int st = R >> 1; st > 0; st >>= 1) {
+      if (rr < st)
+        for (int v = 0; v < 2 * nu * KI; ++v) red[v * T + t] += red[v * T + t + st * Lp];
+      __syncthreads();
+    }
+    if (t < L)
+      for (int j = 0; j < nu; ++j)
+        for (int kk = 0; kk < KI; ++kk) {
+          const int c = (u0 + j * B) * KI + kk;
+          if (c < chunks) part[((size_t)g * chunks + c) * S + 2 * t] = red[(2 * (j * KI + kk)) * T + t];
+        }
+    __threadfence();
+    __syncthreads();
+    if (t == 0) atomicAdd(&ticket[g], (unsigned)nu);
+  }
+}
+
+template <int KI>
+float run_il(const Args& a, int CT, int bpg, int reps, double* part, unsigned* ticket) {
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  dim3 grid(bpg, a.G);
+  const size_t smem = 16 * 256 * 8;
+  probe_il<KI><<<grid, 256, smem>>>(a, CT, part, ticket);
+  CK(cudaDeviceSynchronize());
+  CK(cudaEventRecord(e0));
+  for (int r = 0; r < reps; ++r) probe_il<KI><<<grid, 256, smem>>>(a, CT, part, ticket);
+  CK(cudaEventRecord(e1));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  return ms / reps;
+}
+
 template <int MAP, int MINB>
 float run(const Args& a, int CT, int bpg, int reps, double* part, unsigned* ticket) {
   cudaEvent_t e0, e1;
@@ -311,6 +425,16 @@ int main(int argc, char** argv) {
          ct, ct * R, chunks);
   printf("resident CTAs/SM: map0 %d map1 %d map2 %d map3@4 %d map3@3 %d map3@2 %d\n",
          slots<0, 4>(), slots<1, 4>(), slots<2, 4>(), slots<3, 4>(), slots<3, 3>(), slots<3, 2>());
+  if (argc > 6) {  // interleave mode: adjacent chunks per block, tile-interleaved
+    for (int bpg : {12, 13, 14, 16}) {
+      printf("blocks/group %2d: cyclic %.0f", bpg, bytes / run<0, 4>(a, ct, bpg, 10, part, ticket) / 1e6);
+      printf("  il1 %.0f", bytes / run_il<1>(a, ct, bpg, 10, part, ticket) / 1e6);
+      printf("  il2 %.0f", bytes / run_il<2>(a, ct, bpg, 10, part, ticket) / 1e6);
+      printf("  il4 %.0f", bytes / run_il<4>(a, ct, bpg, 10, part, ticket) / 1e6);
+      printf("  il8 %.0f GB/s\n", bytes / run_il<8>(a, ct, bpg, 10, part, ticket) / 1e6);
+    }
+    return 0;
+  }
   if (argc > 5) {  // ncu mode: cyclic and run+carry only, 4 CTAs/SM, 2 launches each
     int bpg = 148 * 4 / G;
     if (bpg > chunks) bpg = chunks;
