@@ -118,9 +118,13 @@ class LevelShard:
     balance of the cost-sorted plan).
     """
 
-    def __init__(self, rank: int, world: int, process_group=None, coll_device=None):
+    def __init__(self, rank: int, world: int, process_group=None, coll_device=None,
+                 force_collective: bool = False):
         self.rank, self.world, self.pg = int(rank), int(world), process_group
         self.coll_device = coll_device
+        # issue the all-gather even with one rank (the single-GPU NCCL check in
+        # tests/test_gpu_dist.py: same tensors, dtypes and call as N ranks make)
+        self.force_collective = bool(force_collective)
         self.last_load = None
 
     @classmethod
@@ -157,7 +161,7 @@ class LevelShard:
         cdev = self.coll_device or dev
         send = local.to(cdev)
         allr = torch.empty((self.world * rows, width), dtype=torch.float64, device=cdev)
-        if self.world > 1:
+        if self.world > 1 or self.force_collective:
             dist.all_gather_into_tensor(allr, send, group=self.pg)
         else:
             allr.copy_(send)

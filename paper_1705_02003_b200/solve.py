@@ -374,7 +374,7 @@ class EnsembleSolver:
         _lib.call("uqg_status_clear", _lib.ctx(), _lib.stream())
         groups, pad = device_group(n, S, d_keys, sync=False)
         K = pad.numel()
-        if shard is None or shard.world == 1:
+        if shard is None or (shard.world == 1 and not getattr(shard, "force_collective", False)):
             it, cv, en, q = self.run_groups_device(d_coords, groups, K, S, clear_status=False)
         else:
             it, cv, en, q = shard.solve(

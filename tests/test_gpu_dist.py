@@ -73,6 +73,38 @@ def test_sharded_level_bitwise_equals_single_rank(tmp_path):
     assert doc["load"]["groups"] == [len(range(0, K, 2)), len(range(1, K, 2))]
 
 
+def test_nccl_collectives_on_one_gpu(tmp_path):
+    """The NCCL calls the N-GPU step makes - init with device_id, the level's
+    all_gather_into_tensor of float64 rows on the device, barrier, MAX
+    all-reduce - executed by one rank on the box's GPU (NCCL refuses two ranks
+    on one device): same results as the plain single-process level."""
+    import numpy as np
+    import torch
+
+    from paper_1705_02003_b200.configs import get
+
+    out = tmp_path / "nccl.json"
+    env = {k: v for k, v in os.environ.items() if k != "UQG_BENCH_SHARE_GPU"}
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+           "--master-addr", "127.0.0.1", "--master-port", _port(),
+           str(ROOT / "tools" / "dist_level.py"), "--config", "C1", "--out", str(out),
+           "--force-collective"]
+    r = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    doc = json.loads(out.read_text())
+    assert doc["world"] == 1 and doc["backend"] == "nccl"
+    cfg = get("C1")
+    z = np.load(ROOT / "bench_workloads" / "C1.npz")
+    dev = torch.device("cuda", 0)
+    solver = cfg.make_solver()
+    groups, pad, it, cv, en, q = solver.run_level_device(
+        torch.from_numpy(z["coords"]).to(dev), len(z["coords"]), cfg.ensemble_size,
+        torch.from_numpy(z["keys"]).to(dev))
+    assert doc["groups"] == groups.tolist() and doc["iters"] == it.tolist()
+    assert doc["ens"] == en.tolist() and doc["qoi"] == q.tolist()
+    assert doc["load"]["groups"] == [len(doc["ens"])]
+
+
 def test_bench_runs_with_two_ranks():
     r = _torchrun([str(ROOT / "bench.py"), "--gpus", "2", "--config", "C1", "--steps", "2",
                    "--warmup", "3"], {})

@@ -23,6 +23,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C1")
     ap.add_argument("--out", required=True)
+    ap.add_argument("--force-collective", action="store_true",
+                    help="issue the all-gather (and a barrier / MAX all-reduce as bench.py "
+                         "does) even with one rank: the single-GPU NCCL check")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -44,14 +47,21 @@ def main():
     coords, keys = z["coords"], z["keys"]
     solver = cfg.make_solver()
     shard = LevelShard.from_env(coll_device=torch.device("cpu") if share else dev)
+    shard.force_collective = a.force_collective
     d_c = torch.from_numpy(coords).to(dev)
     d_k = torch.from_numpy(keys).to(dev) if keys.size else None
     groups, pad, it, cv, en, q = solver.run_level_device(d_c, len(coords), cfg.ensemble_size, d_k,
                                                          shard)
+    if a.force_collective:  # the bench's other collectives, same tensors and devices
+        dist.barrier()
+        tt = torch.tensor([1.25], device=shard.coll_device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        assert float(tt.item()) == 1.25
     if dist.get_rank() == 0:
         Path(a.out).write_text(json.dumps({
             "world": dist.get_world_size(), "groups": groups.tolist(), "iters": it.tolist(),
-            "conv": cv.tolist(), "ens": en.tolist(), "qoi": q.tolist(), "load": shard.last_load}))
+            "conv": cv.tolist(), "ens": en.tolist(), "qoi": q.tolist(), "load": shard.last_load,
+            "backend": dist.get_backend()}))
     dist.destroy_process_group()
 
 
