@@ -447,7 +447,7 @@ def cpu_baseline(cfg, ids, coords, keys, gold, max_iters, gpu_rows=None):
     full, src = full_iterations(cfg, ens, gold, keys, max_iters)
     S = cfg.ensemble_size
     out = {"unit": "sample-solves/s" if not max_iters else "sample-iterations/s", "cores": 1,
-           "kind": cpu_path_kind() + ("" if r["full"] else " (projected)"), **host_info()}
+           "kind": cpu_path_kind(), "projected": not r["full"], **host_info()}
     if full is None and not r["full"]:
         out.update(value=None, sample="no iteration counts to project a full solve")
         return out
@@ -544,7 +544,7 @@ def run_reference(args, cfg):
         "config": config_dict(cfg, n, K, world, args.scaling, meta),
         "cpu_baseline": {
             "value": value, "unit": unit, "cores": P,
-            "kind": cpu_path_kind() + ("" if maxit is None else " (projected)"),
+            "kind": cpu_path_kind(), "projected": maxit is not None,
             "sample": f"per step {len(samples[0]) if samples else 0} of {K} groups (stratified: "
                       f"every {K / P:.1f}th in surrogate order, offset = step), one per process, "
                       f"1 BLAS thread each; {how}; " + (
