@@ -17,17 +17,19 @@
 // structure are not reproduced (memory-system probe).  Every wait is bounded
 // (clock64): on a protocol error the kernel sets a flag and falls through.
 //
-// Result (round 2, C3 shape, one B200): the protocol works - every variant
-// reproduces the reference kernel's Ap bit for bit with no bounded wait
-// tripping - but it is far from competitive: 16-row steps, 4 stages, 2 CTAs/SM:
-// CL = 2 1.96 TB/s, 4 1.40, 8 1.30; 32-row steps (1 CTA/SM): 1.98 / 1.69; 5 stages:
-// 2.00 - against 5.0 TB/s for the library's kernel.  The rate does not move with
-// the bytes per stage or the stage count, so it is not bytes in flight: 8-16
-// consumer warps per SM (shared memory triples every p tile, so few CTAs fit)
-// that each wait, compute a long dependent FP64 chain and signal three CTAs do
-// not cover their own latencies.  A competitive version would need a dedicated
-// producer warp, many more consumer warps per SM and tiles shared without the
-// 3x replication.
+// Result (round 2, C3 shape, one B200; every variant reproduces the reference
+// kernel's Ap bit for bit and no bounded wait trips):
+//  * first form - thread 0 of a consumer warp also produces, release-scoped remote
+//    arrives, step / unit indices by division: 1.3-2.0 TB/s (ncu: 52 % of the stall
+//    samples on the membar of the releasing arrive, which waits for the warp's Ap
+//    stores);
+//  * relaxed remote arrives (the stage reads are complete once their values are
+//    used): 2.8-3.2 TB/s;
+//  * plus a dedicated producer warp (9th warp, lane 0) that runs ahead of the
+//    consumers, and no divisions in the loops: CL = 2 6.20 TB/s, CL = 4 5.99,
+//    CL = 8 5.59 (4 stages of 16 rows, 2 CTAs/SM); 5 stages of 32 rows, CL = 2: 6.34
+//    - against 4.8 TB/s for the cyclic kernel of tools/face_run_probe.cu and 5.0 for
+//    the library's kernel in the bench.
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 --fmad=false -o /tmp/cmp tools/cluster_mc_probe.cu
 //   timeout 60 /tmp/cmp [cells=512] [G=42]        (S = 32)
@@ -86,7 +88,7 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
 __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, unsigned rank) {
   unsigned addr;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(addr) : "r"(smem_u32(bar)), "r"(rank));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr)
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr)
                : "memory");
 }
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, unsigned parity) {
@@ -155,13 +157,14 @@ __device__ __forceinline__ Span clip(int first, int rows, int limit) {
 }
 
 template <int CL, int NST, int KR>
-__global__ void __launch_bounds__(T, KR <= 16 ? 2 : 1) spmv_mc(Args a) {
+__global__ void __launch_bounds__(T + 32, KR <= 16 ? 2 : 1) spmv_mc(Args a) {
   constexpr int kRows = KR;
   constexpr size_t kPSlot = p_slot(KR), kTSlot = t_slot(KR), kStage = stage_doubles(KR);
   extern __shared__ __align__(128) double sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + (size_t)NST * kStage);
   uint64_t* empty = full + NST;
   const int m = a.m, N = a.N, t = threadIdx.x, sl = t % L, rr = t / L, warp = t / 32;
+  const bool producer = warp == NW;  // warps 0..NW-1 consume, lane 0 of warp NW produces
   const unsigned c = cluster_rank();
   const int n_units = (m + CL - 1) / CL;
   const int n_clusters = gridDim.x / CL, cid = blockIdx.x / CL;
@@ -179,99 +182,98 @@ __global__ void __launch_bounds__(T, KR <= 16 ? 2 : 1) spmv_mc(Args a) {
   const unsigned short pmask = (unsigned short)((1u << c) | (has_w ? 1u << (c - 1) : 0u) |
                                                 (has_e ? 1u << (c + 1) : 0u));
   const unsigned short tmask = (unsigned short)((1u << c) | (has_w ? 1u << (c - 1) : 0u));
-  // my units: cid, cid + n_clusters, ... over all groups; total pipeline iterations
-  int my_units = 0;
-  for (int u = cid; u < n_units * a.G; u += n_clusters) ++my_units;
-  const int total = my_units * steps;
+  double2 acc = make_double2(0.0, 0.0);
+  int s = 0, it = 0;
+  unsigned ph = 0;  // parity of the FULL phase of the current iteration
   bool ok = true;
-
-  // line of this CTA in unit k (the last unit of a group is shifted back so that
-  // every CTA has a line: a few lines are then computed twice, identically)
-  auto unit_line = [&](int k, int& g) -> int {
-    const int u = cid + k * n_clusters;
-    g = u / n_units;
+  // units of this cluster: cid, cid + n_clusters, ... over all groups
+  for (int u = cid; u < n_units * a.G && ok; u += n_clusters) {
+    const int g = u / n_units;
     int l0 = (u - g * n_units) * CL;
-    if (l0 + CL > m) l0 = m - CL;
-    return l0 + (int)c;
-  };
-  // producer: everything this CTA fetches for pipeline iteration `it`
-  auto produce = [&](int it) {
-    const int k = it / steps, st = it - k * steps, s = it % NST;
-    int g;
-    const int i = unit_line(k, g);
+    if (l0 + CL > m) l0 = m - CL;  // last unit of a group shifted back: every CTA has a line
+    const int i = l0 + (int)c;     // this CTA's line
+    const bool w = i > 0, e = i + 1 < m;
     const double* pg = a.p + (size_t)g * N * S;
     const double* txg = a.tx + (size_t)g * (N + m) * S;
-    double* stage = sm + (size_t)s * kStage;
-    const int j0 = st * kRows;
-    const Span ps = clip(j0 - 1, kRows + 2, m), ts = clip(j0, kRows, m);
-    const unsigned pb = (unsigned)ps.n * S * 8, tb = (unsigned)ts.n * S * 8;
-    const bool w = i > 0, e = i + 1 < m;
-    // bytes that will land in MY stage: own p + own faces, west p, east p (if any) + east faces
-    unsigned expect = pb + tb + (w ? pb : 0u) + (e ? pb : 0u) + tb;
-    if (it >= NST && !mbar_wait(&empty[s], (unsigned)(((it / NST) - 1) & 1), a.err)) ok = false;
-    fence_proxy_async();
-    mbar_expect_tx(&full[s], expect);
-    const size_t poff = (size_t)(ps.lo - (j0 - 1)) * S, toff = (size_t)(ts.lo - j0) * S;
-    // own line: p to west / self / east, faces to west / self
-    bulk_mc(stage + (size_t)(i % 3) * kPSlot + poff, pg + ((size_t)i * m + ps.lo) * S, pb, &full[s],
-            pmask);
-    bulk_mc(stage + 3 * kPSlot + (size_t)(i % 2) * kTSlot + toff, txg + ((size_t)i * m + ts.lo) * S,
-            tb, &full[s], tmask);
-    if (!has_w && w)  // cluster's west edge: line i - 1 is nobody's
-      bulk_uc(stage + (size_t)((i + 2) % 3) * kPSlot + poff, pg + ((size_t)(i - 1) * m + ps.lo) * S,
-              pb, &full[s]);
-    if (!has_e) {  // cluster's east edge: line i + 1 (its p only if it exists; its faces always)
-      if (e)
-        bulk_uc(stage + (size_t)((i + 1) % 3) * kPSlot + poff,
-                pg + ((size_t)(i + 1) * m + ps.lo) * S, pb, &full[s]);
-      bulk_uc(stage + 3 * kPSlot + (size_t)((i + 1) % 2) * kTSlot + toff,
-              txg + ((size_t)(i + 1) * m + ts.lo) * S, tb, &full[s]);
-    }
-  };
-
-  if (t == 0)
-    for (int it = 0; it < NST - 1 && it < total; ++it) produce(it);
-
-  double2 acc = make_double2(0.0, 0.0);
-  for (int it = 0; it < total; ++it) {
-    if (t == 0 && it + NST - 1 < total) produce(it + NST - 1);
-    const int k = it / steps, st = it - k * steps, s = it % NST;
-    int g;
-    const int i = unit_line(k, g);
-    if (!mbar_wait(&full[s], (unsigned)((it / NST) & 1), a.err)) ok = false;
-    const double* stage = sm + (size_t)s * kStage;
+    const size_t pc_slot = (size_t)(i % 3) * kPSlot, pw_slot = (size_t)((i + 2) % 3) * kPSlot,
+                 pe_slot = (size_t)((i + 1) % 3) * kPSlot, tw_slot = 3 * kPSlot + (size_t)(i % 2) * kTSlot,
+                 te_slot = 3 * kPSlot + (size_t)((i + 1) % 2) * kTSlot;
+    if (producer) {
+      // the whole warp walks the loop (aligned cluster barrier at the end); lane 0 issues
+      for (int st = 0; st < steps; ++st, ++it) {
+        if ((t & 31) == 0) {
+          double* stage = sm + (size_t)s * kStage;
+          const int j0 = st * kRows;
+          const Span ps = clip(j0 - 1, kRows + 2, m), ts = clip(j0, kRows, m);
+          const unsigned pb = (unsigned)ps.n * S * 8, tb = (unsigned)ts.n * S * 8;
+          // bytes landing in MY stage: own p + own faces, west p, east p (if any) + east faces
+          const unsigned expect = pb + tb + (w ? pb : 0u) + (e ? pb : 0u) + tb;
+          if (it >= NST && !mbar_wait(&empty[s], ph ^ 1u, a.err)) ok = false;
+          if (ok) {
+            fence_proxy_async();
+            mbar_expect_tx(&full[s], expect);
+            const size_t poff = (size_t)(ps.lo - (j0 - 1)) * S, toff = (size_t)(ts.lo - j0) * S;
+            bulk_mc(stage + pc_slot + poff, pg + ((size_t)i * m + ps.lo) * S, pb, &full[s], pmask);
+            bulk_mc(stage + tw_slot + toff, txg + ((size_t)i * m + ts.lo) * S, tb, &full[s], tmask);
+            if (!has_w && w)  // cluster's west edge: line i - 1 is nobody's
+              bulk_uc(stage + pw_slot + poff, pg + ((size_t)(i - 1) * m + ps.lo) * S, pb, &full[s]);
+            if (!has_e) {  // cluster's east edge: line i + 1 (p only if it exists; faces always)
+              if (e)
+                bulk_uc(stage + pe_slot + poff, pg + ((size_t)(i + 1) * m + ps.lo) * S, pb, &full[s]);
+              bulk_uc(stage + te_slot + toff, txg + ((size_t)(i + 1) * m + ts.lo) * S, tb, &full[s]);
+            }
+          }
+        }
+        ok = __shfl_sync(0xffffffffu, (int)ok, 0) != 0;
+        if (!ok) break;
+        if (++s == NST) {
+          s = 0;
+          ph ^= 1u;
+        }
+      }
+    } else {
+      double* apl = a.ap + (size_t)g * N * S + (size_t)i * m * S + 2 * sl;
+      for (int st = 0; st < steps; ++st, ++it) {
+        if (!mbar_wait(&full[s], ph, a.err)) ok = false;
+        ok = __all_sync(0xffffffffu, (int)ok) != 0;
+        if (!ok) break;
+        const double* stage = sm + (size_t)s * kStage;
 #pragma unroll
-    for (int q = 0; q < kRows / 16; ++q) {
-      const int jl = q * 16 + rr, j = st * kRows + jl;
-      if (j < m) {
-        const bool w = i > 0, e = i + 1 < m, sflag = j > 0, n = j < m - 1;
-        const size_t po = (size_t)(jl + 1) * S + 2 * sl, to = (size_t)jl * S + 2 * sl;
-        const double* pcs = stage + (size_t)(i % 3) * kPSlot;
-        const double2 pc = *reinterpret_cast<const double2*>(pcs + po);
-        const double2 ps = *reinterpret_cast<const double2*>(pcs + po - S);
-        const double2 pn = *reinterpret_cast<const double2*>(pcs + po + S);
-        const double2 pw = *reinterpret_cast<const double2*>(stage + (size_t)((i + 2) % 3) * kPSlot + po);
-        const double2 pe = *reinterpret_cast<const double2*>(stage + (size_t)((i + 1) % 3) * kPSlot + po);
-        const double2 tw = *reinterpret_cast<const double2*>(stage + 3 * kPSlot + (size_t)(i % 2) * kTSlot + to);
-        const double2 te = *reinterpret_cast<const double2*>(stage + 3 * kPSlot + (size_t)((i + 1) % 2) * kTSlot + to);
-        double2 y;
-        y.x = row1(tw.x, te.x, pw.x, ps.x, pc.x, pn.x, pe.x, w, sflag, n, e);
-        y.y = row1(tw.y, te.y, pw.y, ps.y, pc.y, pn.y, pe.y, w, sflag, n, e);
-        *reinterpret_cast<double2*>(a.ap + (size_t)g * N * S + ((size_t)i * m + j) * S + 2 * sl) = y;
-        acc.x = fma(pc.x, y.x, acc.x);
-        acc.y = fma(pc.y, y.y, acc.y);
+        for (int q = 0; q < kRows / 16; ++q) {
+          const int jl = q * 16 + rr, j = st * kRows + jl;
+          if (j < m) {
+            const bool sflag = j > 0, n = j < m - 1;
+            const size_t po = (size_t)(jl + 1) * S + 2 * sl, to = (size_t)jl * S + 2 * sl;
+            const double2 pc = *reinterpret_cast<const double2*>(stage + pc_slot + po);
+            const double2 ps = *reinterpret_cast<const double2*>(stage + pc_slot + po - S);
+            const double2 pn = *reinterpret_cast<const double2*>(stage + pc_slot + po + S);
+            const double2 pw = *reinterpret_cast<const double2*>(stage + pw_slot + po);
+            const double2 pe = *reinterpret_cast<const double2*>(stage + pe_slot + po);
+            const double2 tw = *reinterpret_cast<const double2*>(stage + tw_slot + to);
+            const double2 te = *reinterpret_cast<const double2*>(stage + te_slot + to);
+            double2 y;
+            y.x = row1(tw.x, te.x, pw.x, ps.x, pc.x, pn.x, pe.x, w, sflag, n, e);
+            y.y = row1(tw.y, te.y, pw.y, ps.y, pc.y, pn.y, pe.y, w, sflag, n, e);
+            *reinterpret_cast<double2*>(apl + (size_t)j * S) = y;
+            acc.x = fma(pc.x, y.x, acc.x);
+            acc.y = fma(pc.y, y.y, acc.y);
+          }
+        }
+        // this warp is done with stage s: tell every CTA that writes into my stage
+        __syncwarp();
+        if ((t & 31) == 0) {
+          mbar_arrive_remote(&empty[s], c);
+          if (has_w) mbar_arrive_remote(&empty[s], c - 1);
+          if (has_e) mbar_arrive_remote(&empty[s], c + 1);
+        }
+        if (++s == NST) {
+          s = 0;
+          ph ^= 1u;
+        }
       }
     }
-    // this warp is done with stage s: tell every CTA that writes into my stage
-    __syncwarp();
-    if ((t & 31) == 0) {
-      mbar_arrive_remote(&empty[s], c);
-      if (has_w) mbar_arrive_remote(&empty[s], c - 1);
-      if (has_e) mbar_arrive_remote(&empty[s], c + 1);
-    }
-    if (!ok) break;
   }
-  a.out[(size_t)blockIdx.x * T + t] = acc.x + acc.y + (double)warp * 0.0;
+  if (!producer) a.out[(size_t)blockIdx.x * T + t] = acc.x + acc.y;
   cluster_sync();  // nobody exits while a neighbour may still arrive on its barriers
 }
 
@@ -323,7 +325,7 @@ float run(const Args& a, int reps, bool* ok) {
   auto kern = spmv_mc<CL, NST, KR>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
-  cfg.blockDim = dim3(T);
+  cfg.blockDim = dim3(T + 32);
   cfg.dynamicSmemBytes = smem;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
