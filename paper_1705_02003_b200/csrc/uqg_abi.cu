@@ -898,6 +898,10 @@ int pcg_impl(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const 
     return UQG_ECUDA;
   }
   for (int g = 0; g < G; ++g) {
+    if (h_status[g] & 4) {
+      set_error("uqg_pcg: cluster SpMV pipeline failed (group " + std::to_string(g) + ")");
+      return UQG_ECUDA;
+    }
     if (h_status[g] == 2) {
       set_error("non-finite residual in active lane (group " + std::to_string(g) + ")");
       return UQG_EBREAKDOWN;

@@ -272,21 +272,33 @@ __device__ __forceinline__ void stv(double* p, const double (&o)[V]) {
 // partials, then super-partials); tickets [g*tstride]: group ticket, then one
 // per super-chunk.
 
-template <int NS>
+// NB = 0: the reducing threads are the whole block (__syncthreads); NB > 0: they
+// are its first NB threads, synchronised by named barrier 1 (a kernel with
+// extra warps that do not take part in reductions, e.g. a TMA producer warp).
+template <int NB>
+__device__ __forceinline__ void block_sync() {
+  if constexpr (NB == 0) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync 1, %0;" ::"n"(NB) : "memory");
+  }
+}
+
+template <int NS, int NB = 0>
 __device__ __forceinline__ void tree_rows(double* red, int T, int Lp, int R, int t) {
   for (int st = R >> 1; st > 0; st >>= 1) {
     if ((t / Lp) < st) {
 #pragma unroll
       for (int v = 0; v < NS; ++v) red[v * T + t] += red[v * T + t + st * Lp];
     }
-    __syncthreads();
+    block_sync<NB>();
   }
 }
 
 // Tickets of nk chunks (chunk0 + k*stride) whose partials are written and
 // fenced (all threads call after a __syncthreads).  Returns true in the one
 // block that completes the group, with the totals in red[].
-template <int NV, int V>
+template <int NV, int V, int NB = 0>
 __device__ bool finish_chunks(double* red, double* part, unsigned int* ticket, int g, int chunk0,
                               int stride, int nk, const Geo& geo) {
   constexpr int NS = NV * V;
@@ -301,7 +313,7 @@ __device__ bool finish_chunks(double* red, double* part, unsigned int* ticket, i
       const unsigned int tk = atomicAdd(gt, (unsigned)nk);
       s_flag = (tk + (unsigned)nk == (unsigned)C);
     }
-    __syncthreads();
+    block_sync<NB>();
     if (!s_flag) return false;
   } else {
     // one thread per chunk of the batch takes its super-chunk's ticket
@@ -312,7 +324,7 @@ __device__ bool finish_chunks(double* red, double* part, unsigned int* ticket, i
       const unsigned int tk = atomicAdd(gt + 1 + si, 1u);
       s_super[t] = (tk + 1u == (unsigned)(c_hi - c_lo)) ? si : -1;
     }
-    __syncthreads();
+    block_sync<NB>();
     // every super-chunk this batch completed: its partials summed in chunk order
     // (all completed super-chunks at once, the loads of one sum issued together)
     __threadfence();
@@ -340,7 +352,7 @@ __device__ bool finish_chunks(double* red, double* part, unsigned int* ticket, i
       }
     }
     __threadfence();
-    __syncthreads();
+    block_sync<NB>();
     if (t == 0) {
       int fin = 0;
       for (int k = 0; k < nk; ++k) {
@@ -352,7 +364,7 @@ __device__ bool finish_chunks(double* red, double* part, unsigned int* ticket, i
       }
       s_flag = fin;
     }
-    __syncthreads();
+    block_sync<NB>();
     const bool last = s_flag;
     if (!last) return false;
     rows = geo.nsc;
@@ -373,11 +385,11 @@ __device__ bool finish_chunks(double* red, double* part, unsigned int* ticket, i
           acc[v * V + j] += __ldcg(&gp[((size_t)(row0 + cc) * NV + v) * S + V * sl + j]);
     }
   }
-  __syncthreads();  // red[] may still hold the caller's tree values
+  block_sync<NB>();  // red[] may still hold the caller's tree values
 #pragma unroll
   for (int v = 0; v < NS; ++v) red[v * T + t] = acc[v];
-  __syncthreads();
-  tree_rows<NS>(red, T, Lp, R, t);
+  block_sync<NB>();
+  tree_rows<NS, NB>(red, T, Lp, R, t);
   if (t == 0) gt[0] = 0u;  // ready for the next reduction on this counter
   return true;
 }
@@ -417,19 +429,19 @@ __device__ bool reduce_lanes(const double (&val)[NV][V], double* red, double* pa
 // The in-block half of reduce_lanes_batch: one tree pass over the rows for all
 // nk chunks' values in red[((k*NV + v)*V + j)*T + t], then the chunk partials
 // written to part (no fence, no ticket).
-template <int NV, int V>
+template <int NV, int V, int NB = 0>
 __device__ void batch_tree_partials(double* red, double* part, int g, int chunk0, int stride,
                                     int nk, const Geo& geo) {
   constexpr int NS = NV * V;
   const int t = threadIdx.x;
   const int T = geo.T, Lp = geo.Lp, R = geo.R, L = geo.L, S = geo.S;
   const int ns = nk * NS;
-  __syncthreads();
+  block_sync<NB>();
   for (int st = R >> 1; st > 0; st >>= 1) {
     if ((t / Lp) < st) {
       for (int v = 0; v < ns; ++v) red[v * T + t] += red[v * T + t + st * Lp];
     }
-    __syncthreads();
+    block_sync<NB>();
   }
   if (t < L) {
     for (int k = 0; k < nk; ++k)
@@ -442,13 +454,13 @@ __device__ void batch_tree_partials(double* red, double* part, int g, int chunk0
   }
 }
 
-template <int NV, int V>
+template <int NV, int V, int NB = 0>
 __device__ bool reduce_lanes_batch(double* red, double* part, unsigned int* ticket, int g,
                                    int chunk0, int stride, int nk, const Geo& geo) {
-  batch_tree_partials<NV, V>(red, part, g, chunk0, stride, nk, geo);
+  batch_tree_partials<NV, V, NB>(red, part, g, chunk0, stride, nk, geo);
   __threadfence();
-  __syncthreads();
-  return finish_chunks<NV, V>(red, part, ticket, g, chunk0, stride, nk, geo);
+  block_sync<NB>();
+  return finish_chunks<NV, V, NB>(red, part, ticket, g, chunk0, stride, nk, geo);
 }
 
 // "last block of the group" without values (for state transitions); uses the

@@ -883,6 +883,277 @@ __global__ void __launch_bounds__(256, MINB) pcg_spmv_tma_kernel(long long N, lo
   }
 }
 
+// ---------------------------------------------------------------------------
+// Cluster form of the face SpMV (S = 32, constant y-faces, reduction chunks of
+// exactly m + 1 rows: C3).  The two CTAs of a thread-block cluster take two
+// ADJACENT chunks and walk them tile by tile (16 rows).  A ninth warp's lane 0
+// fetches, per tile, its chunk's 18 p rows and 17 x-face rows from L2 ONCE with
+// cp.async.bulk ... .multicast::cluster into the shared memory of every CTA
+// that uses them: the p rows of chunk X are the centre band of X, the east band
+// of X - 1 and the west band of X + 1 (rows +- m = chunk rows -+ 1), its faces
+// the west faces of X and the east faces of X - 1.  A stage holds three p slots
+// (chunk mod 3) and two face slots (chunk mod 2), so a tile lands at the same
+// offset in both CTAs; the cluster's outer bands are fetched by the CTA that
+// needs them.  Per stage: a FULL mbarrier carrying the transaction bytes of all
+// that lands in the stage, and an EMPTY mbarrier on which the eight consumer
+// warps of both CTAs arrive (remotely for the other CTA) once they have read it.
+// The consumers keep the cyclic row map (thread-row rr takes rows rr + 16 k of
+// its chunk in order), FaceRow's arithmetic and the batched chunk reduction, so
+// every bit equals pcg_spmv_fv2d_kernel's.  Every wait is bounded: a protocol
+// failure raises the group's status instead of hanging.
+// (tools/cluster_mc_probe.cu: 6.2 TB/s against 4.8-5.0 for the plain kernel.)
+constexpr int kMcStages = 4;  // stages of one 16-row tile
+constexpr int kMcBatch = 4;   // chunks per batched reduction (shared memory: 2 CTAs/SM)
+constexpr int kMcT = 256;     // consumer threads (8 warps) + one producer warp
+constexpr size_t kMcPSlot = 18 * 32, kMcTSlot = 17 * 32;  // doubles
+constexpr size_t kMcStage = 3 * kMcPSlot + 2 * kMcTSlot;
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ unsigned cluster_ctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile(
+      "barrier.cluster.arrive.release.aligned;\n\t"
+      "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the barrier at the same offset in CTA `rank` of the cluster; relaxed:
+// the stage reads it signals are complete once their values have been used
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, unsigned rank) {
+  unsigned addr;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(addr) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_wait_bounded(uint64_t* bar, uint32_t parity) {
+  const long long t0 = clock64();
+  for (;;) {
+    unsigned ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return true;
+    if (clock64() - t0 > (1LL << 33)) return false;  // seconds: never hang
+  }
+}
+__device__ __forceinline__ void bulk_g2s_mc(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar, unsigned short mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+
+// rows [first, first + rows) clipped to [0, limit): first valid row and count
+struct McSpan {
+  long long lo;
+  int n;
+};
+__device__ __forceinline__ McSpan mc_clip(long long first, int rows, long long limit) {
+  const long long lo = first < 0 ? 0 : first;
+  const long long hi = first + rows > limit ? limit : first + rows;
+  return {lo, hi > lo ? (int)(hi - lo) : 0};
+}
+
+__global__ void __launch_bounds__(kMcT + 32, 2) pcg_spmv_fv2d_mc_kernel(
+    long long N, Geo geo, PcgState st, Fv2dOp op, const double* __restrict__ p,
+    double* __restrict__ ap) {
+  constexpr int V = 2, S = 32, L = 16, R = 16, T = kMcT, NW = T / 32, NST = kMcStages;
+  extern __shared__ __align__(16) double red[];
+  double* stages = red + (size_t)kMcBatch * V * T;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stages + (size_t)NST * kMcStage);
+  uint64_t* empty = full + NST;
+  const int g = blockIdx.y, t = threadIdx.x;
+  if (st.done[g] != kRunning) return;  // the same for both CTAs of the cluster
+  const int xs = xslot(st, st.it[g]);  // buffer of p_k / alpha_k
+  p += (size_t)xs * st.pstride;
+  const unsigned c = cluster_ctarank();  // 0: even chunk of the pair, 1: odd
+  const int m = op.m, ct = (int)geo.chunk_tiles, crows = ct * R;  // crows == m + 1
+  const int ncl = gridDim.x / 2, cid = blockIdx.x / 2;
+  const int chunks = geo.chunks, npairs = (chunks + 1) / 2;
+  const double* pg = p + (size_t)g * N * S;
+  const double* txg = op.tx + (size_t)g * (N + m) * S;
+  double* apg = ap + (size_t)g * N * S;
+  const long long plim = N, tlim = N + m;
+  const bool producer = t >= T;
+  if (t == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 2 * NW);  // the consumer warps of both CTAs
+    }
+    fence_mbar_init();
+  }
+  cluster_sync_all();
+  int s = 0;
+  unsigned ph = 0;  // parity of the FULL phase of the current pipeline iteration
+  long long it = 0;
+  bool ok = true;
+  const int sl = t % L, rr = t / L;
+  for (int q0 = cid; q0 < npairs && ok; q0 += kMcBatch * ncl) {
+    int nkp = (npairs - 1 - q0) / ncl + 1;  // chunk pairs of this batch
+    if (nkp > kMcBatch) nkp = kMcBatch;
+    int nk_mine = 0;                        // ... and my existing chunks among them
+    for (int k = 0; k < nkp && ok; ++k) {
+      const int X = 2 * (q0 + k * ncl) + (int)c;  // my chunk (>= chunks: no rows)
+      if (X < chunks) ++nk_mine;
+      const size_t pc_slot = (size_t)(X % 3) * kMcPSlot, pw_slot = (size_t)((X + 2) % 3) * kMcPSlot,
+                   pe_slot = (size_t)((X + 1) % 3) * kMcPSlot,
+                   tw_slot = 3 * kMcPSlot + (size_t)(X % 2) * kMcTSlot,
+                   te_slot = 3 * kMcPSlot + (size_t)((X + 1) % 2) * kMcTSlot;
+      const long long c0 = (long long)X * crows;  // first row of my chunk
+      if (producer) {
+        // chunks X - 1, X, X + 1 entirely inside the vectors: every tile is whole
+        const bool interior = c0 - crows - 1 >= 0 && c0 + 2LL * crows + 1 <= plim;
+        for (int tile = 0; tile < ct; ++tile, ++it) {
+          if ((t & 31) == 0 && interior) {
+            double* stage = stages + (size_t)s * kMcStage;
+            const long long r0 = c0 + (long long)tile * R;
+            constexpr uint32_t pb = (R + 2) * S * 8u, tb = (R + 1) * S * 8u;
+            if (it >= NST && !mbar_wait_bounded(&empty[s], ph ^ 1u)) ok = false;
+            if (ok) {
+              fence_proxy_async();
+              mbar_expect_tx(&full[s], 3 * pb + 2 * tb);
+              bulk_g2s_mc(stage + pc_slot, pg + (r0 - 1) * S, pb, &full[s], (unsigned short)3);
+              bulk_g2s_mc(stage + tw_slot, txg + (r0 - 1) * S, tb, &full[s],
+                          (unsigned short)(c == 0 ? 1 : 3));
+              if (c == 0) {
+                bulk_g2s(stage + pw_slot, pg + (r0 - crows - 1) * S, pb, &full[s]);
+              } else {
+                bulk_g2s(stage + pe_slot, pg + (r0 + crows - 1) * S, pb, &full[s]);
+                bulk_g2s(stage + te_slot, txg + (r0 + crows - 1) * S, tb, &full[s]);
+              }
+            }
+          } else if ((t & 31) == 0) {
+            double* stage = stages + (size_t)s * kMcStage;
+            const long long r0 = c0 + (long long)tile * R;
+            // tiles of chunks X - 1, X, X + 1 (their rows r0 -+ crows): what lands in my stage
+            const McSpan pX = mc_clip(r0 - 1, R + 2, plim), tX = mc_clip(r0 - 1, R + 1, tlim);
+            const McSpan pW = mc_clip(r0 - crows - 1, R + 2, plim);
+            const McSpan pE = mc_clip(r0 + crows - 1, R + 2, plim),
+                         tE = mc_clip(r0 + crows - 1, R + 1, tlim);
+            const uint32_t expect = (uint32_t)(pX.n + tX.n + pW.n + pE.n + tE.n) * S * 8u;
+            if (it >= NST && !mbar_wait_bounded(&empty[s], ph ^ 1u)) ok = false;
+            if (ok) {
+              fence_proxy_async();
+              if (expect) mbar_expect_tx(&full[s], expect);
+              else mbar_arrive(&full[s]);
+              // my chunk: p rows to both CTAs, faces to myself and to my west neighbour
+              if (pX.n)
+                bulk_g2s_mc(stage + pc_slot + (size_t)(pX.lo - (r0 - 1)) * S, pg + pX.lo * S,
+                            (uint32_t)pX.n * S * 8u, &full[s], (unsigned short)3);
+              if (tX.n)
+                bulk_g2s_mc(stage + tw_slot + (size_t)(tX.lo - (r0 - 1)) * S, txg + tX.lo * S,
+                            (uint32_t)tX.n * S * 8u, &full[s], (unsigned short)(c == 0 ? 1 : 3));
+              if (c == 0) {  // the cluster's west edge: chunk X - 1 is nobody's
+                if (pW.n)
+                  bulk_g2s(stage + pw_slot + (size_t)(pW.lo - (r0 - crows - 1)) * S, pg + pW.lo * S,
+                           (uint32_t)pW.n * S * 8u, &full[s]);
+              } else {  // the east edge: chunk X + 1
+                if (pE.n)
+                  bulk_g2s(stage + pe_slot + (size_t)(pE.lo - (r0 + crows - 1)) * S, pg + pE.lo * S,
+                           (uint32_t)pE.n * S * 8u, &full[s]);
+                if (tE.n)
+                  bulk_g2s(stage + te_slot + (size_t)(tE.lo - (r0 + crows - 1)) * S,
+                           txg + tE.lo * S, (uint32_t)tE.n * S * 8u, &full[s]);
+              }
+            }
+          }
+          ok = __shfl_sync(0xffffffffu, (int)ok, 0) != 0;
+          if (!ok) break;
+          if (++s == NST) {
+            s = 0;
+            ph ^= 1u;
+          }
+        }
+      } else {
+        double acc[V] = {0.0, 0.0};
+        long long row = c0 + rr;
+        long long cend = c0 + crows;
+        if (cend > N) cend = N;
+        int i0 = (int)(row / m), j0 = (int)(row - (long long)i0 * m);
+        for (int tile = 0; tile < ct; ++tile, ++it, row += R) {
+          if (!mbar_wait_bounded(&full[s], ph)) ok = false;
+          ok = __all_sync(0xffffffffu, (int)ok) != 0;
+          if (!ok) break;
+          if (row < cend) {
+            const double* stage = stages + (size_t)s * kMcStage + V * sl;
+            const bool w = i0 > 0, sf = j0 > 0, nf = j0 < m - 1, e = i0 < m - 1;
+            const double2 pc = *reinterpret_cast<const double2*>(stage + pc_slot + (size_t)(rr + 1) * S);
+            const double2 ps = *reinterpret_cast<const double2*>(stage + pc_slot + (size_t)rr * S);
+            const double2 pn = *reinterpret_cast<const double2*>(stage + pc_slot + (size_t)(rr + 2) * S);
+            const double2 pw = *reinterpret_cast<const double2*>(stage + pw_slot + (size_t)(rr + 2) * S);
+            const double2 pe = *reinterpret_cast<const double2*>(stage + pe_slot + (size_t)rr * S);
+            const double2 tw = *reinterpret_cast<const double2*>(stage + tw_slot + (size_t)(rr + 1) * S);
+            const double2 te = *reinterpret_cast<const double2*>(stage + te_slot + (size_t)rr * S);
+            const double twv[V] = {tw.x, tw.y}, tev[V] = {te.x, te.y}, pwv[V] = {pw.x, pw.y},
+                         psv[V] = {ps.x, ps.y}, pcv[V] = {pc.x, pc.y}, pnv[V] = {pn.x, pn.y},
+                         pev[V] = {pe.x, pe.y};
+            double y[V];
+#pragma unroll
+            for (int j = 0; j < V; ++j) {  // FaceRow::apply with constant y-faces a_y
+              const double d = __dadd_rn(__dadd_rn(__dadd_rn(twv[j], tev[j]), op.a_y), op.a_y);
+              double a = 0.0;
+              if (w) a = __dadd_rn(a, __dmul_rn(-twv[j], pwv[j]));
+              if (sf) a = __dadd_rn(a, __dmul_rn(-op.a_y, psv[j]));
+              a = __dadd_rn(a, __dmul_rn(d, pcv[j]));
+              if (nf) a = __dadd_rn(a, __dmul_rn(-op.a_y, pnv[j]));
+              if (e) a = __dadd_rn(a, __dmul_rn(-tev[j], pev[j]));
+              y[j] = a;
+              acc[j] = __fma_rn(pcv[j], a, acc[j]);
+            }
+            stv<V>(apg + row * S + V * sl, y);
+          }
+          j0 += R;
+          while (j0 >= m) {
+            j0 -= m;
+            ++i0;
+          }
+          // this warp has read stage s: tell both CTAs' producers
+          __syncwarp();
+          if ((t & 31) == 0) {
+            mbar_arrive_cluster(&empty[s], 0);
+            mbar_arrive_cluster(&empty[s], 1);
+          }
+          if (++s == NST) {
+            s = 0;
+            ph ^= 1u;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j) red[(k * V + j) * T + t] = acc[j];
+      }
+    }
+    if (producer || !ok) continue;
+    // the batch's chunk partials and tickets (my chunks: 2 q0 + c, stride 2 ncl)
+    if (nk_mine == 0) continue;
+    if (!reduce_lanes_batch<1, V, kMcT>(red, st.part, st.ticket, g, 2 * q0 + (int)c, 2 * ncl,
+                                        nk_mine, geo))
+      continue;
+    if (t < geo.L) {
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const size_t l = (size_t)g * S + V * t + j;
+        const double pap = red[j * geo.T + t];
+        const unsigned char fr = st.frozen[l] | (unsigned char)(pap <= DBL_MIN);
+        st.frozen[l] = fr;
+        st.alpha[(size_t)xs * st.G * S + l] = fr ? 0.0 : __ddiv_rn(st.rz[l], pap);
+      }
+    }
+    if (t == 0) st.it[g] += 1;
+  }
+  if (!ok && (t & 31) == 0) atomicOr(&st.status[g], 4);  // pipeline protocol failure
+  cluster_sync_all();  // nobody exits while the other CTA may still signal its barriers
+}
+
 // ensemble_iterations = max over lanes (ensemble.py:277)
 __global__ void pcg_finalize_kernel(PcgState st, int G, int S, int* ens_iters) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -972,8 +1243,67 @@ void launch_spmv_fv2d(const Geo& geo, int G, cudaStream_t s, long long N, const 
   UQG_DISPATCH_V(gl, spmv_fv2d_kernel, dim3(gl.B, G), 0, s, N, gl, op, x, y);
 }
 
+// UQG_FACE_CLUSTER=1: the cluster / TMA-multicast face SpMV where it applies
+// (S = 32, constant y-faces, chunks of m + 1 rows, 16-byte aligned vectors);
+// bit-identical to the plain kernel.
+static bool face_cluster_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("UQG_FACE_CLUSTER");
+    return e && atoi(e) != 0;
+  }();
+  return on;
+}
+
+static bool launch_pcg_spmv_fv2d_mc(const Geo& geo, int G, cudaStream_t s, long long N,
+                                    const PcgState& st, const Fv2dOp& op, const double* p,
+                                    double* ap) {
+  if (geo.V != 2 || geo.S != 32 || geo.Lp != 16 || geo.T != kMcT || op.ty) return false;
+  if (geo.chunk_tiles * geo.R != (long long)op.m + 1 || geo.chunks < 2) return false;
+  if ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(op.tx) |
+       (uintptr_t)(st.pstride * sizeof(double))) & 15)
+    return false;
+  const size_t smem = ((size_t)kMcBatch * 2 * kMcT + (size_t)kMcStages * kMcStage) * sizeof(double) +
+                      2 * kMcStages * sizeof(uint64_t);
+  static int max_clusters = -1;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cfg.blockDim = dim3(kMcT + 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  if (max_clusters < 0) {
+    if (cudaFuncSetAttribute(pcg_spmv_fv2d_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess) {
+      cudaGetLastError();
+      max_clusters = 0;
+    } else {
+      cfg.gridDim = dim3(2, 1);
+      int mc = 0;
+      if (cudaOccupancyMaxActiveClusters(&mc, pcg_spmv_fv2d_mc_kernel, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        mc = 0;
+      }
+      max_clusters = mc;
+    }
+  }
+  if (max_clusters < 1) return false;
+  // clusters per group sized like blocks per group: pairs of chunks over resident clusters
+  const int npairs = (geo.chunks + 1) / 2;
+  const int b = pick_blocks(geo.gact, npairs, max_clusters);
+  cfg.gridDim = dim3(2 * b, G);
+  Geo gl = geo;
+  gl.B = 2 * b;
+  return cudaLaunchKernelEx(&cfg, pcg_spmv_fv2d_mc_kernel, N, gl, st, op, p, ap) == cudaSuccess;
+}
+
 void launch_pcg_spmv_fv2d(const Geo& geo, int G, cudaStream_t s, long long N, const PcgState& st,
                           const Fv2dOp& op, const double* p, double* ap) {
+  if (face_cluster_enabled() && launch_pcg_spmv_fv2d_mc(geo, G, s, N, st, op, p, ap)) return;
   static SlotCache cf2, cf1;
   const Geo gl = geo.V == 2
                      ? sized(geo, cf2, pcg_spmv_fv2d_kernel<2>, geo.T,

@@ -238,3 +238,36 @@ def test_small_and_odd_meshes_match_oracle(cells, S, maxit):
         assert abs(q_d[i] - q_o[i]) <= 1e-8 * abs(q_o[i])
     assert got[False][0] == it_d and got[False][2] == notes_d
     assert all(got[False][1][i] == q_d[i] for i in ids)
+
+
+_CLUSTER_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1705_02003_b200 as uq
+out = []
+for cells, G in ((128, 5), (128, 1), (512, 2)):      # chunks of m + 1 rows at S = 32
+    f = uq.build_field(0.1, 1.5, 6, 0.0)
+    s = uq.EnsembleSolver2D(f, cells, 1e-8, 400 if cells == 512 else 30000)
+    ys = np.random.default_rng(cells + G).uniform(-1, 1, (G, 32, 6))
+    ys[0, 1] = ys[0, 0]
+    r = s.solve_groups(ys)
+    out.append(np.concatenate([r.iterations.ravel().astype(float), r.qoi.ravel(),
+                               r.converged.ravel().astype(float),
+                               r.ensemble_iterations.astype(float)]))
+np.save(sys.argv[2], np.concatenate(out))
+"""
+
+
+def test_cluster_multicast_face_spmv_bitwise(tmp_path):
+    """UQG_FACE_CLUSTER=1 (thread-block clusters of two CTAs on adjacent chunks, band tiles
+    fetched once by TMA multicast, full / empty mbarriers across the CTAs) gives the plain
+    face kernel's bits for whole solves: n = 128 and n = 512 at S = 32 (chunks of m + 1 rows),
+    several groups and a single group, converged and maxit-limited."""
+    outs = {}
+    for k in ("0", "1"):
+        env = dict(os.environ, UQG_FACE_CLUSTER=k)
+        dst = tmp_path / f"c{k}.npy"
+        subprocess.run([sys.executable, "-c", _CLUSTER_SCRIPT, str(ROOT), str(dst)], env=env,
+                       check=True, timeout=900)
+        outs[k] = np.load(dst)
+    assert np.array_equal(outs["0"], outs["1"])
