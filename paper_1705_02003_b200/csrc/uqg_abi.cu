@@ -680,7 +680,14 @@ int pcg_impl(uqg_ctx* ctx, int N, int nnz, int max_row_len, int S, int G, const 
     Part& q = parts[i];
     q.g0 = (int)((long long)G * i / P);
     q.G = (int)((long long)G * (i + 1) / P) - q.g0;
-    q.s = i == 0 ? s : ctx->aux[i - 1];
+    // UQG_FACE_CLUSTER: the parts run one after the other on the caller's stream - the
+    // cluster SpMV needs whole SMs (two co-scheduled CTAs of 104 KB shared memory each), and
+    // kernels of another stream squeezed in between its clusters cost more than they fill
+    static const bool one_stream = [] {
+      const char* e = getenv("UQG_FACE_CLUSTER");
+      return e && atoi(e) != 0;
+    }();
+    q.s = (i == 0 || one_stream) ? s : ctx->aux[i - 1];
     q.done = false;
     pcg_layout(c, N, geo, q.G, &q.st, &q.r, &q.p, &q.ap, kx);
     q.st.iters = iters + (size_t)q.g0 * S;

@@ -929,17 +929,32 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, unsigned rank
   asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr)
                : "memory");
 }
+// CLUSTER: acquire at cluster scope (the producer's wait on the EMPTY barrier, which the
+// other CTA's warps signal); else CTA scope - enough for the FULL barrier, whose phase is
+// completed by the bulk copies' own complete_tx (a cluster-scope acquire costs an L1
+// invalidate, CCTL.IVALL, per wait: 22 % of the stall samples when the consumers used it)
+template <bool CLUSTER>
 __device__ __forceinline__ bool mbar_wait_bounded(uint64_t* bar, uint32_t parity) {
   const long long t0 = clock64();
   for (;;) {
     unsigned ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
+    if constexpr (CLUSTER) {
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+          "selp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(ok)
+          : "r"(smem_u32(bar)), "r"(parity)
+          : "memory");
+    } else {
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+          "selp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(ok)
+          : "r"(smem_u32(bar)), "r"(parity)
+          : "memory");
+    }
     if (ok) return true;
     if (clock64() - t0 > (1LL << 33)) return false;  // seconds: never hang
   }
@@ -1016,20 +1031,20 @@ __global__ void __launch_bounds__(kMcT + 32, 2) pcg_spmv_fv2d_mc_kernel(
         for (int tile = 0; tile < ct; ++tile, ++it) {
           if ((t & 31) == 0 && interior) {
             double* stage = stages + (size_t)s * kMcStage;
-            const long long r0 = c0 + (long long)tile * R;
+            const size_t o = (size_t)(c0 - 1) * S + (size_t)tile * (R * S);  // row r0 - 1
             constexpr uint32_t pb = (R + 2) * S * 8u, tb = (R + 1) * S * 8u;
-            if (it >= NST && !mbar_wait_bounded(&empty[s], ph ^ 1u)) ok = false;
+            const size_t nb = (size_t)crows * S;  // one chunk of rows
+            if (it >= NST && !mbar_wait_bounded<true>(&empty[s], ph ^ 1u)) ok = false;
             if (ok) {
               fence_proxy_async();
               mbar_expect_tx(&full[s], 3 * pb + 2 * tb);
-              bulk_g2s_mc(stage + pc_slot, pg + (r0 - 1) * S, pb, &full[s], (unsigned short)3);
-              bulk_g2s_mc(stage + tw_slot, txg + (r0 - 1) * S, tb, &full[s],
-                          (unsigned short)(c == 0 ? 1 : 3));
+              bulk_g2s_mc(stage + pc_slot, pg + o, pb, &full[s], (unsigned short)3);
+              bulk_g2s_mc(stage + tw_slot, txg + o, tb, &full[s], (unsigned short)(c == 0 ? 1 : 3));
               if (c == 0) {
-                bulk_g2s(stage + pw_slot, pg + (r0 - crows - 1) * S, pb, &full[s]);
+                bulk_g2s(stage + pw_slot, pg + o - nb, pb, &full[s]);
               } else {
-                bulk_g2s(stage + pe_slot, pg + (r0 + crows - 1) * S, pb, &full[s]);
-                bulk_g2s(stage + te_slot, txg + (r0 + crows - 1) * S, tb, &full[s]);
+                bulk_g2s(stage + pe_slot, pg + o + nb, pb, &full[s]);
+                bulk_g2s(stage + te_slot, txg + o + nb, tb, &full[s]);
               }
             }
           } else if ((t & 31) == 0) {
@@ -1041,7 +1056,7 @@ __global__ void __launch_bounds__(kMcT + 32, 2) pcg_spmv_fv2d_mc_kernel(
             const McSpan pE = mc_clip(r0 + crows - 1, R + 2, plim),
                          tE = mc_clip(r0 + crows - 1, R + 1, tlim);
             const uint32_t expect = (uint32_t)(pX.n + tX.n + pW.n + pE.n + tE.n) * S * 8u;
-            if (it >= NST && !mbar_wait_bounded(&empty[s], ph ^ 1u)) ok = false;
+            if (it >= NST && !mbar_wait_bounded<true>(&empty[s], ph ^ 1u)) ok = false;
             if (ok) {
               fence_proxy_async();
               if (expect) mbar_expect_tx(&full[s], expect);
@@ -1081,7 +1096,7 @@ __global__ void __launch_bounds__(kMcT + 32, 2) pcg_spmv_fv2d_mc_kernel(
         if (cend > N) cend = N;
         int i0 = (int)(row / m), j0 = (int)(row - (long long)i0 * m);
         for (int tile = 0; tile < ct; ++tile, ++it, row += R) {
-          if (!mbar_wait_bounded(&full[s], ph)) ok = false;
+          if (!mbar_wait_bounded<false>(&full[s], ph)) ok = false;
           ok = __all_sync(0xffffffffu, (int)ok) != 0;
           if (!ok) break;
           if (row < cend) {
